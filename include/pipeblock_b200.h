@@ -1,0 +1,187 @@
+/*
+ * pipeblock_b200.h — C-ABI boundary of the B200-native V-shape pipeline executor.
+ *
+ * The reference ("pipeblock", /root/reference/proj/include/pipeblock) is a C++
+ * schedule synthesizer.  Its front end (build_entry -> assemble -> GridSchedule,
+ * or parse(json) -> ScheduleDocument) stays the producer of the per-device op
+ * order.  This header is what that front end (or any FFI: ctypes, cgo, JNI)
+ * binds to hand a schedule to CUDA and get a measured TimedSchedule back — the
+ * real-hardware counterpart of simulate() (simulate.hpp:22).
+ *
+ * Conventions: plain C types only; devices and stages are 1-based exactly as in
+ * the reference; every function returns PB_OK (0) or a negative PB_E* code and
+ * sets a thread-local message readable with pb_last_error().  The caller owns
+ * every input array (the library copies what it keeps) and allocates every
+ * output array.
+ */
+#ifndef PIPEBLOCK_B200_H
+#define PIPEBLOCK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_ABI_VERSION 1
+
+enum {
+    PB_OK = 0,
+    PB_EINVAL = -1,   /* std::invalid_argument in the reference (model.hpp:223, assemble.hpp:86-89,206,408-414) */
+    PB_EDOC = -2,     /* DocumentError (document.hpp:13-16) */
+    PB_ECUDA = -3,    /* CUDA / driver failure, or no sm_100 device */
+    PB_ESPACE = -4,   /* caller-provided output buffer too small */
+    PB_ESTATE = -5    /* handle used out of order (e.g. step before connect) */
+};
+
+/* PassKind (model.hpp:15): F=0, B=1, W=2, BW=3 (fused backward, two cells). */
+enum { PB_F = 0, PB_B = 1, PB_W = 2, PB_BW = 3 };
+
+/* GridPass (model.hpp:162-176, ScheduledPassT<long long>). */
+typedef struct pb_pass {
+    int32_t device;
+    int32_t stage;
+    int32_t kind;
+    int32_t microbatch;
+    int64_t start;
+    int64_t duration;
+} pb_pass;
+
+/* TimedPass (model.hpp:176, ScheduledPassT<double>); times in milliseconds when
+ * produced by the executor, in profile units when produced by pb_simulate. */
+typedef struct pb_timed_pass {
+    int32_t device;
+    int32_t stage;
+    int32_t kind;
+    int32_t microbatch;
+    double start;
+    double duration;
+} pb_timed_pass;
+
+/* Topology (model.hpp:50-56), single default route 1..num_stages. */
+typedef struct pb_topology {
+    int32_t devices;
+    int32_t num_stages;
+    const int32_t* placement; /* num_stages entries, placement[s-1] = device of stage s */
+    const double* stage_mem;  /* num_stages entries; NULL = all 1.0 */
+} pb_topology;
+
+/* RunTimeProfile (model.hpp:189-206). */
+typedef struct pb_profile {
+    double f, b, w, comm;
+} pb_profile;
+
+/* SimResult scalars (simulate.hpp:9-17); per-device vectors go to caller arrays. */
+typedef struct pb_sim_stats {
+    double makespan;
+    double bubble_rate;
+} pb_sim_stats;
+
+const char* pb_last_error(void);
+int pb_abi_version(void);
+
+/* ------------------------------------------------------------------ schedules
+ * An immutable, validated GridSchedule.  Shareable across threads. */
+typedef struct pb_schedule pb_schedule;
+
+/* assemble(build_entry(entry, devices), microbatches, {squeeze, reorder})
+ *   replaces gallery.hpp:499 build_entry + assemble.hpp:405 assemble. */
+int pb_schedule_build(const char* entry, int32_t devices, int32_t microbatches, int32_t do_squeeze,
+                      int32_t do_reorder, pb_schedule** out);
+/* A caller-made GridSchedule (e.g. converted from pipeblock::GridSchedule);
+ * validated like validate_schedule (assemble.hpp:138-183). */
+int pb_schedule_create(const pb_topology* topo, const pb_pass* passes, size_t n, int32_t microbatches,
+                       pb_schedule** out);
+/* parse(text, strict) (document.hpp:192); units must be "cells". */
+int pb_schedule_parse(const char* json_text, int32_t strict, pb_schedule** out);
+/* emit(document) (document.hpp:188): writes up to cap bytes incl. NUL; *len = bytes needed excl. NUL. */
+int pb_schedule_emit(const pb_schedule* s, char* buf, size_t cap, size_t* len);
+int pb_schedule_info(const pb_schedule* s, int32_t* devices, int32_t* num_stages, int32_t* microbatches,
+                     size_t* num_passes);
+int pb_schedule_topology(const pb_schedule* s, int32_t* placement, double* stage_mem);
+/* Passes in canonical (device, start, stage, microbatch) order (assemble.hpp:50-57). */
+int pb_schedule_passes(const pb_schedule* s, pb_pass* out, size_t n);
+/* exact_peak (memory.hpp:63-91): one value per device. */
+int pb_schedule_exact_peak(const pb_schedule* s, double* per_device);
+/* simulate (simulate.hpp:22-86). out: n passes (canonical order) or NULL; per-device arrays may be NULL. */
+int pb_simulate(const pb_schedule* s, const pb_profile* prof, pb_timed_pass* out, size_t n, pb_sim_stats* stats,
+                double* busy, double* idle_total, double* idle_span, double* peak);
+/* The same accounting over measured passes (bubble = 1 - sum busy / (d * makespan), simulate.hpp:81-82). */
+int pb_account(const pb_topology* topo, const pb_timed_pass* passes, size_t n, pb_sim_stats* stats, double* busy,
+               double* peak);
+void pb_schedule_destroy(pb_schedule* s);
+
+/* ------------------------------------------------------------------ executor
+ * GPT-style decoder stack (pre-norm RMSNorm, causal MHA with head_dim 128,
+ * GELU MLP 4h, residual, untied embedding / LM head, mean cross-entropy),
+ * split into num_stages equal chunks of layers.  Stage 1 also holds the token
+ * embedding; the last stage holds the final norm, LM head and loss.  bf16
+ * weights/activations, fp32 accumulation, fp32 gradients, AdamW in fp32. */
+typedef struct pb_model_cfg {
+    int32_t layers;
+    int32_t hidden;
+    int32_t heads;
+    int32_t seq;
+    int32_t vocab;
+    int32_t micro_batch; /* sequences per microbatch */
+    uint64_t seed;
+    float lr, beta1, beta2, eps, weight_decay;
+    int32_t optimizer; /* 1 = AdamW step after the flush, 0 = gradients only */
+    int32_t flags;     /* PB_FLAG_* */
+} pb_model_cfg;
+
+#define PB_FLAG_SERIAL 1     /* device-synchronise after every pass (race check mode) */
+#define PB_FLAG_TIMELINE 2   /* record per-pass CUDA events (TimedSchedule output) */
+
+typedef struct pb_exec_stats {
+    double loss;            /* mean CE over all tokens of the step (last-stage device; NaN elsewhere) */
+    double step_ms;         /* this device: first pass start .. last pass end (CUDA events) */
+    double busy_ms;         /* this device: sum of pass durations */
+    int64_t pool_slots;     /* activation slots allocated = predicted exact_peak on this device */
+    int64_t pool_peak;      /* slots live at once, counted while running */
+    int64_t slot_bytes;     /* bytes per activation slot */
+    int64_t pool_bytes;     /* slot_bytes * pool_slots */
+    int64_t peer_bytes;     /* bytes pulled from peers during the step */
+    int64_t kernel_launches;/* kernels this device launched during the step */
+} pb_exec_stats;
+
+typedef struct pb_exec pb_exec;
+
+/* One pipeline device (1-based `device` of the schedule's topology) bound to
+ * CUDA ordinal `cuda_device`.  Allocates weights (seeded init), gradients,
+ * optimizer state and the lifespan-bounded activation pool. */
+int pb_exec_create(const pb_model_cfg* cfg, const pb_schedule* plan, int32_t device, int32_t cuda_device,
+                   pb_exec** out);
+/* Peer wiring.  Same process: pass the peer handles directly.  Separate
+ * processes: export an IPC blob, exchange blobs (e.g. torch.distributed
+ * all_gather_object), then connect with all devices' blobs in device order. */
+int pb_exec_connect_local(pb_exec* const* all_devices, int32_t n);
+int pb_exec_export(pb_exec* e, void* blob, size_t cap, size_t* len);
+int pb_exec_connect_ipc(pb_exec* e, const void* const* blobs, const size_t* lens, int32_t n);
+/* One training step: every pass of this device in grid order, then the
+ * optimizer.  tokens/labels: micro_batch*seq*microbatches int32 each,
+ * microbatch-major; host pointers when inputs_on_host != 0 (copied in on the
+ * compute stream inside the step), else device pointers.  Only stage-1's
+ * device reads tokens and only the last stage's device reads labels.
+ * timeline: NULL or an array of this device's pass count (canonical order). */
+int pb_exec_step(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32_t inputs_on_host,
+                 pb_timed_pass* timeline, size_t timeline_n, pb_exec_stats* stats);
+/* Enqueue-only variant for CUDA-event timing by the caller: no host sync. */
+int pb_exec_step_async(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32_t inputs_on_host);
+int pb_exec_sync(pb_exec* e, pb_timed_pass* timeline, size_t timeline_n, pb_exec_stats* stats);
+int pb_exec_num_passes(const pb_exec* e, size_t* n);
+void* pb_exec_stream(pb_exec* e); /* cudaStream_t of the compute stream */
+/* Parameter access for parity tests: tensors are enumerated per stage owned
+ * by this device; names like "s3.l1.wqkv", "s1.emb", "s8.head", "s8.norm". */
+int pb_exec_param_count(const pb_exec* e, int32_t* n);
+int pb_exec_param_info(const pb_exec* e, int32_t i, char* name, size_t cap, int64_t* numel);
+int pb_exec_param_get(pb_exec* e, int32_t i, int32_t which /*0 weight bf16->f32, 1 grad f32*/, float* host);
+int pb_exec_param_set(pb_exec* e, int32_t i, const float* host); /* rounds to bf16, sets fp32 master */
+int pb_exec_zero_grads(pb_exec* e);
+void pb_exec_destroy(pb_exec* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPEBLOCK_B200_H */

@@ -1,0 +1,10 @@
+"""B200-native executor for the V-shape building-block pipeline schedules of
+arXiv 2405.15362 (V-Min, V-Half, V-ZB; 1F1B and ZB-H1 as baselines).
+
+Layers:
+  pipeblock  — the reference's schedule API (build_entry/assemble/simulate/parse/emit)
+  executor   — runs a GridSchedule on B200s through the C-ABI (include/pipeblock_b200.h)
+"""
+from . import pipeblock  # noqa: F401
+
+__all__ = ["pipeblock"]

@@ -1,0 +1,192 @@
+// C-ABI for the schedule front end (include/pipeblock_b200.h, "schedules").
+#include <cstring>
+#include <string>
+
+#include "capi_common.hpp"
+#include "schedule/vsched.hpp"
+
+using namespace vsched;
+
+struct pb_schedule {
+    Grid grid;
+    Document doc;  // what emit() writes (carries source block / steps when built here)
+};
+
+namespace pbx {
+thread_local std::string g_err;
+}
+
+extern "C" const char* pb_last_error(void) { return pbx::g_err.c_str(); }
+extern "C" int pb_abi_version(void) { return PB_ABI_VERSION; }
+
+namespace {
+
+Topology topo_from_c(const pb_topology* t) {
+    if (!t || t->devices < 1 || t->num_stages < 1 || !t->placement) throw std::invalid_argument("bad topology");
+    Topology o;
+    o.devices = t->devices;
+    o.num_stages = t->num_stages;
+    for (int s = 0; s < t->num_stages; ++s) {
+        if (t->placement[s] < 1 || t->placement[s] > t->devices)
+            throw std::invalid_argument("placement device out of range");
+        o.placement.push_back(t->placement[s]);
+        o.stage_mem.push_back(t->stage_mem ? t->stage_mem[s] : 1.0);
+    }
+    o.routes = {Topology::iota(1, o.num_stages)};
+    return o;
+}
+
+pb_schedule* finish(Grid g, Document d) {
+    auto probs = validate_schedule(g);
+    if (!probs.empty()) throw std::invalid_argument(probs.front());
+    auto* s = new pb_schedule;
+    s->grid = std::move(g);
+    s->doc = std::move(d);
+    return s;
+}
+
+}  // namespace
+
+extern "C" int pb_schedule_build(const char* entry, int32_t devices, int32_t microbatches, int32_t sq, int32_t re,
+                                 pb_schedule** out) {
+    return pbx::guard([&] {
+        if (!entry || !out) throw std::invalid_argument("null argument");
+        Build b = build_entry(entry, devices);
+        Grid g = assemble(b, microbatches, sq != 0, re != 0);
+        Document d = document_for_assembly(b, g, sq != 0, re != 0);
+        *out = finish(std::move(g), std::move(d));
+    });
+}
+
+extern "C" int pb_schedule_create(const pb_topology* topo, const pb_pass* passes, size_t n, int32_t microbatches,
+                                  pb_schedule** out) {
+    return pbx::guard([&] {
+        if (!out || (n && !passes)) throw std::invalid_argument("null argument");
+        Grid g;
+        g.topo = topo_from_c(topo);
+        g.microbatches = microbatches;
+        for (size_t i = 0; i < n; ++i) {
+            const pb_pass& p = passes[i];
+            if (p.kind < 0 || p.kind > 3) throw std::invalid_argument("kind must be 0..3");
+            if (p.stage < 1 || p.stage > g.topo.num_stages) throw std::invalid_argument("stage out of range");
+            if (p.microbatch < 0 || p.microbatch >= microbatches) throw std::invalid_argument("microbatch out of range");
+            g.ops.push_back({p.device, p.stage, Kind(p.kind), p.microbatch, p.start, p.duration});
+        }
+        sort_canonical(g);
+        Document d;
+        d.topo = g.topo;
+        d.microbatches = microbatches;
+        d.grid = g;
+        *out = finish(std::move(g), std::move(d));
+    });
+}
+
+extern "C" int pb_schedule_parse(const char* text, int32_t strict, pb_schedule** out) {
+    return pbx::guard([&] {
+        if (!text || !out) throw std::invalid_argument("null argument");
+        Document d = parse_document(text, strict != 0);
+        if (!d.is_grid()) throw std::invalid_argument("executor needs a 'cells' document, got units 'time'");
+        Grid g = d.grid;
+        sort_canonical(g);
+        *out = finish(std::move(g), std::move(d));
+    });
+}
+
+extern "C" int pb_schedule_emit(const pb_schedule* s, char* buf, size_t cap, size_t* len) {
+    return pbx::guard([&] {
+        if (!s) throw std::invalid_argument("null schedule");
+        std::string t = emit_document(s->doc);
+        if (len) *len = t.size();
+        if (!buf) return;
+        if (cap < t.size() + 1) throw pbx::Space("emit buffer too small");
+        std::memcpy(buf, t.c_str(), t.size() + 1);
+    });
+}
+
+extern "C" int pb_schedule_info(const pb_schedule* s, int32_t* devices, int32_t* stages, int32_t* mbs, size_t* n) {
+    return pbx::guard([&] {
+        if (!s) throw std::invalid_argument("null schedule");
+        if (devices) *devices = s->grid.topo.devices;
+        if (stages) *stages = s->grid.topo.num_stages;
+        if (mbs) *mbs = s->grid.microbatches;
+        if (n) *n = s->grid.ops.size();
+    });
+}
+
+extern "C" int pb_schedule_topology(const pb_schedule* s, int32_t* placement, double* stage_mem) {
+    return pbx::guard([&] {
+        if (!s) throw std::invalid_argument("null schedule");
+        for (int i = 0; i < s->grid.topo.num_stages; ++i) {
+            if (placement) placement[i] = s->grid.topo.placement[i];
+            if (stage_mem) stage_mem[i] = s->grid.topo.stage_mem[i];
+        }
+    });
+}
+
+extern "C" int pb_schedule_passes(const pb_schedule* s, pb_pass* out, size_t n) {
+    return pbx::guard([&] {
+        if (!s || !out) throw std::invalid_argument("null argument");
+        if (n < s->grid.ops.size()) throw pbx::Space("pass buffer too small");
+        for (size_t i = 0; i < s->grid.ops.size(); ++i) {
+            const auto& o = s->grid.ops[i];
+            out[i] = {o.device, o.stage, int32_t(o.kind), o.mb, o.start, o.dur};
+        }
+    });
+}
+
+extern "C" int pb_schedule_exact_peak(const pb_schedule* s, double* per_device) {
+    return pbx::guard([&] {
+        if (!s || !per_device) throw std::invalid_argument("null argument");
+        auto p = exact_peak(s->grid);
+        std::memcpy(per_device, p.data(), p.size() * sizeof(double));
+    });
+}
+
+static void fill_stats(const SimResult& r, pb_timed_pass* out, size_t n, pb_sim_stats* st, double* busy, double* idle_t,
+                       double* idle_s, double* peak) {
+    if (out) {
+        if (n < r.schedule.ops.size()) throw pbx::Space("timed buffer too small");
+        for (size_t i = 0; i < r.schedule.ops.size(); ++i) {
+            const auto& o = r.schedule.ops[i];
+            out[i] = {o.device, o.stage, int32_t(o.kind), o.mb, o.start, o.dur};
+        }
+    }
+    if (st) *st = {r.makespan, r.bubble_rate};
+    for (size_t k = 0; k < r.busy.size(); ++k) {
+        if (busy) busy[k] = r.busy[k];
+        if (idle_t) idle_t[k] = r.idle_total[k];
+        if (idle_s) idle_s[k] = r.idle_span[k];
+        if (peak) peak[k] = r.peak[k];
+    }
+}
+
+extern "C" int pb_simulate(const pb_schedule* s, const pb_profile* prof, pb_timed_pass* out, size_t n,
+                           pb_sim_stats* st, double* busy, double* idle_t, double* idle_s, double* peak) {
+    return pbx::guard([&] {
+        if (!s || !prof) throw std::invalid_argument("null argument");
+        SimResult r = simulate(s->grid, Profile{prof->f, prof->b, prof->w, prof->comm});
+        fill_stats(r, out, n, st, busy, idle_t, idle_s, peak);
+    });
+}
+
+extern "C" int pb_account(const pb_topology* topo, const pb_timed_pass* passes, size_t n, pb_sim_stats* st,
+                          double* busy, double* peak) {
+    return pbx::guard([&] {
+        Timed t;
+        t.topo = topo_from_c(topo);
+        for (size_t i = 0; i < n; ++i) {
+            const auto& p = passes[i];
+            if (p.device < 1 || p.device > t.topo.devices) throw std::invalid_argument("device out of range");
+            t.ops.push_back({p.device, p.stage, Kind(p.kind & 3), p.microbatch, p.start, p.duration});
+        }
+        SimResult r = account(t);
+        fill_stats(r, nullptr, 0, st, busy, nullptr, nullptr, peak);
+    });
+}
+
+extern "C" void pb_schedule_destroy(pb_schedule* s) { delete s; }
+
+// schedule access for the executor (same library)
+namespace pbx {
+const Grid& schedule_grid(const pb_schedule* s) { return s->grid; }
+}  // namespace pbx
