@@ -1,0 +1,38 @@
+// Host interface of the sm_100a kernels (kernels/*.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pbk {
+
+enum Epi : int {
+    EPI_STORE = 0,  // C(bf16) = acc
+    EPI_GELU = 1,   // C(bf16) = acc (pre-activation u), C2(bf16) = gelu(u)
+    EPI_RESID = 2,  // C(bf16) = acc + aux(bf16)      (residual add; C may alias aux)
+    EPI_DGELU = 3,  // C(bf16) = acc * gelu'(aux)     (aux = pre-activation u)
+    EPI_F32 = 4,    // C(f32) (+)= acc                (weight gradients, accumulate flag)
+};
+
+struct GemmArgs {
+    int M = 0, N = 0, K = 0;
+    const __nv_bfloat16* A = nullptr;
+    int lda = 0;
+    bool a_mn = false;  // A stored [K][M] (else [M][K])
+    const __nv_bfloat16* B = nullptr;
+    int ldb = 0;
+    bool b_mn = false;  // B stored [K][N] (else [N][K])
+    void* C = nullptr;
+    int ldc = 0;
+    void* C2 = nullptr;
+    const __nv_bfloat16* aux = nullptr;
+    int ldaux = 0;
+    int epi = EPI_STORE;
+    int accumulate = 0;
+};
+
+void gemm(const GemmArgs& g, cudaStream_t s);
+int gemm_bn(const GemmArgs& g);
+int num_sms();
+
+}  // namespace pbk

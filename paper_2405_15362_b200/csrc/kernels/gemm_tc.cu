@@ -1,0 +1,331 @@
+// Persistent warp-specialised bf16 GEMM on 5th-gen tensor cores (sm_100a).
+//
+//   C[M,N] (op)= A[M,K] * B[K,N]     fp32 accumulate in TMEM
+//
+// One CTA per SM, 192 threads:
+//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (mbarrier full/empty)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+// Two TMEM accumulators (2 x BN fp32 columns) let the epilogue of tile i
+// overlap the mainloop of tile i+1.
+//
+// Operand majors cover the three pass shapes of a pipeline stage without any
+// transposes in HBM:
+//   F  Y  = X  . W^T   A=[M][K] (K-major)   B=[N][K] (K-major)
+//   B  dX = dY . W     A=[M][K] (K-major)   B=[K][N] (MN-major)
+//   W  dW += dY^T . X  A=[K][M] (MN-major)  B=[K][N] (MN-major)
+#include <cudaTypedefs.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "gemm.hpp"
+#include "sm100.cuh"
+
+namespace pbk {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct KParams {
+    int M, N, K;
+    void* C;
+    void* C2;
+    const __nv_bfloat16* aux;
+    int ldc, ldaux;
+    int accumulate;
+};
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, KParams p) {
+    using C_ = Cfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::kStages * C_::kStageBytes);
+    uint64_t* empty = full + C_::kStages;
+    uint64_t* tfull = empty + C_::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id();
+    const int num_m = p.M / BM, num_n = p.N / BN;
+    const int num_tiles = num_m * num_n;
+    const int num_k = p.K / BK;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tma_a);
+        tma_prefetch(&tma_b);
+        for (int s = 0; s < C_::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<C_::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], C_::kStageBytes);
+                    uint8_t* sa = smem + stage * C_::kStageBytes;
+                    uint8_t* sb = sa + C_::kABytes;
+                    const int k0 = kb * BK;
+                    if constexpr (A_MN) {  // [K][M]: boxes of 64 M x 64 K
+                        tma_load_2d(sa, &tma_a, &full[stage], m0, k0);
+                        tma_load_2d(sa + 8192, &tma_a, &full[stage], m0 + 64, k0);
+                    } else {  // [M][K]: one box 64 K x 128 rows
+                        tma_load_2d(sa, &tma_a, &full[stage], k0, m0);
+                    }
+                    if constexpr (B_MN) {  // [K][N]: BN/64 boxes of 64 N x 64 K
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
+                    } else {  // [N][K]
+                        tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
+                    }
+                    if (++stage == C_::kStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_k; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t sa = smem_u32(smem + stage * C_::kStageBytes);
+                    const uint32_t sb = sa + C_::kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
+                        tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
+                    if (kb == num_k - 1) tc_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == C_::kStages) stage = 0, phase ^= 1;
+            }
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_in_tile = int(q * 32 + lane_id());
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = m0 + row_in_tile;
+            const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                tmem_ld32(tbase + c, v);
+                tmem_ld_wait();
+                const int col = n0 + c;
+                if constexpr (EPI == EPI_F32) {
+                    float* dst = reinterpret_cast<float*>(p.C) + size_t(row) * p.ldc + col;
+                    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        if (p.accumulate) {
+                            float4 old = d4[j];
+                            o.x += old.x, o.y += old.y, o.z += old.z, o.w += old.w;
+                        }
+                        d4[j] = o;
+                    }
+                } else {
+                    if constexpr (EPI == EPI_RESID || EPI == EPI_DGELU) {
+                        const uint4* s4 = reinterpret_cast<const uint4*>(p.aux + size_t(row) * p.ldaux + col);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 a = s4[j];
+                            uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                float lo = bf16_lo(w[e]), hi = bf16_hi(w[e]);
+                                if constexpr (EPI == EPI_RESID) {
+                                    v[8 * j + 2 * e] += lo;
+                                    v[8 * j + 2 * e + 1] += hi;
+                                } else {
+                                    v[8 * j + 2 * e] *= gelu_grad(lo);
+                                    v[8 * j + 2 * e + 1] *= gelu_grad(hi);
+                                }
+                            }
+                        }
+                    }
+                    uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + size_t(row) * p.ldc + col);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        d4[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                           pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                    if constexpr (EPI == EPI_GELU) {
+                        // activation from the bf16-rounded pre-activation, as the backward sees it
+                        uint4* g4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C2) + size_t(row) * p.ldc + col);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            float g[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                g[e] = gelu_f(__bfloat162float(__float2bfloat16_rn(v[8 * j + e])));
+                            g4[j] = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]),
+                                               pack_bf16(g[6], g[7]));
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<C_::kTmemCols>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+            throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// 2-D bf16 tensor [outer][inner] with row stride `ld` elements; box = box_inner x box_outer; 128B swizzle.
+CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                     uint32_t box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void launch(const GemmArgs& g, cudaStream_t s) {
+    using C_ = Cfg<BN>;
+    static bool attr = [] {
+        cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+        return true;
+    }();
+    (void)attr;
+    CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
+    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, BN);
+    KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate};
+    const int tiles = (g.M / BM) * (g.N / BN);
+    const int grid = tiles < sm_count() ? tiles : sm_count();
+    gemm_kernel<BN, A_MN, B_MN, EPI><<<grid, kThreads, C_::kSmem, s>>>(ta, tb, kp);
+}
+
+template <int BN>
+void dispatch(const GemmArgs& g, cudaStream_t s) {
+    if (!g.a_mn && !g.b_mn) {
+        switch (g.epi) {
+            case EPI_STORE: return launch<BN, false, false, EPI_STORE>(g, s);
+            case EPI_GELU: return launch<BN, false, false, EPI_GELU>(g, s);
+            case EPI_RESID: return launch<BN, false, false, EPI_RESID>(g, s);
+            case EPI_F32: return launch<BN, false, false, EPI_F32>(g, s);
+            default: break;
+        }
+    } else if (!g.a_mn && g.b_mn) {
+        switch (g.epi) {
+            case EPI_STORE: return launch<BN, false, true, EPI_STORE>(g, s);
+            case EPI_DGELU: return launch<BN, false, true, EPI_DGELU>(g, s);
+            case EPI_RESID: return launch<BN, false, true, EPI_RESID>(g, s);
+            case EPI_F32: return launch<BN, false, true, EPI_F32>(g, s);
+            default: break;
+        }
+    } else if (g.a_mn && g.b_mn) {
+        if (g.epi == EPI_F32) return launch<BN, true, true, EPI_F32>(g, s);
+        if (g.epi == EPI_STORE) return launch<BN, true, true, EPI_STORE>(g, s);
+    } else {
+        if (g.epi == EPI_F32) return launch<BN, true, false, EPI_F32>(g, s);
+        if (g.epi == EPI_STORE) return launch<BN, true, false, EPI_STORE>(g, s);
+    }
+    throw std::invalid_argument("gemm: unsupported operand-major / epilogue combination");
+}
+
+}  // namespace
+
+int num_sms() { return sm_count(); }
+
+int gemm_bn(const GemmArgs& g) {
+    const int tiles256 = (g.N % 256 == 0) ? (g.M / BM) * (g.N / 256) : 0;
+    return (tiles256 >= num_sms()) ? 256 : 128;
+}
+
+void gemm(const GemmArgs& g, cudaStream_t s) {
+    if (g.M % BM || g.N % 128 || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
+        throw std::invalid_argument("gemm: M%128, N%128, K%64 must be 0 (M=" + std::to_string(g.M) +
+                                    " N=" + std::to_string(g.N) + " K=" + std::to_string(g.K) + ")");
+    if (gemm_bn(g) == 256)
+        dispatch<256>(g, s);
+    else
+        dispatch<128>(g, s);
+}
+
+}  // namespace pbk

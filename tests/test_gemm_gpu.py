@@ -1,0 +1,91 @@
+"""tcgen05 GEMM vs torch fp32 on the same bf16 inputs (all three pass shapes)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from tests import kernels as K  # noqa: E402
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+def gelu(x):
+    return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+SHAPES = [(128, 128, 64), (256, 384, 128), (512, 1024, 512), (2048, 6144, 2048), (384, 2304, 768)]
+
+
+@pytest.mark.parametrize("M,N,Kd", SHAPES)
+def test_forward_shape(M, N, Kd):
+    g = torch.Generator(device="cuda").manual_seed(M + N + Kd)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(A, W, C)
+    torch.cuda.synchronize()
+    ref = A.float() @ W.float().t()
+    assert rel(C, ref) < 4e-3
+
+
+@pytest.mark.parametrize("M,N,Kd", SHAPES)
+def test_backward_shape(M, N, Kd):
+    # dX[M,N] = dY[M,K] . W[K,N]  with W stored [K][N] (MN-major B)
+    g = torch.Generator(device="cuda").manual_seed(7 + M)
+    dY = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Kd, N, device="cuda", generator=g).bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(dY, W, C, b_mn=True)
+    torch.cuda.synchronize()
+    assert rel(C, dY.float() @ W.float()) < 4e-3
+
+
+@pytest.mark.parametrize("M,N,Kd", SHAPES)
+def test_weight_shape_accumulate(M, N, Kd):
+    # dW[M,N] += dY^T . X with dY stored [K][M], X stored [K][N]
+    g = torch.Generator(device="cuda").manual_seed(11 + N)
+    dY = torch.randn(Kd, M, device="cuda", generator=g).bfloat16()
+    X = torch.randn(Kd, N, device="cuda", generator=g).bfloat16()
+    C = torch.randn(M, N, device="cuda", generator=g)
+    C0 = C.clone()
+    K.gemm(dY, X, C, a_mn=True, b_mn=True, epi=4, accumulate=1)
+    torch.cuda.synchronize()
+    assert rel(C, C0 + dY.float().t() @ X.float()) < 1e-4 * max(1.0, Kd / 64)
+    K.gemm(dY, X, C, a_mn=True, b_mn=True, epi=4, accumulate=0)
+    torch.cuda.synchronize()
+    assert rel(C, dY.float().t() @ X.float()) < 1e-5
+
+
+def test_fused_epilogues():
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M, N, Kd = 256, 512, 256
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16() * 0.1
+    u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    gg = torch.empty_like(u)
+    K.gemm(A, W, u, epi=1, C2=gg)
+    R = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    out = torch.empty_like(u)
+    K.gemm(A, W, out, epi=2, aux=R)
+    Wt = torch.randn(Kd, N, device="cuda", generator=g).bfloat16() * 0.1
+    dg = torch.empty_like(u)
+    K.gemm(A, Wt, dg, b_mn=True, epi=3, aux=u)
+    torch.cuda.synchronize()
+    ref_u = A.float() @ W.float().t()
+    assert rel(u, ref_u) < 4e-3
+    assert rel(gg, gelu(u.float())) < 4e-3
+    assert rel(out, ref_u + R.float()) < 4e-3
+    x = u.float().requires_grad_(True)
+    (gl,) = torch.autograd.grad(gelu(x), x, torch.ones_like(x))
+    assert rel(dg, (A.float() @ Wt.float()) * gl) < 5e-3
+
+
+def test_rejects_bad_shapes():
+    A = torch.zeros(100, 64, device="cuda", dtype=torch.bfloat16)
+    W = torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16)
+    C = torch.zeros(100, 128, device="cuda", dtype=torch.bfloat16)
+    from paper_2405_15362_b200._lib import ScheduleError
+    with pytest.raises(ScheduleError):
+        K.gemm(A, W, C)
