@@ -19,6 +19,21 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
              int32_t b_mn, void* C, int32_t ldc, void* C2, const void* aux, int32_t ldaux, int32_t epi,
              int32_t accumulate, void* stream);
 
+/* causal attention, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T] (base-2 LSE of scaled scores) */
+int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
+/* dqkv [T,3h]; dsum [heads,T], dq_acc [T,h] fp32 scratch */
+int pbt_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum, float* dq_acc,
+                 void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream);
+int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h, void* stream);
+int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
+                    float* dgamma, int32_t T, int32_t h, void* stream);
+int pbt_embed_fwd(const int32_t* tok, const void* emb, void* x, int32_t T, int32_t h, void* stream);
+int pbt_embed_bwd(const int32_t* tok, const void* dx, float* demb, int32_t T, int32_t h, void* stream);
+int pbt_cross_entropy(void* logits, const int32_t* labels, float* loss, int32_t T, int32_t V, float scale,
+                      void* stream);
+int pbt_adamw(float* w, void* wb, float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+              float wd, int32_t step, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

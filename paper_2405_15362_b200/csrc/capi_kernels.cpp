@@ -27,3 +27,63 @@ extern "C" int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t 
         cuda_check("pbt_gemm");
     });
 }
+
+#define BF(p) static_cast<const __nv_bfloat16*>(p)
+#define BFM(p) static_cast<__nv_bfloat16*>(p)
+#define ST(s) static_cast<cudaStream_t>(s)
+
+extern "C" int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads,
+                            void* stream) {
+    return pbx::guard([&] {
+        pbk::attn_fwd(BF(qkv), BFM(out), lse2, batch, seq, heads, ST(stream));
+        cuda_check("pbt_attn_fwd");
+    });
+}
+extern "C" int pbt_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum,
+                            float* dq_acc, void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream) {
+    return pbx::guard([&] {
+        pbk::attn_bwd(BF(qkv), BF(out), BF(dout), lse2, dsum, dq_acc, BFM(dqkv), batch, seq, heads, ST(stream));
+        cuda_check("pbt_attn_bwd");
+    });
+}
+extern "C" int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h,
+                               void* stream) {
+    return pbx::guard([&] {
+        pbk::rmsnorm_fwd(BF(x), BF(g), BFM(y), rstd, T, h, ST(stream));
+        cuda_check("pbt_rmsnorm_fwd");
+    });
+}
+extern "C" int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, const float* rstd, const void* dres,
+                               void* dx, float* dgamma, int32_t T, int32_t h, void* stream) {
+    return pbx::guard([&] {
+        pbk::rmsnorm_bwd(BF(dy), BF(x), BF(g), rstd, BF(dres), BFM(dx), T, h, ST(stream));
+        if (dgamma) pbk::rmsnorm_dgamma(BF(dy), BF(x), rstd, dgamma, T, h, ST(stream));
+        cuda_check("pbt_rmsnorm_bwd");
+    });
+}
+extern "C" int pbt_embed_fwd(const int32_t* tok, const void* emb, void* x, int32_t T, int32_t h, void* stream) {
+    return pbx::guard([&] {
+        pbk::embed_fwd(tok, BF(emb), BFM(x), T, h, ST(stream));
+        cuda_check("pbt_embed_fwd");
+    });
+}
+extern "C" int pbt_embed_bwd(const int32_t* tok, const void* dx, float* demb, int32_t T, int32_t h, void* stream) {
+    return pbx::guard([&] {
+        pbk::embed_bwd(tok, BF(dx), demb, T, h, ST(stream));
+        cuda_check("pbt_embed_bwd");
+    });
+}
+extern "C" int pbt_cross_entropy(void* logits, const int32_t* labels, float* loss, int32_t T, int32_t V, float scale,
+                                 void* stream) {
+    return pbx::guard([&] {
+        pbk::cross_entropy(BFM(logits), labels, loss, T, V, scale, ST(stream));
+        cuda_check("pbt_cross_entropy");
+    });
+}
+extern "C" int pbt_adamw(float* w, void* wb, float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                         float eps, float wd, int32_t step, void* stream) {
+    return pbx::guard([&] {
+        pbk::adamw(w, BFM(wb), g, m, v, size_t(n), lr, b1, b2, eps, wd, step, ST(stream));
+        cuda_check("pbt_adamw");
+    });
+}

@@ -1,0 +1,562 @@
+// One pipeline device: weights of the stages it owns, the lifespan-bounded
+// activation pool, the outbox ring for stage-boundary messages, and the
+// per-pass kernel chains.  The host walks this device's passes in grid order
+// and only ENQUEUES: every cross-device dependency is a device-side wait, so
+// the host runs ahead and the GPU starts each pass as soon as its inputs land.
+//
+// Transport (neighbour pull over NVLink):
+//   producer: last kernel writes the boundary tensor into its outbox slot k,
+//             then cuStreamWriteValue32(consumer.ready[src][k] = gen)
+//   consumer: copy stream waits ready >= gen, cudaMemcpyAsync peer->local
+//             (copy engines, no SM time), writes producer.ack[k] = gen, and the
+//             compute stream waits on that copy only when the pass starts
+//   producer: before reusing outbox slot k waits ack[k] >= previous gen
+// Outbox slots are interval-coloured over [producer start, consumer start) in
+// grid time, and grid start order is a global topological order
+// (assemble.hpp:185-187), so every wait points strictly back in grid time:
+// deadlock-free by induction over cells.
+#include "executor.hpp"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+namespace pbx {
+
+using vsched::Kind;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DriverFns {
+    PFN_cuStreamWaitValue32_v11070 wait = nullptr;
+    PFN_cuStreamWriteValue32_v11070 write = nullptr;
+};
+const DriverFns& drv() {
+    static DriverFns f = [] {
+        DriverFns d;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            throw CudaError("cuStreamWaitValue32 unavailable");
+        d.wait = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            throw CudaError("cuStreamWriteValue32 unavailable");
+        d.write = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+        return d;
+    }();
+    return f;
+}
+
+void wait_value(cudaStream_t s, const uint32_t* addr, uint32_t v) {
+    CUresult r = drv().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed: " + std::to_string(int(r)));
+}
+void write_value(cudaStream_t s, uint32_t* addr, uint32_t v) {
+    CUresult r = drv().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                             CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed: " + std::to_string(int(r)));
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ layout
+void Exec::build_layout() {
+    const size_t Th = size_t(T) * h;
+    auto add = [](size_t& cur, size_t bytes) {
+        size_t o = cur;
+        cur = align_up(cur + bytes, 1024);
+        return o;
+    };
+    slot_bytes = 0;
+    for (int s : stages) {
+        StageLayout L;
+        size_t cur = 0;
+        L.x.resize(size_t(Lc) + 1);
+        L.dx.resize(size_t(Lc) + 1);
+        for (int l = 0; l <= Lc; ++l) {
+            L.x[l] = add(cur, Th * 2);
+            L.dx[l] = add(cur, Th * 2);
+        }
+        L.layer.resize(Lc);
+        for (int l = 0; l < Lc; ++l) {
+            auto& y = L.layer[l];
+            y.a = add(cur, Th * 2);
+            y.qkv = add(cur, 3 * Th * 2);
+            y.o = add(cur, Th * 2);
+            y.x1 = add(cur, Th * 2);
+            y.b = add(cur, Th * 2);
+            y.u = add(cur, 4 * Th * 2);
+            y.gl = add(cur, 4 * Th * 2);
+            y.dqkv = add(cur, 3 * Th * 2);
+            y.dx1 = add(cur, Th * 2);
+            y.rstd1 = add(cur, size_t(T) * 4);
+            y.rstd2 = add(cur, size_t(T) * 4);
+            y.lse = add(cur, size_t(H) * T * 4);
+        }
+        if (s == S) {
+            L.hf = add(cur, Th * 2);
+            L.rstdf = add(cur, size_t(T) * 4);
+            L.logits = add(cur, size_t(T) * V * 2);
+        }
+        L.bytes = cur;
+        layout[s] = L;
+        slot_bytes = std::max(slot_bytes, cur);
+    }
+}
+
+// ------------------------------------------------------------------ params
+void Exec::build_params() {
+    size_t off = 0;
+    auto add = [&](const std::string& name, size_t numel, int id, float std, float constant) {
+        PTensor t{name, off, numel, id, std, constant};
+        off += align_up(numel, 64);
+        ptensors.push_back(t);
+        return ptensors.size() - 1;
+    };
+    const float std_in = 0.02f, std_out = 0.02f / std::sqrt(2.f * cfg.layers);
+    for (int s : stages) {
+        StageParams sp;
+        if (s == 1) sp.emb = add("s1.emb", size_t(V) * h, 1, std_in, 0.f);
+        for (int l = 0; l < Lc; ++l) {
+            const int gl = (s - 1) * Lc + l;
+            const std::string pre = "s" + std::to_string(s) + ".l" + std::to_string(l) + ".";
+            LayerParams lp;
+            lp.g1 = add(pre + "norm1", h, 16 + gl * 8 + 0, 0.f, 1.f);
+            lp.wqkv = add(pre + "wqkv", size_t(3) * h * h, 16 + gl * 8 + 1, std_in, 0.f);
+            lp.wo = add(pre + "wo", size_t(h) * h, 16 + gl * 8 + 2, std_out, 0.f);
+            lp.g2 = add(pre + "norm2", h, 16 + gl * 8 + 3, 0.f, 1.f);
+            lp.w1 = add(pre + "w1", size_t(4) * h * h, 16 + gl * 8 + 4, std_in, 0.f);
+            lp.w2 = add(pre + "w2", size_t(4) * h * h, 16 + gl * 8 + 5, std_out, 0.f);
+            sp.layers.push_back(lp);
+        }
+        if (s == S) {
+            sp.gf = add("s" + std::to_string(s) + ".norm", h, 2, 0.f, 1.f);
+            sp.head = add("s" + std::to_string(s) + ".head", size_t(V) * h, 3, std_in, 0.f);
+        }
+        sparams[s] = sp;
+    }
+    n_params = off;
+}
+
+Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda_dev)
+    : cfg(c), plan(make_plan(grid)), dev(device), cuda(cuda_dev) {
+    if (device < 1 || device > plan.topo.devices) throw std::invalid_argument("device out of range");
+    S = plan.topo.num_stages;
+    if (cfg.layers % S) throw std::invalid_argument("layers must be a multiple of the stage count");
+    Lc = cfg.layers / S;
+    h = cfg.hidden;
+    H = cfg.heads;
+    V = cfg.vocab;
+    seq = cfg.seq;
+    mbs = cfg.micro_batch;
+    T = seq * mbs;
+    if (H * 128 != h) throw std::invalid_argument("hidden must equal heads * 128");
+    if (seq % 128 || h % 128 || V % 128) throw std::invalid_argument("seq, hidden, vocab must be multiples of 128");
+    for (int s = 1; s <= S; ++s)
+        if (plan.topo.device_of(s) == dev) stages.push_back(s);
+    m = plan.microbatches;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw CudaError("no CUDA device available (the executor has no CPU fallback)");
+    }
+    if (cuda < 0 || cuda >= ndev) throw CudaError("cuda device ordinal out of range");
+    ck(cudaSetDevice(cuda), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, cuda), "cudaGetDeviceProperties");
+    if (prop.major != 10) throw CudaError("executor kernels are built for sm_100a; device is sm_" +
+                                          std::to_string(prop.major * 10 + prop.minor));
+    drv();
+
+    build_layout();
+    build_params();
+    ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking), "stream");
+
+    auto dmalloc = [&](size_t bytes, const char* what) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(bytes, 256)), what);
+        allocations.push_back(p);
+        return p;
+    };
+    master = static_cast<float*>(dmalloc(n_params * 4, "params"));
+    wts = static_cast<__nv_bfloat16*>(dmalloc(n_params * 2, "params"));
+    grads = static_cast<float*>(dmalloc(n_params * 4, "grads"));
+    adam_m = static_cast<float*>(dmalloc(n_params * 4, "adam"));
+    adam_v = static_cast<float*>(dmalloc(n_params * 4, "adam"));
+    ck(cudaMemsetAsync(grads, 0, n_params * 4, cs), "memset");
+    ck(cudaMemsetAsync(adam_m, 0, n_params * 4, cs), "memset");
+    ck(cudaMemsetAsync(adam_v, 0, n_params * 4, cs), "memset");
+    ck(cudaMemsetAsync(master, 0, n_params * 4, cs), "memset");
+    for (const auto& t : ptensors)
+        pbk::init_normal(master + t.off, t.numel, cfg.seed * 1000003ull + uint64_t(t.id), t.std, t.constant, cs);
+    pbk::f32_to_bf16(master, wts, n_params, cs);
+
+    nslots = plan.slots[dev];
+    pool = static_cast<uint8_t*>(dmalloc(slot_bytes * size_t(std::max(nslots, 1)), "activation pool"));
+    msg_bytes = align_up(size_t(T) * h * 2, 1024);
+    nout = std::max(plan.outboxes[dev], 1);
+    outbox = static_cast<uint8_t*>(dmalloc(msg_bytes * size_t(nout), "outbox"));
+    nflags = size_t(plan.max_outbox + 1) * size_t(plan.topo.devices + 2);
+    flags = static_cast<uint32_t*>(dmalloc(nflags * 4, "flags"));
+    ck(cudaMemsetAsync(flags, 0, nflags * 4, cs), "memset");
+    scratch = static_cast<__nv_bfloat16*>(dmalloc(size_t(T) * h * 2, "scratch"));
+    dsum = static_cast<float*>(dmalloc(size_t(H) * T * 4, "scratch"));
+    dq_acc = static_cast<float*>(dmalloc(size_t(T) * h * 4, "scratch"));
+    tokens = static_cast<int32_t*>(dmalloc(size_t(m) * T * 4, "inputs"));
+    labels = static_cast<int32_t*>(dmalloc(size_t(m) * T * 4, "inputs"));
+    loss_dev = static_cast<float*>(dmalloc(64, "loss"));
+    ck(cudaMallocHost(reinterpret_cast<void**>(&loss_host), 64), "pinned");
+
+    const auto& ops = plan.dev_ops[dev];
+    pos_of.assign(plan.ops.size(), -1);
+    for (size_t j = 0; j < ops.size(); ++j) pos_of[ops[j]] = int(j);
+    ev_start.resize(ops.size());
+    ev_end.resize(ops.size());
+    ev_pull.resize(ops.size());
+    ev_free.resize(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) {
+        ck(cudaEventCreate(&ev_start[i]), "event");
+        ck(cudaEventCreate(&ev_end[i]), "event");
+        ck(cudaEventCreateWithFlags(&ev_pull[i], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming), "event");
+    }
+    ck(cudaEventCreate(&ev_step0), "event");
+    ck(cudaEventCreate(&ev_step1), "event");
+    peers.assign(size_t(plan.topo.devices) + 1, Peer{});
+    peers[dev] = Peer{outbox, flags, false};
+    ck(cudaStreamSynchronize(cs), "init");
+}
+
+Exec::~Exec() {
+    cudaSetDevice(cuda);
+    cudaDeviceSynchronize();
+    for (auto* v : {&ev_start, &ev_end, &ev_pull, &ev_free})
+        for (auto e : *v) cudaEventDestroy(e);
+    cudaEventDestroy(ev_step0);
+    cudaEventDestroy(ev_step1);
+    for (auto& p : peers)
+        if (p.ipc) {
+            cudaIpcCloseMemHandle(p.outbox);
+            cudaIpcCloseMemHandle(p.flags);
+        }
+    for (void* p : allocations) cudaFree(p);
+    if (loss_host) cudaFreeHost(loss_host);
+    cudaStreamDestroy(cs);
+    cudaStreamDestroy(xs);
+}
+
+// ------------------------------------------------------------------ passes
+__nv_bfloat16* Exec::bf(int slot, size_t off) const {
+    return reinterpret_cast<__nv_bfloat16*>(pool + size_t(slot) * slot_bytes + off);
+}
+float* Exec::f32(int slot, size_t off) const { return reinterpret_cast<float*>(pool + size_t(slot) * slot_bytes + off); }
+__nv_bfloat16* Exec::outbox_ptr(int k) const { return reinterpret_cast<__nv_bfloat16*>(outbox + size_t(k) * msg_bytes); }
+
+void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __nv_bfloat16* B, bool b_mn, void* C,
+                int epi, const __nv_bfloat16* aux, void* C2, int accumulate) {
+    pbk::GemmArgs g;
+    g.M = M, g.N = N, g.K = K;
+    g.A = A, g.a_mn = a_mn, g.lda = a_mn ? M : K;
+    g.B = B, g.b_mn = b_mn, g.ldb = b_mn ? N : K;
+    g.C = C, g.ldc = N, g.C2 = C2;
+    g.aux = aux, g.ldaux = N;
+    g.epi = epi, g.accumulate = accumulate;
+    pbk::gemm(g, cs);
+    ++launches;
+}
+
+void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
+    const StageLayout& L = layout.at(s);
+    const StageParams& P = sparams.at(s);
+    __nv_bfloat16* x0 = bf(slot, L.x[0]);
+    if (s == 1) {
+        pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, cs);
+        ++launches;
+    }
+    for (int l = 0; l < Lc; ++l) {
+        const auto& y = L.layer[l];
+        const auto& w = P.layers[l];
+        __nv_bfloat16* x = bf(slot, L.x[l]);
+        __nv_bfloat16* xo = (l == Lc - 1 && s < S) ? out : bf(slot, L.x[l + 1]);
+        pbk::rmsnorm_fwd(x, W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs);
+        gemm(T, 3 * h, h, bf(slot, y.a), false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE);
+        pbk::attn_fwd(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs);
+        gemm(T, h, h, bf(slot, y.o), false, W(w.wo), false, bf(slot, y.x1), pbk::EPI_RESID, x);
+        pbk::rmsnorm_fwd(bf(slot, y.x1), W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs);
+        gemm(T, 4 * h, h, bf(slot, y.b), false, W(w.w1), false, bf(slot, y.u), pbk::EPI_GELU, nullptr,
+             bf(slot, y.gl));
+        gemm(T, h, 4 * h, bf(slot, y.gl), false, W(w.w2), false, xo, pbk::EPI_RESID, bf(slot, y.x1));
+        launches += 3;
+    }
+    if (s == S) {
+        pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), W(P.gf), bf(slot, L.hf), f32(slot, L.rstdf), T, h, cs);
+        gemm(T, V, h, bf(slot, L.hf), false, W(P.head), false, bf(slot, L.logits), pbk::EPI_STORE);
+        pbk::cross_entropy(bf(slot, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
+                           cs);
+        launches += 2;
+    }
+}
+
+void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
+    (void)mb;
+    const StageLayout& L = layout.at(s);
+    const StageParams& P = sparams.at(s);
+    if (s == S) {
+        // dhf = dlogits . Whead ; dx_L = rmsnorm_bwd(dhf)
+        gemm(T, h, V, bf(slot, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
+        pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), W(P.gf), f32(slot, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
+                         cs);
+        pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), f32(slot, L.rstdf), G(P.gf), T, h, cs);
+        launches += 2;
+    }
+    for (int l = Lc - 1; l >= 0; --l) {
+        const auto& y = L.layer[l];
+        const auto& w = P.layers[l];
+        __nv_bfloat16* dy = bf(slot, L.dx[l + 1]);
+        __nv_bfloat16* dxo = (l == 0 && s > 1) ? out : bf(slot, L.dx[l]);
+        // du = (dy . W2) * gelu'(u), written over u
+        gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u));
+        gemm(T, h, 4 * h, bf(slot, y.u), false, W(w.w1), true, scratch, pbk::EPI_STORE);
+        pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs);
+        pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), T, h, cs);
+        gemm(T, h, h, bf(slot, y.dx1), false, W(w.wo), true, scratch, pbk::EPI_STORE);
+        pbk::attn_bwd(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
+                      seq, H, cs);
+        gemm(T, h, 3 * h, bf(slot, y.dqkv), false, W(w.wqkv), true, scratch, pbk::EPI_STORE);
+        pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs);
+        pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), T, h, cs);
+        launches += 8;
+    }
+}
+
+void Exec::pass_weight(int s, int mb, int slot) {
+    const StageLayout& L = layout.at(s);
+    const StageParams& P = sparams.at(s);
+    for (int l = Lc - 1; l >= 0; --l) {
+        const auto& y = L.layer[l];
+        const auto& w = P.layers[l];
+        gemm(h, 4 * h, T, bf(slot, L.dx[l + 1]), true, bf(slot, y.gl), true, G(w.w2), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(4 * h, h, T, bf(slot, y.u), true, bf(slot, y.b), true, G(w.w1), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(h, h, T, bf(slot, y.dx1), true, bf(slot, y.o), true, G(w.wo), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, y.a), true, G(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
+    }
+    if (s == S)
+        gemm(V, h, T, bf(slot, L.logits), true, bf(slot, L.hf), true, G(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
+    if (s == 1) {
+        pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, cs);
+        ++launches;
+    }
+}
+
+// ------------------------------------------------------------------ step
+uint32_t Exec::gen_total(const Msg& msg) const {
+    return uint32_t(steps_done) * plan.uses[msg.src_dev][msg.outbox] + msg.gen;
+}
+uint32_t* Exec::ack_flag(uint32_t* base, int k) const { return base + k; }
+uint32_t* Exec::ready_flag(uint32_t* base, int src, int k) const {
+    return base + size_t(plan.max_outbox + 1) * size_t(1 + src) + k;
+}
+
+void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
+    if (!connected && plan.topo.devices > 1) throw StateError("pb_exec_step before peers are connected");
+    ck(cudaSetDevice(cuda), "cudaSetDevice");
+    launches = 0;
+    peer_bytes = 0;
+    const size_t nin = size_t(m) * T * 4;
+    const auto kind = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    ck(cudaEventRecord(ev_step0, cs), "event");
+    const bool has_first = std::find(stages.begin(), stages.end(), 1) != stages.end();
+    const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
+    if (has_first) {
+        if (!tok) throw std::invalid_argument("tokens required on the device holding stage 1");
+        ck(cudaMemcpyAsync(tokens, tok, nin, kind, cs), "tokens");
+    }
+    if (has_last) {
+        if (!lab) throw std::invalid_argument("labels required on the device holding the last stage");
+        ck(cudaMemcpyAsync(labels, lab, nin, kind, cs), "labels");
+        ck(cudaMemsetAsync(loss_dev, 0, 4, cs), "loss");
+    }
+    const auto& ops = plan.dev_ops[dev];
+    int live = 0;
+    pool_live_peak = 0;
+    for (size_t j = 0; j < ops.size(); ++j) {
+        const int i = ops[j];
+        const PlanOp& po = plan.ops[i];
+        const auto& o = po.op;
+        const StageLayout& L = layout.at(o.stage);
+        // ---- incoming boundary tensor
+        __nv_bfloat16* in_dst = nullptr;
+        const Msg* in = po.in_msg >= 0 ? &plan.msgs[po.in_msg] : nullptr;
+        if (in) in_dst = o.kind == Kind::F ? bf(po.slot, L.x[0]) : bf(po.slot, L.dx[Lc]);
+        if (in && !in->local()) {
+            if (o.kind == Kind::F && po.free_op >= 0) {
+                ck(cudaStreamWaitEvent(xs, ev_free[size_t(pos_of[po.free_op])], 0), "wait");
+            }
+            const Peer& src = peers[in->src_dev];
+            const uint32_t g = gen_total(*in);
+            wait_value(xs, ready_flag(flags, in->src_dev, in->outbox), g);
+            ck(cudaMemcpyAsync(in_dst, reinterpret_cast<uint8_t*>(src.outbox) + size_t(in->outbox) * msg_bytes,
+                               size_t(T) * h * 2, cudaMemcpyDeviceToDevice, xs),
+               "peer copy");
+            write_value(xs, ack_flag(src.flags, in->outbox), g);
+            ck(cudaEventRecord(ev_pull[j], xs), "event");
+            ck(cudaStreamWaitEvent(cs, ev_pull[j], 0), "wait");
+            peer_bytes += int64_t(T) * h * 2;
+        }
+        // ---- outgoing: outbox slot must be drained by its previous (remote) consumer
+        const Msg* out = po.out_msg >= 0 ? &plan.msgs[po.out_msg] : nullptr;
+        if (out && out->prev_remote && gen_total(*out) > 1) wait_value(cs, ack_flag(flags, out->outbox), gen_total(*out) - 1);
+        if (timeline) ck(cudaEventRecord(ev_start[j], cs), "event");
+        if (in && in->local())
+            ck(cudaMemcpyAsync(in_dst, outbox_ptr(in->outbox), size_t(T) * h * 2, cudaMemcpyDeviceToDevice, cs),
+               "local copy");
+        __nv_bfloat16* out_ptr = out ? outbox_ptr(out->outbox) : nullptr;
+        switch (o.kind) {
+            case Kind::F:
+                ++live;
+                pool_live_peak = std::max(pool_live_peak, live);
+                pass_forward(o.stage, o.mb, po.slot, out_ptr);
+                break;
+            case Kind::B: pass_backward(o.stage, o.mb, po.slot, out_ptr); break;
+            case Kind::W: pass_weight(o.stage, o.mb, po.slot); break;
+            case Kind::BW:
+                pass_backward(o.stage, o.mb, po.slot, out_ptr);
+                pass_weight(o.stage, o.mb, po.slot);
+                break;
+        }
+        if (timeline) ck(cudaEventRecord(ev_end[j], cs), "event");
+        if (out && !out->local()) write_value(cs, ready_flag(peers[out->dst_dev].flags, dev, out->outbox), gen_total(*out));
+        if (o.kind == Kind::W || o.kind == Kind::BW) {
+            --live;
+            ck(cudaEventRecord(ev_free[j], cs), "event");
+        }
+        if (serial) {
+            ck(cudaStreamSynchronize(xs), "serial");
+            ck(cudaStreamSynchronize(cs), "serial");
+        }
+    }
+    if (cfg.optimizer) {
+        ++adam_step;
+        pbk::adamw(master, wts, grads, adam_m, adam_v, n_params, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
+                   cfg.weight_decay, adam_step, cs);
+        ++launches;
+    }
+    if (has_last) ck(cudaMemcpyAsync(loss_host, loss_dev, 4, cudaMemcpyDeviceToHost, cs), "loss");
+    ck(cudaEventRecord(ev_step1, cs), "event");
+    ck(cudaGetLastError(), "launch");
+    ++steps_done;
+    pending = true;
+}
+
+void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
+    ck(cudaSetDevice(cuda), "cudaSetDevice");
+    ck(cudaStreamSynchronize(cs), "step");
+    ck(cudaStreamSynchronize(xs), "step");
+    pending = false;
+    const auto& ops = plan.dev_ops[dev];
+    const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
+    double busy = 0;
+    if (timeline) {
+        if (tl && tl_n < ops.size()) throw Space("timeline buffer too small");
+        for (size_t j = 0; j < ops.size(); ++j) {
+            float a = 0, b = 0;
+            ck(cudaEventElapsedTime(&a, ev_step0, ev_start[j]), "elapsed");
+            ck(cudaEventElapsedTime(&b, ev_step0, ev_end[j]), "elapsed");
+            busy += double(b) - double(a);
+            if (tl) {
+                const auto& o = plan.ops[ops[j]].op;
+                tl[j] = {o.device, o.stage, int32_t(o.kind), o.mb, double(a), double(b) - double(a)};
+            }
+        }
+    }
+    if (st) {
+        float total = 0;
+        ck(cudaEventElapsedTime(&total, ev_step0, ev_step1), "elapsed");
+        st->loss = has_last ? double(*loss_host) : NAN;
+        st->step_ms = total;
+        st->busy_ms = busy;
+        st->pool_slots = nslots;
+        st->pool_peak = pool_live_peak;
+        st->slot_bytes = int64_t(slot_bytes);
+        st->pool_bytes = int64_t(slot_bytes) * nslots;
+        st->peer_bytes = peer_bytes;
+        st->kernel_launches = launches;
+    }
+}
+
+// ------------------------------------------------------------------ peers
+void Exec::connect_local(const std::vector<Exec*>& all) {
+    if (int(all.size()) != plan.topo.devices) throw std::invalid_argument("connect: need one exec per device");
+    for (Exec* e : all) {
+        if (e->plan.ops.size() != plan.ops.size()) throw std::invalid_argument("connect: executors run different plans");
+        peers[e->dev] = Peer{e->outbox, e->flags, false};
+        if (e->cuda != cuda) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, cuda, e->cuda);
+            if (!can) throw CudaError("no peer access between GPUs " + std::to_string(cuda) + " and " + std::to_string(e->cuda));
+            cudaSetDevice(cuda);
+            cudaError_t r = cudaDeviceEnablePeerAccess(e->cuda, 0);
+            if (r != cudaSuccess && r != cudaErrorPeerAccessAlreadyEnabled) ck(r, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    }
+    connected = true;
+}
+
+struct IpcBlob {
+    uint32_t magic;
+    int32_t device;
+    int32_t cuda;
+    uint64_t plan_ops;
+    cudaIpcMemHandle_t outbox, flags;
+};
+
+size_t Exec::export_blob(void* buf, size_t cap) {
+    IpcBlob b{};
+    b.magic = 0x50423230;
+    b.device = dev;
+    b.cuda = cuda;
+    b.plan_ops = plan.ops.size();
+    ck(cudaSetDevice(cuda), "cudaSetDevice");
+    ck(cudaIpcGetMemHandle(&b.outbox, outbox), "cudaIpcGetMemHandle");
+    ck(cudaIpcGetMemHandle(&b.flags, flags), "cudaIpcGetMemHandle");
+    if (buf) {
+        if (cap < sizeof b) throw Space("blob buffer too small");
+        std::memcpy(buf, &b, sizeof b);
+    }
+    return sizeof b;
+}
+
+void Exec::connect_ipc(const std::vector<std::pair<const void*, size_t>>& blobs) {
+    if (int(blobs.size()) != plan.topo.devices) throw std::invalid_argument("connect_ipc: need one blob per device");
+    ck(cudaSetDevice(cuda), "cudaSetDevice");
+    for (const auto& [p, n] : blobs) {
+        if (n < sizeof(IpcBlob)) throw std::invalid_argument("connect_ipc: short blob");
+        IpcBlob b;
+        std::memcpy(&b, p, sizeof b);
+        if (b.magic != 0x50423230 || b.plan_ops != plan.ops.size()) throw std::invalid_argument("connect_ipc: bad blob");
+        if (b.device == dev) continue;
+        // only neighbours exchange messages, but every peer is mapped (cheap)
+        void *ob = nullptr, *fl = nullptr;
+        ck(cudaIpcOpenMemHandle(&ob, b.outbox, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        ck(cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        peers[b.device] = Peer{ob, static_cast<uint32_t*>(fl), true};
+    }
+    connected = true;
+}
+
+}  // namespace pbx

@@ -1,0 +1,102 @@
+// Device-side runtime of one pipeline device (see executor.cpp).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "capi_common.hpp"
+#include "kernels/ops.hpp"
+#include "plan.hpp"
+
+namespace pbx {
+
+struct LayerSlots {  // byte offsets inside an activation slot
+    size_t a, qkv, o, x1, b, u, gl, dqkv, dx1, rstd1, rstd2, lse;
+};
+struct StageLayout {
+    std::vector<size_t> x, dx;  // Lc+1 residual-stream buffers and their gradients
+    std::vector<LayerSlots> layer;
+    size_t hf = 0, rstdf = 0, logits = 0;
+    size_t bytes = 0;
+};
+struct LayerParams {
+    size_t g1, wqkv, wo, g2, w1, w2;  // indices into ptensors
+};
+struct StageParams {
+    std::vector<LayerParams> layers;
+    size_t emb = 0, gf = 0, head = 0;
+};
+struct PTensor {
+    std::string name;
+    size_t off, numel;
+    int id;
+    float std, constant;
+};
+struct Peer {
+    void* outbox = nullptr;
+    uint32_t* flags = nullptr;
+    bool ipc = false;
+};
+
+class Exec {
+  public:
+    Exec(const pb_model_cfg& cfg, const vsched::Grid& grid, int device, int cuda_dev);
+    ~Exec();
+    void connect_local(const std::vector<Exec*>& all);
+    size_t export_blob(void* buf, size_t cap);
+    void connect_ipc(const std::vector<std::pair<const void*, size_t>>& blobs);
+    void enqueue(const int32_t* tok, const int32_t* lab, bool on_host);
+    void finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st);
+
+    pb_model_cfg cfg;
+    ExecPlan plan;
+    int dev, cuda;
+    int S = 0, Lc = 0, T = 0, h = 0, H = 0, V = 0, seq = 0, mbs = 0, m = 0;
+    std::vector<int> stages;
+    std::vector<PTensor> ptensors;
+    float *master = nullptr, *grads = nullptr, *adam_m = nullptr, *adam_v = nullptr;
+    __nv_bfloat16* wts = nullptr;
+    size_t n_params = 0;
+    cudaStream_t cs = nullptr, xs = nullptr;
+    bool timeline = true, serial = false, connected = false, pending = false;
+    int adam_step = 0;
+
+  private:
+    void build_layout();
+    void build_params();
+    __nv_bfloat16* bf(int slot, size_t off) const;
+    float* f32(int slot, size_t off) const;
+    __nv_bfloat16* outbox_ptr(int k) const;
+    const __nv_bfloat16* W(size_t p) const { return wts + ptensors[p].off; }
+    float* G(size_t p) const { return grads + ptensors[p].off; }
+    void gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __nv_bfloat16* B, bool b_mn, void* C,
+              int epi, const __nv_bfloat16* aux = nullptr, void* C2 = nullptr, int accumulate = 0);
+    void pass_forward(int s, int mb, int slot, __nv_bfloat16* out);
+    void pass_backward(int s, int mb, int slot, __nv_bfloat16* out);
+    void pass_weight(int s, int mb, int slot);
+    uint32_t gen_total(const Msg& m) const;
+    uint32_t* ack_flag(uint32_t* base, int k) const;
+    uint32_t* ready_flag(uint32_t* base, int src, int k) const;
+
+    std::map<int, StageLayout> layout;
+    std::map<int, StageParams> sparams;
+    size_t slot_bytes = 0, msg_bytes = 0, nflags = 0;
+    int nslots = 0, nout = 0, pool_live_peak = 0;
+    uint8_t* pool = nullptr;
+    uint8_t* outbox = nullptr;
+    uint32_t* flags = nullptr;
+    __nv_bfloat16* scratch = nullptr;
+    float *dsum = nullptr, *dq_acc = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
+    int32_t *tokens = nullptr, *labels = nullptr;
+    std::vector<void*> allocations;
+    std::vector<cudaEvent_t> ev_start, ev_end, ev_pull, ev_free;
+    cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
+    std::vector<Peer> peers;
+    std::vector<int> pos_of;
+    int64_t steps_done = 0, launches = 0, peer_bytes = 0;
+};
+
+}  // namespace pbx

@@ -1,0 +1,317 @@
+// Memory-bound kernels of a pipeline stage: RMSNorm fwd/bwd (+ gamma grads),
+// embedding gather / scatter-add, fused LM-head softmax cross-entropy
+// (loss + dlogits in place), AdamW.  128-bit vector I/O, warp-shuffle
+// reductions, one row per warp where a row fits.
+#include <stdexcept>
+
+#include "ops.hpp"
+#include "sm100.cuh"
+
+namespace pbk {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int k = 16; k; k >>= 1) v += __shfl_xor_sync(0xffffffff, v, k);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int k = 16; k; k >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffff, v, k));
+    return v;
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[2 * i] = bf16_lo(w[i]), f[2 * i + 1] = bf16_hi(w[i]);
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+}
+
+// y = x * rsqrt(mean(x^2) + eps) * g ; one warp per row
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                   __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h, float eps) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h);
+    const int nch = h >> 3;
+    float ss = 0.f;
+    for (int c = lane; c < nch; c += 32) {
+        float f[8];
+        unpack8(xr[c], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+    }
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss / float(h) + eps);
+    if (lane == 0) rstd[row] = r;
+    const uint4* gr = reinterpret_cast<const uint4*>(g);
+    uint4* yr = reinterpret_cast<uint4*>(y + size_t(row) * h);
+    for (int c = lane; c < nch; c += 32) {
+        float f[8], w[8];
+        unpack8(xr[c], f);
+        unpack8(gr[c], w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = f[i] * r * w[i];
+        yr[c] = pack8(f);
+    }
+}
+
+// dx = dres + r*g*dy - x * r^3/h * sum(g*dy*x) ; one warp per row, no atomics
+__global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
+                                   const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int T,
+                                   int h) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const int nch = h >> 3;
+    const uint4* gr = reinterpret_cast<const uint4*>(g);
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + size_t(row) * h);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h);
+    const float r = rstd[row];
+    float dot = 0.f;
+    for (int c = lane; c < nch; c += 32) {
+        float a[8], b[8], w[8];
+        unpack8(dyr[c], a);
+        unpack8(xr[c], b);
+        unpack8(gr[c], w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot += w[i] * a[i] * b[i];
+    }
+    dot = warp_sum(dot);
+    const float k = dot * r * r * r / float(h);
+    uint4* dxr = reinterpret_cast<uint4*>(dx + size_t(row) * h);
+    const uint4* dres_r = dres ? reinterpret_cast<const uint4*>(dres + size_t(row) * h) : nullptr;
+    for (int c = lane; c < nch; c += 32) {
+        float a[8], b[8], w[8], o[8];
+        unpack8(dyr[c], a);
+        unpack8(xr[c], b);
+        unpack8(gr[c], w);
+        if (dres_r) {
+            unpack8(dres_r[c], o);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += r * w[i] * a[i] - b[i] * k;
+        dxr[c] = pack8(o);
+    }
+}
+
+// dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t] ; thread = 8 columns x a slab of rows
+__global__ void rmsnorm_dgamma_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                      const float* __restrict__ rstd, float* __restrict__ dgamma, int T, int h,
+                                      int rows_per_block) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column chunk
+    if (c * 8 >= h) return;
+    const int r0 = blockIdx.y * rows_per_block, r1 = min(T, r0 + rows_per_block);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int row = r0; row < r1; ++row) {
+        float a[8], b[8];
+        unpack8(reinterpret_cast<const uint4*>(dy + size_t(row) * h)[c], a);
+        unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], b);
+        const float r = rstd[row];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += a[i] * b[i] * r;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) atomicAdd(dgamma + c * 8 + i, acc[i]);
+}
+
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ emb,
+                                 __nv_bfloat16* __restrict__ x, int T, int h) {
+    const int row = blockIdx.x;
+    const uint4* src = reinterpret_cast<const uint4*>(emb + size_t(tok[row]) * h);
+    uint4* dst = reinterpret_cast<uint4*>(x + size_t(row) * h);
+    for (int c = threadIdx.x; c < (h >> 3); c += blockDim.x) dst[c] = src[c];
+}
+
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
+                                 float* __restrict__ demb, int T, int h) {
+    const int row = blockIdx.x;
+    float* dst = demb + size_t(tok[row]) * h;
+    const uint4* src = reinterpret_cast<const uint4*>(dx + size_t(row) * h);
+    for (int c = threadIdx.x; c < (h >> 3); c += blockDim.x) {
+        float f[8];
+        unpack8(src[c], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) atomicAdd(dst + c * 8 + i, f[i]);
+    }
+}
+
+// one block per row: loss += (lse - z[label]) * scale ; z <- (softmax(z) - onehot) * scale  (bf16, in place)
+__global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ logits, const int32_t* __restrict__ labels,
+                                                 float* __restrict__ loss, int V, float scale) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    __nv_bfloat16* z = logits + size_t(row) * V;
+    const int nch = V >> 3;
+    uint4* z4 = reinterpret_cast<uint4*>(z);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    float m = -INFINITY;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+        float f[8];
+        unpack8(z4[c], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, f[i]);
+    }
+    m = warp_max(m);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (warp == 0) {
+        float v = lane < nw ? red[lane] : -INFINITY;
+        v = warp_max(v);
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    m = red[0];
+    __syncthreads();
+    float s = 0.f;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+        float f[8];
+        unpack8(z4[c], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += __expf(f[i] - m);
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+        float v = lane < nw ? red[lane] : 0.f;
+        v = warp_sum(v);
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    s = red[0];
+    const int lab = labels[row];
+    const float zl = __bfloat162float(z[lab]);
+    __syncthreads();
+    const float inv = 1.f / s;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+        float f[8];
+        unpack8(z4[c], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float p = __expf(f[i] - m) * inv;
+            if (c * 8 + i == lab) p -= 1.f;
+            f[i] = p * scale;
+        }
+        z4[c] = pack8(f);
+    }
+    if (threadIdx.x == 0) atomicAdd(loss, (m + __logf(s) - zl) * scale);
+}
+
+// AdamW on fp32 masters; refreshes the bf16 copy and zeroes the gradient.
+__global__ void adamw_kernel(float* __restrict__ w, __nv_bfloat16* __restrict__ wb, float* __restrict__ gr,
+                             float* __restrict__ m, float* __restrict__ v, size_t n, float lr, float b1, float b2,
+                             float eps, float wd, float bc1, float bc2) {
+    size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    const size_t stride = size_t(gridDim.x) * blockDim.x * 4;
+    for (; i < n; i += stride) {
+        float4 W = *reinterpret_cast<float4*>(w + i), G = *reinterpret_cast<float4*>(gr + i);
+        float4 M = *reinterpret_cast<float4*>(m + i), Vv = *reinterpret_cast<float4*>(v + i);
+        float* wp = &W.x;
+        float* gp = &G.x;
+        float* mp = &M.x;
+        float* vp = &Vv.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            mp[k] = b1 * mp[k] + (1.f - b1) * gp[k];
+            vp[k] = b2 * vp[k] + (1.f - b2) * gp[k] * gp[k];
+            const float mh = mp[k] / bc1, vh = vp[k] / bc2;
+            wp[k] -= lr * (mh / (sqrtf(vh) + eps) + wd * wp[k]);
+        }
+        *reinterpret_cast<float4*>(w + i) = W;
+        *reinterpret_cast<float4*>(m + i) = M;
+        *reinterpret_cast<float4*>(v + i) = Vv;
+        *reinterpret_cast<float4*>(gr + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<uint2*>(wb + i) = make_uint2(pack_bf16(W.x, W.y), pack_bf16(W.z, W.w));
+    }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, size_t n) {
+    size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    const size_t stride = size_t(gridDim.x) * blockDim.x * 4;
+    for (; i < n; i += stride) {
+        float4 a = *reinterpret_cast<const float4*>(src + i);
+        *reinterpret_cast<uint2*>(dst + i) = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
+    }
+}
+
+// counter-based N(0, std) init (splitmix64 -> Box-Muller), deterministic in (seed, index)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__global__ void init_normal_kernel(float* __restrict__ w, size_t n, uint64_t seed, float std, float constant) {
+    size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (; i < n; i += stride) {
+        if (std == 0.f) {
+            w[i] = constant;
+            continue;
+        }
+        uint64_t r = mix64(seed * 0x2545F4914F6CDD1Dull + i);
+        float u1 = (float((r >> 40) & 0xFFFFFF) + 1.f) * (1.f / 16777217.f);
+        float u2 = float((r >> 16) & 0xFFFFFF) * (1.f / 16777216.f);
+        w[i] = std * sqrtf(-2.f * __logf(u1)) * __cosf(6.283185307179586f * u2);
+    }
+}
+
+int grid_for(size_t n, int per_thread, int block) {
+    size_t blocks = (n / per_thread + block - 1) / block;
+    int cap = num_sms() * 8;
+    return int(blocks < size_t(cap) ? (blocks ? blocks : 1) : cap);
+}
+
+}  // namespace
+
+void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
+                 cudaStream_t s) {
+    if (h % 8) throw std::invalid_argument("rmsnorm: h % 8");
+    rmsnorm_fwd_kernel<<<(T + 7) / 8, 256, 0, s>>>(x, g, y, rstd, T, h, 1e-5f);
+}
+
+void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
+                 const __nv_bfloat16* dres, __nv_bfloat16* dx, int T, int h, cudaStream_t s) {
+    rmsnorm_bwd_kernel<<<(T + 7) / 8, 256, 0, s>>>(dy, x, g, rstd, dres, dx, T, h);
+}
+
+void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, int T, int h,
+                    cudaStream_t s) {
+    const int rows = 128;
+    dim3 grid((h / 8 + 127) / 128, (T + rows - 1) / rows);
+    rmsnorm_dgamma_kernel<<<grid, 128, 0, s>>>(dy, x, rstd, dgamma, T, h, rows);
+}
+
+void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s) {
+    embed_fwd_kernel<<<T, 128, 0, s>>>(tok, emb, x, T, h);
+}
+void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, cudaStream_t s) {
+    embed_bwd_kernel<<<T, 128, 0, s>>>(tok, dx, demb, T, h);
+}
+void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale,
+                   cudaStream_t s) {
+    if (V % 8) throw std::invalid_argument("cross_entropy: V % 8");
+    ce_kernel<<<T, 512, 0, s>>>(logits, labels, loss, V, scale);
+}
+void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
+           float eps, float wd, int step, cudaStream_t s) {
+    if (n % 4) throw std::invalid_argument("adamw: n % 4");
+    const float bc1 = 1.f - powf(b1, float(step)), bc2 = 1.f - powf(b2, float(step));
+    adamw_kernel<<<grid_for(n, 4, 256), 256, 0, s>>>(w, wb, g, m, v, n, lr, b1, b2, eps, wd, bc1, bc2);
+}
+void f32_to_bf16(const float* src, __nv_bfloat16* dst, size_t n, cudaStream_t s) {
+    f32_to_bf16_kernel<<<grid_for(n, 4, 256), 256, 0, s>>>(src, dst, n);
+}
+void init_normal(float* w, size_t n, uint64_t seed, float std, float constant, cudaStream_t s) {
+    init_normal_kernel<<<grid_for(n, 1, 256), 256, 0, s>>>(w, n, seed, std, constant);
+}
+
+}  // namespace pbk

@@ -1,7 +1,37 @@
-// Host interface of the non-GEMM sm_100a kernels.
+// Host interface of the non-GEMM sm_100a kernels (attention.cu, ops.cu).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
-namespace pbk {}  // namespace pbk
+#include "gemm.hpp"
+
+namespace pbk {
+
+// causal MHA, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T]
+void attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int batch, int seq, int heads,
+              cudaStream_t s);
+// dqkv [T,3h] from dout [T,h]; dsum [heads,T] and dq_acc [T,h] fp32 are scratch
+void attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
+              float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s);
+
+void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
+                 cudaStream_t s);
+// dx = dres (may be null) + d/dx rmsnorm(x)*g applied to dy
+void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
+                 const __nv_bfloat16* dres, __nv_bfloat16* dx, int T, int h, cudaStream_t s);
+// dgamma (fp32) += sum_t dy * x * rstd
+void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, int T, int h,
+                    cudaStream_t s);
+void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s);
+void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, cudaStream_t s);
+// loss (fp32 scalar) += scale * sum_rows CE ; logits <- scale * (softmax - onehot), in place
+void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale,
+                   cudaStream_t s);
+void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
+           float eps, float wd, int step, cudaStream_t s);
+void f32_to_bf16(const float* src, __nv_bfloat16* dst, size_t n, cudaStream_t s);
+void init_normal(float* w, size_t n, uint64_t seed, float std, float constant, cudaStream_t s);
+
+}  // namespace pbk

@@ -1,0 +1,127 @@
+"""Attention / RMSNorm / embedding / cross-entropy / AdamW kernels vs torch fp32."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from tests import kernels as K  # noqa: E402
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+def ref_attention(qkv, batch, seq, heads):
+    h = heads * 128
+    q, k, v = qkv.float().view(batch, seq, 3, heads, 128).unbind(2)
+    q, k, v = (t.transpose(1, 2) for t in (q, k, v))  # b, H, s, d
+    s = q @ k.transpose(-1, -2) / math.sqrt(128)
+    mask = torch.triu(torch.ones(seq, seq, dtype=torch.bool, device=qkv.device), 1)
+    s = s.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ v
+    return o.transpose(1, 2).reshape(batch * seq, h), lse
+
+
+@pytest.mark.parametrize("batch,seq,heads", [(1, 64, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2)])
+def test_attention_forward(batch, seq, heads):
+    g = torch.Generator(device="cuda").manual_seed(seq + heads)
+    qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g).bfloat16()
+    out, lse2 = K.attn_fwd(qkv, batch, seq, heads)
+    torch.cuda.synchronize()
+    ref, lse = ref_attention(qkv, batch, seq, heads)
+    assert rel(out, ref) < 1e-2
+    got_lse = (lse2 * math.log(2)).view(heads, batch, seq).permute(1, 0, 2)
+    assert (got_lse - lse).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("batch,seq,heads", [(1, 64, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2)])
+def test_attention_backward(batch, seq, heads):
+    g = torch.Generator(device="cuda").manual_seed(1 + seq + heads)
+    qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g).bfloat16()
+    dout = torch.randn(batch * seq, heads * 128, device="cuda", generator=g).bfloat16()
+    out, lse2 = K.attn_fwd(qkv, batch, seq, heads)
+    dqkv = K.attn_bwd(qkv, out, dout, lse2, batch, seq, heads)
+    torch.cuda.synchronize()
+    x = qkv.float().requires_grad_(True)
+    ref, _ = ref_attention(x, batch, seq, heads)
+    (gx,) = torch.autograd.grad(ref, x, dout.float())
+    H = heads * 128
+    for name, sl in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
+        assert rel(dqkv[:, sl], gx[:, sl]) < 2e-2, name
+
+
+def test_rmsnorm_forward_backward():
+    g = torch.Generator(device="cuda").manual_seed(5)
+    T, h = 300, 1024
+    x = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    gam = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).bfloat16()
+    y, rstd = K.rmsnorm_fwd(x, gam)
+    xf = x.float().requires_grad_(True)
+    gf = gam.float().requires_grad_(True)
+    r = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5)
+    yr = xf * r * gf
+    torch.cuda.synchronize()
+    assert rel(y, yr) < 4e-3
+    assert rel(rstd, r.squeeze(-1)) < 1e-5
+    dy = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    dres = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    dgam = torch.zeros(h, device="cuda")
+    dx = K.rmsnorm_bwd(dy, x, gam, rstd, dres, dgam)
+    gx, gg = torch.autograd.grad(yr, (xf, gf), dy.float())
+    torch.cuda.synchronize()
+    assert rel(dx, gx + dres.float()) < 5e-3
+    assert rel(dgam, gg) < 1e-4
+
+
+def test_embedding():
+    g = torch.Generator(device="cuda").manual_seed(9)
+    V, h, T = 512, 256, 1000
+    emb = torch.randn(V, h, device="cuda", generator=g).bfloat16()
+    tok = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
+    x = K.embed_fwd(tok, emb)
+    dx = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    demb = torch.zeros(V, h, device="cuda")
+    K.embed_bwd(tok, dx, demb)
+    ref = torch.zeros(V, h, device="cuda").index_add_(0, tok.long(), dx.float())
+    torch.cuda.synchronize()
+    assert torch.equal(x, emb[tok.long()])
+    assert rel(demb, ref) < 1e-6
+
+
+@pytest.mark.parametrize("T,V", [(64, 1024), (256, 50304)])
+def test_cross_entropy(T, V):
+    g = torch.Generator(device="cuda").manual_seed(T)
+    z = (3 * torch.randn(T, V, device="cuda", generator=g)).bfloat16()
+    lab = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
+    loss = torch.zeros(1, device="cuda")
+    zz = z.clone()
+    scale = 1.0 / (T * 3)
+    K.cross_entropy(zz, lab, loss, scale)
+    zf = z.float().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(zf, lab.long(), reduction="sum") * scale
+    (gz,) = torch.autograd.grad(ref, zf)
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) / ref.item() < 1e-4
+    assert rel(zz, gz) < 5e-3
+
+
+def test_adamw():
+    g = torch.Generator(device="cuda").manual_seed(2)
+    n = 4096
+    w = torch.randn(n, device="cuda", generator=g)
+    gr = torch.randn(n, device="cuda", generator=g)
+    m = torch.zeros(n, device="cuda")
+    v = torch.zeros(n, device="cuda")
+    wb = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    p = torch.nn.Parameter(w.clone())
+    opt = torch.optim.AdamW([p], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    p.grad = gr.clone()
+    opt.step()
+    K.adamw(w, wb, gr, m, v, 1e-3, 0.9, 0.95, 1e-8, 0.1, 1)
+    torch.cuda.synchronize()
+    assert rel(w, p.detach()) < 1e-6
+    assert torch.equal(wb, w.bfloat16())
+    assert gr.abs().max().item() == 0.0

@@ -1,0 +1,62 @@
+"""The CPU numerics oracle: schedule-driven F/B/W execution equals plain autograd,
+and out-of-order passes are rejected.  (CPU only; small config.)"""
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as N
+from paper_2405_15362_b200 import pipeblock as pb
+
+CFG = SimpleNamespace(layers=4, hidden=256, heads=2, seq=128, vocab=512, micro_batch=1)
+
+
+def make_params(S, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    out = {}
+    for n, shp in N.shapes(CFG, S).items():
+        if n.endswith(("norm", "norm1", "norm2")):
+            out[n] = 1 + 0.1 * torch.randn(shp, generator=g)
+        else:
+            out[n] = 0.05 * torch.randn(shp, generator=g)
+    return out
+
+
+def batch(m, seed=1):
+    rng = np.random.default_rng(seed)
+    t = rng.integers(0, CFG.vocab, size=(m, CFG.seq + 1))
+    return t[:, :-1].astype(np.int32), t[:, 1:].astype(np.int32)
+
+
+@pytest.mark.parametrize("entry,p", [("zb-h1", 1), ("1f1b", 2), ("zb-h1", 4), ("v-min", 2), ("v-half", 2), ("v-zb", 2)])
+def test_schedule_step_matches_autograd(entry, p):
+    g = pb.assemble(pb.build_entry(entry, p), 4)
+    S = g.topology.num_stages
+    params = make_params(S)
+    tok, lab = batch(4)
+    l_ref, g_ref = N.reference_step(params, tok, lab, CFG, S)
+    l_sch, g_sch = N.schedule_step(params, tok, lab, CFG, g.passes, S)
+    assert abs(l_ref - l_sch) < 1e-5 * abs(l_ref)
+    for n in g_ref:
+        assert N.rel_l2(g_sch[n], g_ref[n]) < 1e-5, n
+
+
+def test_partition_invariance():
+    p2 = make_params(4)
+    p1 = N.rename_for(p2, CFG, 4, 1)
+    tok, lab = batch(2)
+    l4, g4 = N.reference_step(p2, tok, lab, CFG, 4)
+    l1, g1 = N.reference_step(p1, tok, lab, CFG, 1)
+    assert abs(l4 - l1) < 1e-6 * abs(l1)
+    g4r = N.rename_for(g4, CFG, 4, 1)
+    for n in g1:
+        assert N.rel_l2(g4r[n], g1[n]) < 1e-5
+
+
+def test_out_of_order_passes_rejected():
+    g = pb.assemble(pb.build_entry("v-half", 2), 2)
+    bad = [q._replace(start=-1) if (q.kind == "W" and q.stage == 3 and q.microbatch == 0) else q for q in g.passes]
+    tok, lab = batch(2)
+    with pytest.raises(RuntimeError, match="before its"):
+        N.schedule_step(make_params(4), tok, lab, CFG, bad, 4)
