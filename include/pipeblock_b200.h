@@ -133,6 +133,7 @@ typedef struct pb_model_cfg {
 
 #define PB_FLAG_SERIAL 1     /* device-synchronise after every pass (race check mode) */
 #define PB_FLAG_TIMELINE 2   /* record per-pass CUDA events (TimedSchedule output) */
+#define PB_FLAG_GEMM_TIMING 4 /* CUDA events around every GEMM launch (roofline of the dominant kernel) */
 
 typedef struct pb_exec_stats {
     double loss;            /* mean CE over all tokens of the step (last-stage device; NaN elsewhere) */
@@ -144,6 +145,9 @@ typedef struct pb_exec_stats {
     int64_t pool_bytes;     /* slot_bytes * pool_slots */
     int64_t peer_bytes;     /* bytes pulled from peers during the step */
     int64_t kernel_launches;/* kernels this device launched during the step */
+    double gemm_ms;         /* PB_FLAG_GEMM_TIMING: summed GEMM launch durations (CUDA events, compute stream) */
+    double gemm_flops;      /* algorithmic FLOPs of those GEMMs (2*M*N*K each) */
+    int64_t gemm_launches;
 } pb_exec_stats;
 
 typedef struct pb_exec pb_exec;
@@ -171,6 +175,8 @@ int pb_exec_step(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32
 int pb_exec_step_async(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32_t inputs_on_host);
 int pb_exec_sync(pb_exec* e, pb_timed_pass* timeline, size_t timeline_n, pb_exec_stats* stats);
 int pb_exec_num_passes(const pb_exec* e, size_t* n);
+/* Change PB_FLAG_* between steps (e.g. one GEMM-timed step for the roofline). */
+int pb_exec_set_flags(pb_exec* e, int32_t flags);
 void* pb_exec_stream(pb_exec* e); /* cudaStream_t of the compute stream */
 /* Parameter access for parity tests: tensors are enumerated per stage owned
  * by this device; names like "s3.l1.wqkv", "s1.emb", "s8.head", "s8.norm". */

@@ -48,7 +48,8 @@ class pb_model_cfg(C.Structure):
 class pb_exec_stats(C.Structure):
     _fields_ = [("loss", C.c_double), ("step_ms", C.c_double), ("busy_ms", C.c_double), ("pool_slots", C.c_int64),
                 ("pool_peak", C.c_int64), ("slot_bytes", C.c_int64), ("pool_bytes", C.c_int64),
-                ("peer_bytes", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("peer_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("gemm_ms", C.c_double),
+                ("gemm_flops", C.c_double), ("gemm_launches", C.c_int64)]
 
 
 # every symbol include/pipeblock_b200.h declares (checked by tests/test_capi.py)
@@ -57,7 +58,7 @@ EXPORTS = [
     "pb_schedule_emit", "pb_schedule_info", "pb_schedule_topology", "pb_schedule_passes", "pb_schedule_exact_peak",
     "pb_simulate", "pb_account", "pb_schedule_destroy", "pb_exec_create", "pb_exec_connect_local",
     "pb_exec_export", "pb_exec_connect_ipc", "pb_exec_step", "pb_exec_step_async", "pb_exec_sync",
-    "pb_exec_num_passes", "pb_exec_stream", "pb_exec_param_count", "pb_exec_param_info", "pb_exec_param_get",
+    "pb_exec_num_passes", "pb_exec_set_flags", "pb_exec_stream", "pb_exec_param_count", "pb_exec_param_info", "pb_exec_param_get",
     "pb_exec_param_set", "pb_exec_zero_grads", "pb_exec_destroy",
 ]
 

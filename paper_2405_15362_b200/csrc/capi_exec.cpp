@@ -24,6 +24,7 @@ extern "C" int pb_exec_create(const pb_model_cfg* cfg, const pb_schedule* plan, 
         auto* e = new pbx::Exec(*cfg, pbx::schedule_grid(plan), device, cuda_device);
         e->timeline = (cfg->flags & PB_FLAG_TIMELINE) != 0;
         e->serial = (cfg->flags & PB_FLAG_SERIAL) != 0;
+        e->gemm_timing = (cfg->flags & PB_FLAG_GEMM_TIMING) != 0;
         if (e->plan.topo.devices == 1) e->connect_local({e});
         *out = new pb_exec{e};
     });
@@ -73,6 +74,16 @@ extern "C" int pb_exec_num_passes(const pb_exec* h, size_t* n) {
     return pbx::guard([&] {
         auto& e = X(const_cast<pb_exec*>(h));
         *n = e.plan.dev_ops[e.dev].size();
+    });
+}
+
+extern "C" int pb_exec_set_flags(pb_exec* h, int32_t flags) {
+    return pbx::guard([&] {
+        auto& e = X(h);
+        if (e.pending) throw pbx::StateError("set_flags while a step is in flight");
+        e.timeline = (flags & PB_FLAG_TIMELINE) != 0;
+        e.serial = (flags & PB_FLAG_SERIAL) != 0;
+        e.gemm_timing = (flags & PB_FLAG_GEMM_TIMING) != 0;
     });
 }
 

@@ -246,6 +246,7 @@ Exec::~Exec() {
     cudaDeviceSynchronize();
     for (auto* v : {&ev_start, &ev_end, &ev_pull, &ev_free})
         for (auto e : *v) cudaEventDestroy(e);
+    for (auto e : gev) cudaEventDestroy(e);
     cudaEventDestroy(ev_step0);
     cudaEventDestroy(ev_step1);
     for (auto& p : peers)
@@ -275,7 +276,18 @@ void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __
     g.C = C, g.ldc = N, g.C2 = C2;
     g.aux = aux, g.ldaux = N;
     g.epi = epi, g.accumulate = accumulate;
-    pbk::gemm(g, cs);
+    if (gemm_timing) {
+        if (gev_used + 2 > gev.size()) {
+            gev.resize(gev.size() + 512);
+            for (size_t i = gev.size() - 512; i < gev.size(); ++i) ck(cudaEventCreate(&gev[i]), "event");
+        }
+        ck(cudaEventRecord(gev[gev_used++], cs), "event");
+        pbk::gemm(g, cs);
+        ck(cudaEventRecord(gev[gev_used++], cs), "event");
+        gemm_flops_acc += 2.0 * double(M) * double(N) * double(K);
+    } else {
+        pbk::gemm(g, cs);
+    }
     ++launches;
 }
 
@@ -376,6 +388,8 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     ck(cudaSetDevice(cuda), "cudaSetDevice");
     launches = 0;
     peer_bytes = 0;
+    gev_used = 0;
+    gemm_flops_acc = 0;
     const size_t nin = size_t(m) * T * 4;
     const auto kind = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     ck(cudaEventRecord(ev_step0, cs), "event");
@@ -495,6 +509,15 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
         st->pool_bytes = int64_t(slot_bytes) * nslots;
         st->peer_bytes = peer_bytes;
         st->kernel_launches = launches;
+        double gms = 0;
+        for (size_t i = 0; i + 1 < gev_used; i += 2) {
+            float t = 0;
+            ck(cudaEventElapsedTime(&t, gev[i], gev[i + 1]), "elapsed");
+            gms += t;
+        }
+        st->gemm_ms = gms;
+        st->gemm_flops = gemm_flops_acc;
+        st->gemm_launches = int64_t(gev_used / 2);
     }
 }
 

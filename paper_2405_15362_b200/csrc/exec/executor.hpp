@@ -61,7 +61,7 @@ class Exec {
     __nv_bfloat16* wts = nullptr;
     size_t n_params = 0;
     cudaStream_t cs = nullptr, xs = nullptr;
-    bool timeline = true, serial = false, connected = false, pending = false;
+    bool timeline = true, serial = false, connected = false, pending = false, gemm_timing = false;
     int adam_step = 0;
 
   private:
@@ -97,6 +97,9 @@ class Exec {
     std::vector<Peer> peers;
     std::vector<int> pos_of;
     int64_t steps_done = 0, launches = 0, peer_bytes = 0;
+    std::vector<cudaEvent_t> gev;
+    size_t gev_used = 0;
+    double gemm_flops_acc = 0;
 };
 
 }  // namespace pbx

@@ -28,6 +28,7 @@ from ._lib import KINDS, check, lib, pb_exec_stats, pb_model_cfg, pb_timed_pass
 
 PB_FLAG_SERIAL = 1
 PB_FLAG_TIMELINE = 2
+PB_FLAG_GEMM_TIMING = 4
 
 
 @dataclass
@@ -47,13 +48,15 @@ class ModelConfig:
     optimizer: bool = True
     timeline: bool = True
     serial: bool = False
+    gemm_timing: bool = False
 
     @property
     def tokens_per_microbatch(self) -> int:
         return self.seq * self.micro_batch
 
     def c(self) -> pb_model_cfg:
-        flags = (PB_FLAG_TIMELINE if self.timeline else 0) | (PB_FLAG_SERIAL if self.serial else 0)
+        flags = ((PB_FLAG_TIMELINE if self.timeline else 0) | (PB_FLAG_SERIAL if self.serial else 0)
+                 | (PB_FLAG_GEMM_TIMING if self.gemm_timing else 0))
         return pb_model_cfg(self.layers, self.hidden, self.heads, self.seq, self.vocab, self.micro_batch, self.seed,
                             self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, int(self.optimizer), flags)
 
@@ -77,11 +80,14 @@ class StepStats:
     pool_bytes: int
     peer_bytes: int
     kernel_launches: int
+    gemm_ms: float = 0.0
+    gemm_flops: float = 0.0
+    gemm_launches: int = 0
 
     @staticmethod
     def of(s: pb_exec_stats) -> "StepStats":
         return StepStats(s.loss, s.step_ms, s.busy_ms, s.pool_slots, s.pool_peak, s.slot_bytes, s.pool_bytes,
-                         s.peer_bytes, s.kernel_launches)
+                         s.peer_bytes, s.kernel_launches, s.gemm_ms, s.gemm_flops, s.gemm_launches)
 
 
 def _i32(x) -> C.POINTER(C.c_int32):
@@ -152,6 +158,12 @@ class DeviceExecutor:
         st = pb_exec_stats()
         check(lib().pb_exec_sync(self._h, self._tl, self.num_passes, C.byref(st)))
         return self.timeline(), StepStats.of(st)
+
+    def set_flags(self, timeline: bool = True, serial: bool = False, gemm_timing: bool = False) -> None:
+        flags = ((PB_FLAG_TIMELINE if timeline else 0) | (PB_FLAG_SERIAL if serial else 0)
+                 | (PB_FLAG_GEMM_TIMING if gemm_timing else 0))
+        check(lib().pb_exec_set_flags(self._h, flags))
+        self.cfg = __import__("dataclasses").replace(self.cfg, timeline=timeline, serial=serial, gemm_timing=gemm_timing)
 
     def timeline(self) -> List[pb.TimedPass]:
         if not self.cfg.timeline:

@@ -1,0 +1,125 @@
+"""Executor parity on the B200: loss and every gradient of one pipeline step
+vs the CPU fp32 oracle on the same (bf16-valued) weights and tokens, for each
+schedule family; measured activation slots vs the reference's exact_peak."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import numerics as N  # noqa: E402
+from paper_2405_15362_b200 import pipeblock as pb  # noqa: E402
+from paper_2405_15362_b200.executor import ModelConfig, PipelineExecutor, synthetic_batch  # noqa: E402
+
+# tolerances: bf16 activations/weights on the GPU vs fp32 on the CPU
+LOSS_RTOL = 5e-3
+GRAD_REL_L2 = 3e-2
+GRAD_COS = 0.999
+
+CFG = ModelConfig(layers=8, hidden=256, heads=2, seq=256, vocab=1024, micro_batch=2, optimizer=False)
+M = 8
+CASES = [("zb-h1", 1), ("1f1b", 2), ("zb-h1", 2), ("v-min", 2), ("v-half", 2), ("v-zb", 2), ("v-half", 4),
+         ("v-min", 4), ("v-zb", 4), ("1f1b", 4)]
+
+_ref_cache = {}
+
+
+def oracle(weights, tokens, labels, S):
+    key = S
+    if key not in _ref_cache:
+        w = {n: torch.from_numpy(v.reshape(N.shapes(CFG, S)[n])) for n, v in weights.items()}
+        _ref_cache[key] = N.reference_step(w, tokens, labels, CFG, S)
+    return _ref_cache[key]
+
+
+@pytest.mark.parametrize("entry,p", CASES)
+def test_step_matches_oracle(entry, p):
+    sched = pb.assemble(pb.build_entry(entry, p), M)
+    S = sched.topology.num_stages
+    ex = PipelineExecutor(CFG, sched)
+    tokens, labels = synthetic_batch(CFG, M)
+    res = ex.step(tokens, labels)
+    names = list(ex.params())
+    weights = {n: ex.get(n, "weight") for n in names}
+    loss_ref, grads_ref = oracle(weights, tokens, labels, S)
+    assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
+    for n in names:
+        g = ex.get(n, "grad")
+        r = grads_ref[n].numpy().ravel()
+        assert N.rel_l2(g, r) < GRAD_REL_L2, (n, N.rel_l2(g, r))
+        assert N.cosine(g, r) > GRAD_COS, (n, N.cosine(g, r))
+    # lifespan-bounded pool: slots allocated == predicted exact_peak, all used
+    peaks = pb.exact_peak(sched)
+    for d, st in res.per_device.items():
+        assert st.pool_slots == int(peaks[d - 1])
+        assert st.pool_peak == int(peaks[d - 1])
+    # measured timeline covers every pass exactly once and respects the grid order per device
+    assert sorted((q.stage, q.kind, q.microbatch) for q in res.timeline) == sorted(
+        (q.stage, q.kind, q.microbatch) for q in sched.passes)
+    for d in range(1, p + 1):
+        mine = [q for q in res.timeline if q.device == d]
+        grid = sched.device_passes(d)
+        assert [(q.stage, q.kind, q.microbatch) for q in mine] == [(q.stage, q.kind, q.microbatch) for q in grid]
+        assert all(a.start + a.duration <= b.start + 1e-3 for a, b in zip(mine, mine[1:]))
+    assert 0.0 <= res.bubble_rate < 1.0
+
+
+def test_schedules_agree_on_gpu():
+    """Same weights (partition-independent init) and tokens: all schedules give the same gradients."""
+    tokens, labels = synthetic_batch(CFG, M)
+    base = None
+    for entry, p in [("zb-h1", 1), ("v-half", 2), ("v-zb", 4), ("1f1b", 4)]:
+        sched = pb.assemble(pb.build_entry(entry, p), M)
+        ex = PipelineExecutor(CFG, sched)
+        res = ex.step(tokens, labels)
+        g = {n: ex.get(n, "grad") for n in ex.params()}
+        g1 = N.rename_for({n: torch.from_numpy(v) for n, v in g.items()}, CFG, sched.topology.num_stages, 1)
+        if base is None:
+            base = (res.loss, g1)
+            continue
+        assert abs(res.loss - base[0]) < 1e-4 * abs(base[0])
+        for n in base[1]:
+            assert N.rel_l2(g1[n], base[1][n]) < 2e-3, (entry, p, n)
+
+
+def test_serial_mode_matches_overlapped():
+    import dataclasses
+    sched = pb.assemble(pb.build_entry("v-half", 4), M)
+    tokens, labels = synthetic_batch(CFG, M)
+    a = PipelineExecutor(CFG, sched)
+    ra = a.step(tokens, labels)
+    b = PipelineExecutor(dataclasses.replace(CFG, serial=True), sched)
+    rb = b.step(tokens, labels)
+    assert abs(ra.loss - rb.loss) < 1e-5 * abs(ra.loss)
+    for n in a.params():
+        assert N.rel_l2(a.get(n, "grad"), b.get(n, "grad")) < 1e-3
+
+
+def test_optimizer_steps_reduce_loss():
+    import dataclasses
+    cfg = dataclasses.replace(CFG, optimizer=True, lr=1e-3)
+    sched = pb.assemble(pb.build_entry("v-zb", 2), M)
+    ex = PipelineExecutor(cfg, sched)
+    # learnable stream: next token = current + 1 (mod V)
+    start = np.random.default_rng(0).integers(0, cfg.vocab, size=(M, 1))
+    seqs = (start + np.arange(cfg.tokens_per_microbatch + 1)) % cfg.vocab
+    tokens = np.ascontiguousarray(seqs[:, :-1].astype(np.int32))
+    labels = np.ascontiguousarray(seqs[:, 1:].astype(np.int32))
+    losses = [ex.step(tokens, labels).loss for _ in range(8)]
+    assert losses[-1] < 0.5 * losses[0], losses
+    assert all(np.isfinite(losses))
+
+
+def test_device_inputs_equal_host_inputs():
+    sched = pb.assemble(pb.build_entry("v-min", 2), M)
+    tokens, labels = synthetic_batch(CFG, M)
+    ex = PipelineExecutor(CFG, sched)
+    r1 = ex.step(tokens, labels, on_host=True)
+    g1 = ex.get("s1.emb", "grad")
+    for d in ex.devices:
+        d.zero_grads()
+    tt, ll = torch.from_numpy(tokens).cuda(), torch.from_numpy(labels).cuda()
+    torch.cuda.synchronize()
+    r2 = ex.step(tt, ll, on_host=False)
+    assert abs(r1.loss - r2.loss) < 1e-6 * abs(r1.loss)
+    assert N.rel_l2(ex.get("s1.emb", "grad"), g1) < 1e-5
