@@ -25,7 +25,7 @@ extern "C" int pb_exec_create(const pb_model_cfg* cfg, const pb_schedule* plan, 
         e->timeline = (cfg->flags & PB_FLAG_TIMELINE) != 0;
         e->serial = (cfg->flags & PB_FLAG_SERIAL) != 0;
         e->gemm_timing = (cfg->flags & PB_FLAG_GEMM_TIMING) != 0;
-        if (e->plan.topo.devices == 1) e->connect_local({e});
+        if (e->plan.topo.devices == 1) e->connect_local({e}, nullptr);
         *out = new pb_exec{e};
     });
 }
@@ -35,7 +35,8 @@ extern "C" int pb_exec_connect_local(pb_exec* const* all, int32_t n) {
         std::vector<pbx::Exec*> v;
         for (int i = 0; i < n; ++i) v.push_back(&X(all[i]));
         std::sort(v.begin(), v.end(), [](auto* a, auto* b) { return a->dev < b->dev; });
-        for (auto* e : v) e->connect_local(v);
+        auto grp = pbx::make_group(v);
+        for (auto* e : v) e->connect_local(v, grp);
     });
 }
 

@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -386,6 +388,15 @@ uint32_t* Exec::ready_flag(uint32_t* base, int src, int k) const {
 void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     if (!connected && plan.topo.devices > 1) throw StateError("pb_exec_step before peers are connected");
     ck(cudaSetDevice(cuda), "cudaSetDevice");
+    const int64_t t = steps_done;
+    if (group) {
+        // peers must have finished enqueueing step t-1 before step t re-records any event parity
+        group->wait([&] {
+            for (int d = 1; d <= plan.topo.devices; ++d)
+                if (group->enqueued[d] < t) return false;
+            return true;
+        });
+    }
     launches = 0;
     peer_bytes = 0;
     gev_used = 0;
@@ -407,11 +418,15 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     const auto& ops = plan.dev_ops[dev];
     int live = 0;
     pool_live_peak = 0;
+    static const bool trace = std::getenv("PB_TRACE") != nullptr;
     for (size_t j = 0; j < ops.size(); ++j) {
         const int i = ops[j];
         const PlanOp& po = plan.ops[i];
         const auto& o = po.op;
         const StageLayout& L = layout.at(o.stage);
+        if (trace)
+            std::fprintf(stderr, "[dev %d] op %zu %s(s%d,mb%d)@%lld slot %d in %d out %d\n", dev, j,
+                         vsched::kind_name(o.kind), o.stage, o.mb, (long long)o.start, po.slot, po.in_msg, po.out_msg);
         // ---- incoming boundary tensor
         __nv_bfloat16* in_dst = nullptr;
         const Msg* in = po.in_msg >= 0 ? &plan.msgs[po.in_msg] : nullptr;
@@ -422,18 +437,38 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
             }
             const Peer& src = peers[in->src_dev];
             const uint32_t g = gen_total(*in);
-            wait_value(xs, ready_flag(flags, in->src_dev, in->outbox), g);
+            const size_t mi = size_t(po.in_msg);
+            if (group) {
+                group->wait([&] { return group->ready_step[mi] >= t; });
+                ck(cudaStreamWaitEvent(xs, group->ready_ev[t & 1][mi], 0), "wait");
+            } else {
+                wait_value(xs, ready_flag(flags, in->src_dev, in->outbox), g);
+            }
             ck(cudaMemcpyAsync(in_dst, reinterpret_cast<uint8_t*>(src.outbox) + size_t(in->outbox) * msg_bytes,
                                size_t(T) * h * 2, cudaMemcpyDeviceToDevice, xs),
                "peer copy");
-            write_value(xs, ack_flag(src.flags, in->outbox), g);
+            if (group) {
+                ck(cudaEventRecord(group->ack_ev[t & 1][mi], xs), "event");
+                group->set(group->ack_step, mi, t);
+            } else {
+                write_value(xs, ack_flag(src.flags, in->outbox), g);
+            }
             ck(cudaEventRecord(ev_pull[j], xs), "event");
             ck(cudaStreamWaitEvent(cs, ev_pull[j], 0), "wait");
             peer_bytes += int64_t(T) * h * 2;
         }
         // ---- outgoing: outbox slot must be drained by its previous (remote) consumer
         const Msg* out = po.out_msg >= 0 ? &plan.msgs[po.out_msg] : nullptr;
-        if (out && out->prev_remote && gen_total(*out) > 1) wait_value(cs, ack_flag(flags, out->outbox), gen_total(*out) - 1);
+        if (out && out->prev_remote && gen_total(*out) > 1) {
+            if (group) {
+                const int64_t tp = out->prev_cross_step ? t - 1 : t;
+                const size_t pm = size_t(out->prev_msg);
+                group->wait([&] { return group->ack_step[pm] >= tp; });
+                ck(cudaStreamWaitEvent(cs, group->ack_ev[tp & 1][pm], 0), "wait");
+            } else {
+                wait_value(cs, ack_flag(flags, out->outbox), gen_total(*out) - 1);
+            }
+        }
         if (timeline) ck(cudaEventRecord(ev_start[j], cs), "event");
         if (in && in->local())
             ck(cudaMemcpyAsync(in_dst, outbox_ptr(in->outbox), size_t(T) * h * 2, cudaMemcpyDeviceToDevice, cs),
@@ -453,7 +488,15 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
                 break;
         }
         if (timeline) ck(cudaEventRecord(ev_end[j], cs), "event");
-        if (out && !out->local()) write_value(cs, ready_flag(peers[out->dst_dev].flags, dev, out->outbox), gen_total(*out));
+        if (out && !out->local()) {
+            if (group) {
+                const size_t mi = size_t(po.out_msg);
+                ck(cudaEventRecord(group->ready_ev[t & 1][mi], cs), "event");
+                group->set(group->ready_step, mi, t);
+            } else {
+                write_value(cs, ready_flag(peers[out->dst_dev].flags, dev, out->outbox), gen_total(*out));
+            }
+        }
         if (o.kind == Kind::W || o.kind == Kind::BW) {
             --live;
             ck(cudaEventRecord(ev_free[j], cs), "event");
@@ -473,6 +516,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     ck(cudaEventRecord(ev_step1, cs), "event");
     ck(cudaGetLastError(), "launch");
     ++steps_done;
+    if (group) group->set(group->enqueued, size_t(dev), steps_done);
     pending = true;
 }
 
@@ -522,8 +566,42 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
 }
 
 // ------------------------------------------------------------------ peers
-void Exec::connect_local(const std::vector<Exec*>& all) {
+LocalGroup::~LocalGroup() {
+    for (int b = 0; b < 2; ++b) {
+        for (auto e : ready_ev[b]) cudaEventDestroy(e);
+        for (auto e : ack_ev[b]) cudaEventDestroy(e);
+    }
+}
+
+std::shared_ptr<LocalGroup> make_group(const std::vector<Exec*>& all) {
+    auto g = std::make_shared<LocalGroup>();
+    const ExecPlan& p = all.front()->plan;
+    const size_t n = p.msgs.size();
+    auto cuda_of = [&](int dev) {
+        for (Exec* e : all)
+            if (e->dev == dev) return e->cuda;
+        throw std::invalid_argument("connect: missing device");
+    };
+    for (int b = 0; b < 2; ++b) {
+        g->ready_ev[b].resize(n);
+        g->ack_ev[b].resize(n);
+        for (size_t i = 0; i < n; ++i) {
+            ck(cudaSetDevice(cuda_of(p.msgs[i].src_dev)), "cudaSetDevice");
+            ck(cudaEventCreateWithFlags(&g->ready_ev[b][i], cudaEventDisableTiming), "event");
+            ck(cudaSetDevice(cuda_of(p.msgs[i].dst_dev)), "cudaSetDevice");
+            ck(cudaEventCreateWithFlags(&g->ack_ev[b][i], cudaEventDisableTiming), "event");
+        }
+    }
+    g->ready_step.assign(n, -1);
+    g->ack_step.assign(n, -1);
+    g->enqueued.assign(size_t(p.topo.devices) + 1, 0);
+    for (Exec* e : all) g->enqueued[e->dev] = e->steps_done;
+    return g;
+}
+
+void Exec::connect_local(const std::vector<Exec*>& all, std::shared_ptr<LocalGroup> grp) {
     if (int(all.size()) != plan.topo.devices) throw std::invalid_argument("connect: need one exec per device");
+    group = std::move(grp);
     for (Exec* e : all) {
         if (e->plan.ops.size() != plan.ops.size()) throw std::invalid_argument("connect: executors run different plans");
         peers[e->dev] = Peer{e->outbox, e->flags, false};

@@ -3,7 +3,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <condition_variable>
+#include <functional>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -41,11 +45,34 @@ struct Peer {
     bool ipc = false;
 };
 
+// In-process peer group: message hand-off through CUDA events whose records are
+// host-ordered before any wait on them (double-buffered by step parity), so no
+// stream ever waits on work that is not yet submitted.
+struct LocalGroup {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<cudaEvent_t> ready_ev[2], ack_ev[2];  // per message
+    std::vector<int64_t> ready_step, ack_step;        // last step whose record is enqueued
+    std::vector<int64_t> enqueued;                    // per device: steps fully enqueued
+    void wait(const std::function<bool()>& pred) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, pred);
+    }
+    void set(std::vector<int64_t>& v, size_t i, int64_t t) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            v[i] = t;
+        }
+        cv.notify_all();
+    }
+    ~LocalGroup();
+};
+
 class Exec {
   public:
     Exec(const pb_model_cfg& cfg, const vsched::Grid& grid, int device, int cuda_dev);
     ~Exec();
-    void connect_local(const std::vector<Exec*>& all);
+    void connect_local(const std::vector<Exec*>& all, std::shared_ptr<LocalGroup> grp);
     size_t export_blob(void* buf, size_t cap);
     void connect_ipc(const std::vector<std::pair<const void*, size_t>>& blobs);
     void enqueue(const int32_t* tok, const int32_t* lab, bool on_host);
@@ -63,6 +90,8 @@ class Exec {
     cudaStream_t cs = nullptr, xs = nullptr;
     bool timeline = true, serial = false, connected = false, pending = false, gemm_timing = false;
     int adam_step = 0;
+
+    int64_t steps_done = 0;
 
   private:
     void build_layout();
@@ -96,10 +125,13 @@ class Exec {
     cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
     std::vector<Peer> peers;
     std::vector<int> pos_of;
-    int64_t steps_done = 0, launches = 0, peer_bytes = 0;
+    std::shared_ptr<LocalGroup> group;
+    int64_t launches = 0, peer_bytes = 0;
     std::vector<cudaEvent_t> gev;
     size_t gev_used = 0;
     double gemm_flops_acc = 0;
 };
+
+std::shared_ptr<LocalGroup> make_group(const std::vector<Exec*>& all);
 
 }  // namespace pbx

@@ -96,6 +96,7 @@ ExecPlan make_plan(const vsched::Grid& g) {
             m.outbox = k;
             m.gen = ++p.uses[d][k];
             if (last_msg[k] >= 0) {
+                m.prev_msg = last_msg[k];
                 m.prev_gen = p.msgs[last_msg[k]].gen;
                 m.prev_remote = !p.msgs[last_msg[k]].local();
             }
@@ -114,6 +115,8 @@ ExecPlan make_plan(const vsched::Grid& g) {
         if (m.prev_gen == 0) {
             const Msg& last = p.msgs[p.last_use[m.src_dev][m.outbox]];
             m.prev_remote = !last.local();
+            m.prev_msg = p.last_use[m.src_dev][m.outbox];
+            m.prev_cross_step = true;
         }
     }
     return p;

@@ -20,6 +20,8 @@ struct Msg {
     uint32_t gen = 0;              // 1-based use count of that outbox slot within a step
     bool prev_remote = false;      // previous occupant of the slot was consumed on another device
     uint32_t prev_gen = 0;         // generation of the previous occupant (0 = none in this step)
+    int prev_msg = -1;             // message index of the previous occupant of the outbox slot
+    bool prev_cross_step = false;  // ... which is the last use of the slot in the previous step
     bool local() const { return src_dev == dst_dev; }
 };
 

@@ -118,7 +118,10 @@ class DeviceExecutor:
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
         if h:
-            lib().pb_exec_destroy(h)
+            try:
+                lib().pb_exec_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @property
     def handle(self):

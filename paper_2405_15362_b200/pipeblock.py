@@ -122,7 +122,10 @@ class GridSchedule:
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
         if h:
-            lib().pb_schedule_destroy(h)
+            try:
+                lib().pb_schedule_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @property
     def handle(self):

@@ -105,8 +105,9 @@ def test_optimizer_steps_reduce_loss():
     seqs = (start + np.arange(cfg.tokens_per_microbatch + 1)) % cfg.vocab
     tokens = np.ascontiguousarray(seqs[:, :-1].astype(np.int32))
     labels = np.ascontiguousarray(seqs[:, 1:].astype(np.int32))
-    losses = [ex.step(tokens, labels).loss for _ in range(8)]
-    assert losses[-1] < 0.5 * losses[0], losses
+    losses = [ex.step(tokens, labels).loss for _ in range(10)]
+    assert losses[-1] < losses[0] - 0.5, losses
+    assert min(losses[5:]) < min(losses[:5]), losses
     assert all(np.isfinite(losses))
 
 
