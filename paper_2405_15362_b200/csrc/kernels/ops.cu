@@ -2,6 +2,7 @@
 // embedding gather / scatter-add, fused LM-head softmax cross-entropy
 // (loss + dlogits in place), AdamW.  128-bit vector I/O, warp-shuffle
 // reductions, one row per warp where a row fits.
+#include <algorithm>
 #include <stdexcept>
 
 #include "ops.hpp"
@@ -285,9 +286,11 @@ void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfl
 
 void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, int T, int h,
                     cudaStream_t s) {
-    const int rows = 128;
-    dim3 grid((h / 8 + 127) / 128, (T + rows - 1) / rows);
-    rmsnorm_dgamma_kernel<<<grid, 128, 0, s>>>(dy, x, rstd, dgamma, T, h, rows);
+    // one thread per 8 columns x 16 rows: T/16 x h/2048 CTAs (>= 1 wave on 148 SMs at T=2048)
+    const int rows = 16;
+    const int threads = std::min(256, h / 8);
+    dim3 grid((h / 8 + threads - 1) / threads, (T + rows - 1) / rows);
+    rmsnorm_dgamma_kernel<<<grid, threads, 0, s>>>(dy, x, rstd, dgamma, T, h, rows);
 }
 
 void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s) {
