@@ -21,9 +21,14 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
 
 /* causal attention, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T] (base-2 LSE of scaled scores) */
 int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
+/* same on tcgen05/TMEM (the executor's forward attention); seq % 128 == 0 */
+int pbt_attn_fwd_tc(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
 /* dqkv [T,3h]; dsum [heads,T], dq_acc [T,h] fp32 scratch */
 int pbt_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum, float* dq_acc,
                  void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream);
+/* same on tcgen05/TMEM (the executor's backward attention) */
+int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum, float* dq_acc,
+                    void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream);
 int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h, void* stream);
 int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
                     float* dgamma, int32_t T, int32_t h, void* stream);

@@ -87,3 +87,17 @@ extern "C" int pbt_adamw(float* w, void* wb, float* g, float* m, float* v, int64
         cuda_check("pbt_adamw");
     });
 }
+extern "C" int pbt_attn_fwd_tc(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads,
+                               void* stream) {
+    return pbx::guard([&] {
+        pbk::attn_fwd_tc(BF(qkv), BFM(out), lse2, batch, seq, heads, ST(stream));
+        cuda_check("pbt_attn_fwd_tc");
+    });
+}
+extern "C" int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum,
+                               float* dq_acc, void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream) {
+    return pbx::guard([&] {
+        pbk::attn_bwd_tc(BF(qkv), BF(out), BF(dout), lse2, dsum, dq_acc, BFM(dqkv), batch, seq, heads, ST(stream));
+        cuda_check("pbt_attn_bwd_tc");
+    });
+}

@@ -308,7 +308,7 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         __nv_bfloat16* xo = (l == Lc - 1 && s < S) ? out : bf(slot, L.x[l + 1]);
         pbk::rmsnorm_fwd(x, W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs);
         gemm(T, 3 * h, h, bf(slot, y.a), false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE);
-        pbk::attn_fwd(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs);
+        pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs);
         gemm(T, h, h, bf(slot, y.o), false, W(w.wo), false, bf(slot, y.x1), pbk::EPI_RESID, x);
         pbk::rmsnorm_fwd(bf(slot, y.x1), W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs);
         gemm(T, 4 * h, h, bf(slot, y.b), false, W(w.w1), false, bf(slot, y.u), pbk::EPI_GELU, nullptr,
@@ -348,7 +348,7 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs);
         pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), T, h, cs);
         gemm(T, h, h, bf(slot, y.dx1), false, W(w.wo), true, scratch, pbk::EPI_STORE);
-        pbk::attn_bwd(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
+        pbk::attn_bwd_tc(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
                       seq, H, cs);
         gemm(T, h, 3 * h, bf(slot, y.dqkv), false, W(w.wqkv), true, scratch, pbk::EPI_STORE);
         pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs);

@@ -445,6 +445,15 @@ void attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int bat
     attn_fwd_kernel<<<grid, 128, 5 * 16384, s>>>(qkv, out, lse2, seq, heads, batch * seq, 0.08838834764831845f);
 }
 
+void attn_bwd_pre(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* dsum, float* dq_acc, int heads, int T,
+                  cudaStream_t s) {
+    attn_bwd_pre_kernel<<<T, 256, 0, s>>>(dout, out, dsum, dq_acc, heads, T);
+}
+
+void attn_dq_store(const float* dq_acc, __nv_bfloat16* dqkv, int heads, int T, cudaStream_t s) {
+    attn_dq_store_kernel<<<T, 256, 0, s>>>(dq_acc, dqkv, heads, 0.08838834764831845f);
+}
+
 void attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
               float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s) {
     constexpr int kSmem = 6 * 16384 + 8192 + 2 * 128 * 4;

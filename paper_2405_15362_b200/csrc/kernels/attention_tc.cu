@@ -1,0 +1,520 @@
+// Causal flash attention forward on 5th-gen tensor cores (sm_100a).
+//
+// One CTA per (128-query tile, head, sequence); 192 threads:
+//   warp 0     TMA: Q tile once, then a 2-stage ring of K/V tiles (128 keys x 128 d)
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//                S_j  = Q K_j^T      (M=128 q, N=128 keys, K=128 d)  -> TMEM S[j%2]
+//                O   += P_j V_j      (M=128 q, N=128 d,   K=128 keys) -> TMEM O
+//   warps 2-5  softmax: thread = query row = TMEM lane; reads its S row with
+//              tcgen05.ld, online softmax in registers (no shuffles), writes P
+//              (bf16, 128B-swizzled K-major) to smem for the PV MMA.
+// S_{j+1} is computed while the softmax of S_j runs (two S buffers).  The
+// running max is rescaled lazily: O (in TMEM) is only rescaled when a row's
+// max grows by more than 2^8, which keeps the result exact (O and the row sum
+// share the same stale max) and avoids a TMEM round trip per tile.
+#include <stdexcept>
+
+#include "ops.hpp"
+#include "sm100.cuh"
+
+namespace pbk {
+
+namespace {
+
+constexpr int D = 128;
+constexpr int BQ = 128;
+constexpr int BK = 128;
+constexpr int kTile = BQ * D * 2;  // 32 KB: two 128B-swizzled atoms of [128 rows][64]
+constexpr int kStages = 2;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct FwdSmem {
+    static constexpr int q = 0;
+    static constexpr int k0 = kTile;
+    static constexpr int v0 = k0 + kStages * kTile;
+    static constexpr int p = v0 + kStages * kTile;
+    static constexpr int bars = p + kTile;
+    static constexpr int total = bars + 256 + 1024;
+};
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// byte offset of (row, col) in a [128 rows][128 cols] bf16 tile stored as two
+// 128B-swizzled K-major atoms (cols 0-63, 64-127)
+__device__ __forceinline__ uint32_t sw128(int row, int col) {
+    return uint32_t((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2);
+}
+
+__global__ void __launch_bounds__(192, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
+                       float* __restrict__ lse2, int seq, int H, int T, float scale) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::bars);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;   // [2]
+    uint64_t* kv_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;    // [2]
+    uint64_t* s_free = bars + 7;    // [2]
+    uint64_t* p_full = bars + 9;
+    uint64_t* p_empty = bars + 10;
+    uint64_t* o_full = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const uint32_t warp = warp_id();
+    const int nqb = seq / BQ;
+    const int qb = nqb - 1 - int(blockIdx.x);  // heaviest tiles first
+    const int head = blockIdx.y, b = blockIdx.z;
+    const int row0 = b * seq + qb * BQ;        // first token row of this Q tile
+    const int nkv = qb + 1;                    // causal: key tiles 0..qb
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 4);
+        }
+        mbar_init(p_full, 4);
+        mbar_init(p_empty, 1);
+        mbar_init(o_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;  // cols [0,128) S0, [128,256) S1, [256,384) O
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const int cq = head * D, ck = H * D + head * D, cv = 2 * H * D + head * D;
+            mbar_expect_tx(q_full, kTile);
+            tma_load_2d(sm + FwdSmem::q, &tm, q_full, cq, row0);
+            tma_load_2d(sm + FwdSmem::q + 16384, &tm, q_full, cq + 64, row0);
+            for (int j = 0; j < nkv; ++j) {
+                const int st = j & 1;
+                if (j >= kStages) mbar_wait(&kv_empty[st], ((j - kStages) >> 1) & 1);
+                mbar_expect_tx(&kv_full[st], 2 * kTile);
+                const int kr = b * seq + j * BK;
+                uint8_t* ks = sm + FwdSmem::k0 + st * kTile;
+                uint8_t* vs = sm + FwdSmem::v0 + st * kTile;
+                tma_load_2d(ks, &tm, &kv_full[st], ck, kr);
+                tma_load_2d(ks + 16384, &tm, &kv_full[st], ck + 64, kr);
+                tma_load_2d(vs, &tm, &kv_full[st], cv, kr);
+                tma_load_2d(vs + 16384, &tm, &kv_full[st], cv + 64, kr);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t idesc_o = idesc_bf16(128, 128, false, true);
+        const uint32_t sq = smem_u32(sm + FwdSmem::q);
+        const uint32_t sp = smem_u32(sm + FwdSmem::p);
+        mbar_wait(q_full, 0);
+        auto issue_pv = [&](int j) {  // O += P_j V_j
+            mbar_wait(p_full, j & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t sv = smem_u32(sm + FwdSmem::v0 + (j & 1) * kTile);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t ad = sdesc(sp + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bd = sdesc(sv + kk * 2048, 16384, 1024);
+                    tc_mma(tmem + 256, ad, bd, idesc_o, (j | kk) != 0);
+                }
+                tc_commit(&kv_empty[j & 1]);
+                tc_commit(p_empty);
+            }
+            __syncwarp();
+        };
+        for (int j = 0; j < nkv; ++j) {
+            const int st = j & 1;
+            mbar_wait(&kv_full[st], (j >> 1) & 1);
+            if (j >= 2) mbar_wait(&s_free[st], ((j - 2) >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t sk = smem_u32(sm + FwdSmem::k0 + st * kTile);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t ad = sdesc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bd = sdesc(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+                    tc_mma(tmem + st * 128, ad, bd, idesc_s, kk != 0);
+                }
+                tc_commit(&s_full[st]);
+            }
+            __syncwarp();
+            if (j >= 1) issue_pv(j - 1);
+        }
+        issue_pv(nkv - 1);
+        if (elect_one()) tc_commit(o_full);
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ softmax
+        const uint32_t q4 = warp & 3;
+        const int r = int(q4 * 32 + lane_id());  // query row in tile == TMEM lane
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const float sl2 = scale * kLog2e;
+        float m_used = -INFINITY, l = 0.f;
+        uint8_t* sp = sm + FwdSmem::p;
+        for (int j = 0; j < nkv; ++j) {
+            const int st = j & 1;
+            mbar_wait(&s_full[st], (j >> 1) & 1);
+            tc_fence_after();
+            float s[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + st * 128 + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&s_free[st]);
+            float mx = -INFINITY;
+            const bool diag = (j == nkv - 1);
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                float v = s[c] * sl2;
+                if (diag && c > r) v = -INFINITY;
+                s[c] = v;
+                mx = fmaxf(mx, v);
+            }
+            const float m_new = fmaxf(m_used, mx);
+            bool rescale = (j > 0) && (m_new > m_used + 8.f);
+            if (j > 0) {
+                mbar_wait(p_empty, (j - 1) & 1);  // PV_{j-1} done: P smem free, O stable
+                tc_fence_after();
+            }
+            if (__any_sync(0xffffffff, rescale)) {
+                const float f = rescale ? exp2f(m_used - m_new) : 1.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float o[32];
+                    tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tmem + lane_base + 256 + c * 32, o);
+                }
+                tmem_st_wait();
+                if (rescale) {
+                    l *= f;
+                    m_used = m_new;
+                }
+            }
+            if (j == 0) m_used = m_new;
+            float rs = 0.f;
+#pragma unroll
+            for (int c8 = 0; c8 < 16; ++c8) {
+                float p[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    p[e] = exp2f(s[c8 * 8 + e] - m_used);
+                    rs += p[e];
+                }
+                uint4 w = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
+                                     pack_bf16(p[6], p[7]));
+                *reinterpret_cast<uint4*>(sp + sw128(r, c8 * 8)) = w;
+            }
+            l += rs;
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(p_full);
+        }
+        // epilogue: O / l -> bf16
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        const float inv = 1.f / l;
+        __nv_bfloat16* orow = out + size_t(row0 + r) * (H * D) + head * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float o[32];
+            tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                                    pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+        }
+        lse2[size_t(head) * T + row0 + r] = m_used + log2f(l);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<512>(tmem);
+    }
+}
+
+
+// ------------------------------------------------------------------ backward
+// One CTA per (128-key tile kb, head, sequence), looping over query tiles qb >= kb:
+//   S^T  = K Q^T,  dP^T = V dO^T                       -> TMEM [0,128), [128,256)
+//   compute warps (thread = key row): P^T = exp2(S^T*c - lse2[q]), dS^T = P^T (dP^T - D[q])
+//                                     -> bf16 smem (128B-swizzled, rows = keys)
+//   dV += P^T dO,  dK += dS^T Q                          -> TMEM [256,384), [384,512)
+//   dQ_tile = dS K  (A = dS^T read MN-major)             -> TMEM [0,128), then red.global.add.v4.f32
+struct BwdSmem {
+    static constexpr int k = 0;
+    static constexpr int v = k + kTile;
+    static constexpr int q = v + kTile;
+    static constexpr int dO = q + kTile;
+    static constexpr int pt = dO + kTile;
+    static constexpr int dst = pt + kTile;
+    static constexpr int lse = dst + kTile;      // [2][2][128] floats
+    static constexpr int bars = lse + 2048;
+    static constexpr int total = bars + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                       const float* __restrict__ lse2, const float* __restrict__ dsum, float* __restrict__ dq_acc,
+                       __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::bars);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* qdo_full = bars + 1;
+    uint64_t* qdo_empty = bars + 2;
+    uint64_t* s_full = bars + 3;
+    uint64_t* ds_full = bars + 4;
+    uint64_t* dq_full = bars + 5;
+    uint64_t* s_free = bars + 6;
+    uint64_t* dkv_full = bars + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    float* sL = reinterpret_cast<float*>(sm + BwdSmem::lse);
+
+    const uint32_t warp = warp_id();
+    const int nqb = seq / BQ;
+    const int kb = int(blockIdx.x);  // kb = 0 has the most query tiles: dispatched first
+    const int head = blockIdx.y, b = blockIdx.z;
+    const int tok0 = b * seq;
+    const int nq = nqb - kb;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm_qkv);
+        tma_prefetch(&tm_do);
+        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 6) ? 4 : 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const int ck = H * D + head * D, cv = 2 * H * D + head * D, cq = head * D;
+            const int kr = tok0 + kb * BK;
+            mbar_expect_tx(kv_full, 2 * kTile);
+            tma_load_2d(sm + BwdSmem::k, &tm_qkv, kv_full, ck, kr);
+            tma_load_2d(sm + BwdSmem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
+            tma_load_2d(sm + BwdSmem::v, &tm_qkv, kv_full, cv, kr);
+            tma_load_2d(sm + BwdSmem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
+            for (int i = 0; i < nq; ++i) {
+                if (i > 0) mbar_wait(qdo_empty, (i - 1) & 1);
+                const int qr = tok0 + (kb + i) * BQ;
+                mbar_expect_tx(qdo_full, 2 * kTile);
+                tma_load_2d(sm + BwdSmem::q, &tm_qkv, qdo_full, cq, qr);
+                tma_load_2d(sm + BwdSmem::q + 16384, &tm_qkv, qdo_full, cq + 64, qr);
+                tma_load_2d(sm + BwdSmem::dO, &tm_do, qdo_full, head * D, qr);
+                tma_load_2d(sm + BwdSmem::dO + 16384, &tm_do, qdo_full, head * D + 64, qr);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
+        constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
+        const uint32_t sk = smem_u32(sm + BwdSmem::k), sv = smem_u32(sm + BwdSmem::v);
+        const uint32_t sq = smem_u32(sm + BwdSmem::q), sdo = smem_u32(sm + BwdSmem::dO);
+        const uint32_t spt = smem_u32(sm + BwdSmem::pt), sdst = smem_u32(sm + BwdSmem::dst);
+        mbar_wait(kv_full, 0);
+        for (int i = 0; i < nq; ++i) {
+            mbar_wait(qdo_full, i & 1);
+            if (i > 0) mbar_wait(s_free, (i - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
+                }
+                tc_commit(s_full);
+            }
+            __syncwarp();
+            mbar_wait(ds_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 256, sdesc(spt + o, 16, 1024), sdesc(sdo + kk * 2048, 16384, 1024), id_kmn,
+                           (i | kk) != 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
+                           (i | kk) != 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma(tmem + 0, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
+                           id_mnmn, kk != 0);
+                tc_commit(qdo_empty);
+                tc_commit(dq_full);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) tc_commit(dkv_full);
+        __syncwarp();
+    } else {
+        const uint32_t q4 = warp & 3;
+        const int r = int(q4 * 32 + lane_id());
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const float sl2 = scale * kLog2e;
+        uint8_t* spt = sm + BwdSmem::pt;
+        uint8_t* sdst = sm + BwdSmem::dst;
+        const int key = kb * BK + r;  // key index within the sequence
+        for (int i = 0; i < nq; ++i) {
+            const int qb = kb + i;
+            float* Lb = sL + (i & 1) * 256;
+            Lb[r] = lse2[size_t(head) * T + tok0 + qb * BQ + r];
+            Lb[128 + r] = dsum[size_t(head) * T + tok0 + qb * BQ + r];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            const bool diag = (qb == kb);
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + c * 32, sv);
+                tmem_ld32(tmem + lane_base + 128 + c * 32, dp);
+                tmem_ld_wait();
+                float p[32], ds[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int ql = c * 32 + e;
+                    float v = exp2f(sv[e] * sl2 - Lb[ql]);
+                    if (diag && key > qb * BQ + ql) v = 0.f;
+                    p[e] = v;
+                    ds[e] = v * (dp[e] - Lb[128 + ql]);
+                }
+#pragma unroll
+                for (int e8 = 0; e8 < 4; ++e8) {
+                    const int col = c * 32 + e8 * 8;
+                    *reinterpret_cast<uint4*>(spt + sw128(r, col)) =
+                        make_uint4(pack_bf16(p[e8 * 8], p[e8 * 8 + 1]), pack_bf16(p[e8 * 8 + 2], p[e8 * 8 + 3]),
+                                   pack_bf16(p[e8 * 8 + 4], p[e8 * 8 + 5]), pack_bf16(p[e8 * 8 + 6], p[e8 * 8 + 7]));
+                    *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
+                        make_uint4(pack_bf16(ds[e8 * 8], ds[e8 * 8 + 1]), pack_bf16(ds[e8 * 8 + 2], ds[e8 * 8 + 3]),
+                                   pack_bf16(ds[e8 * 8 + 4], ds[e8 * 8 + 5]), pack_bf16(ds[e8 * 8 + 6], ds[e8 * 8 + 7]));
+                }
+            }
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(ds_full);
+            // dQ tile: thread = query row r
+            mbar_wait(dq_full, i & 1);
+            tc_fence_after();
+            float* dqrow = dq_acc + size_t(tok0 + qb * BQ + r) * (H * D) + head * D;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                float v[32];
+                tmem_ld32(tmem + lane_base + c * 32, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c * 32 + e * 4),
+                                 "f"(v[4 * e]), "f"(v[4 * e + 1]), "f"(v[4 * e + 2]), "f"(v[4 * e + 3])
+                                 : "memory");
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(s_free);
+        }
+        // dV, dK rows (thread = key row)
+        mbar_wait(dkv_full, 0);
+        tc_fence_after();
+        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            float v[32], k[32];
+            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
+            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
+            tmem_ld_wait();
+            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
+            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                dv[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
+                                   pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
+                dk[e] = make_uint4(pack_bf16(k[8 * e] * scale, k[8 * e + 1] * scale),
+                                   pack_bf16(k[8 * e + 2] * scale, k[8 * e + 3] * scale),
+                                   pack_bf16(k[8 * e + 4] * scale, k[8 * e + 5] * scale),
+                                   pack_bf16(k[8 * e + 6] * scale, k[8 * e + 7] * scale));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<512>(tmem);
+    }
+}
+
+}  // namespace
+
+void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
+                 float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s) {
+    if (seq % 128) throw std::invalid_argument("attention: seq must be a multiple of 128");
+    attn_bwd_pre(dout, out, dsum, dq_acc, heads, batch * seq, s);
+    static bool once = [] {
+        cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::total);
+        return true;
+    }();
+    (void)once;
+    const int T = batch * seq;
+    const CUtensorMap tq = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
+    const CUtensorMap td = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 128);
+    dim3 grid(seq / BK, heads, batch);
+    attn_bwd_tc_kernel<<<grid, 192, BwdSmem::total, s>>>(tq, td, lse2, dsum, dq_acc, dqkv, seq, heads, T,
+                                                        0.08838834764831845f);
+    attn_dq_store(dq_acc, dqkv, heads, T, s);
+}
+
+void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int batch, int seq, int heads,
+                 cudaStream_t s) {
+    if (seq % 128) throw std::invalid_argument("attention: seq must be a multiple of 128");
+    static bool once = [] {
+        cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::total);
+        return true;
+    }();
+    (void)once;
+    const int T = batch * seq;
+    const CUtensorMap tm = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
+    dim3 grid(seq / BQ, heads, batch);
+    attn_fwd_tc_kernel<<<grid, 192, FwdSmem::total, s>>>(tm, out, lse2, seq, heads, T, 0.08838834764831845f);
+}
+
+}  // namespace pbk

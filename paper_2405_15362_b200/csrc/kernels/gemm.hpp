@@ -1,5 +1,6 @@
 // Host interface of the sm_100a kernels (kernels/*.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -34,5 +35,8 @@ struct GemmArgs {
 void gemm(const GemmArgs& g, cudaStream_t s);
 int gemm_bn(const GemmArgs& g);
 int num_sms();
+// 2-D bf16 tensor map [outer][inner], row stride ld elements, box_inner x box_outer, 128B swizzle
+CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                     uint32_t box_outer);
 
 }  // namespace pbk

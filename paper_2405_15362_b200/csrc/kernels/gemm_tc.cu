@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+}  // namespace
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -254,6 +256,8 @@ CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t 
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     return m;
 }
+
+namespace {
 
 int sm_count() {
     static int n = [] {

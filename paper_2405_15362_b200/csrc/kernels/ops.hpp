@@ -12,9 +12,18 @@ namespace pbk {
 // causal MHA, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T]
 void attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int batch, int seq, int heads,
               cudaStream_t s);
+// same contract on tcgen05/TMEM (attention_tc.cu); seq % 128 == 0
+void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int batch, int seq, int heads,
+                 cudaStream_t s);
 // dqkv [T,3h] from dout [T,h]; dsum [heads,T] and dq_acc [T,h] fp32 are scratch
 void attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
               float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s);
+// same contract on tcgen05/TMEM (attention_tc.cu); seq % 128 == 0
+void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
+                 float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s);
+void attn_bwd_pre(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* dsum, float* dq_acc, int heads, int T,
+                  cudaStream_t s);
+void attn_dq_store(const float* dq_acc, __nv_bfloat16* dqkv, int heads, int T, cudaStream_t s);
 
 void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
                  cudaStream_t s);

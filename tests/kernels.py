@@ -87,3 +87,21 @@ def cross_entropy(logits, labels, loss, scale):
 def adamw(w, wb, g, m, v, lr, b1, b2, eps, wd, step):
     _lib.check(_lib.lib().pbt_adamw(_f(w), _p(wb), _f(g), _f(m), _f(v), C.c_int64(w.numel()), C.c_float(lr),
                                     C.c_float(b1), C.c_float(b2), C.c_float(eps), C.c_float(wd), step, _s()))
+
+
+def attn_fwd_tc(qkv, batch, seq, heads):
+    T = batch * seq
+    out = torch.empty(T, heads * 128, device="cuda", dtype=torch.bfloat16)
+    lse2 = torch.empty(heads, T, device="cuda", dtype=torch.float32)
+    _lib.check(_lib.lib().pbt_attn_fwd_tc(_p(qkv), _p(out), _f(lse2), batch, seq, heads, _s()))
+    return out, lse2
+
+
+def attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads):
+    T = batch * seq
+    dsum = torch.empty(heads, T, device="cuda", dtype=torch.float32)
+    dq = torch.empty(T, heads * 128, device="cuda", dtype=torch.float32)
+    dqkv = torch.empty_like(qkv)
+    _lib.check(_lib.lib().pbt_attn_bwd_tc(_p(qkv), _p(out), _p(dout), _f(lse2), _f(dsum), _f(dq), _p(dqkv), batch,
+                                          seq, heads, _s()))
+    return dqkv

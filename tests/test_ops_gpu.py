@@ -37,6 +37,18 @@ def test_attention_forward(batch, seq, heads):
     assert (got_lse - lse).abs().max().item() < 2e-2
 
 
+@pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16)])
+def test_attention_forward_tcgen05(batch, seq, heads):
+    g = torch.Generator(device="cuda").manual_seed(seq * 3 + heads)
+    qkv = (2 * torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g)).bfloat16()
+    out, lse2 = K.attn_fwd_tc(qkv, batch, seq, heads)
+    torch.cuda.synchronize()
+    ref, lse = ref_attention(qkv, batch, seq, heads)
+    assert rel(out, ref) < 1e-2
+    got_lse = (lse2 * math.log(2)).view(heads, batch, seq).permute(1, 0, 2)
+    assert (got_lse - lse).abs().max().item() < 2e-2
+
+
 @pytest.mark.parametrize("batch,seq,heads", [(1, 64, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2)])
 def test_attention_backward(batch, seq, heads):
     g = torch.Generator(device="cuda").manual_seed(1 + seq + heads)
@@ -51,6 +63,22 @@ def test_attention_backward(batch, seq, heads):
     H = heads * 128
     for name, sl in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
         assert rel(dqkv[:, sl], gx[:, sl]) < 2e-2, name
+
+
+@pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16)])
+def test_attention_backward_tcgen05(batch, seq, heads):
+    g = torch.Generator(device="cuda").manual_seed(5 + seq + heads)
+    qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g).bfloat16()
+    dout = torch.randn(batch * seq, heads * 128, device="cuda", generator=g).bfloat16()
+    out, lse2 = K.attn_fwd_tc(qkv, batch, seq, heads)
+    dqkv = K.attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads)
+    torch.cuda.synchronize()
+    x = qkv.float().requires_grad_(True)
+    ref, _ = ref_attention(x, batch, seq, heads)
+    (gx,) = torch.autograd.grad(ref, x, dout.float())
+    H = heads * 128
+    for name, sl in (("dq", slice(0, H)), ("dk", slice(H, 2 * H)), ("dv", slice(2 * H, 3 * H))):
+        assert rel(dqkv[:, sl], gx[:, sl]) < 2e-2, (name, rel(dqkv[:, sl], gx[:, sl]))
 
 
 def test_rmsnorm_forward_backward():
