@@ -215,10 +215,15 @@ def main():
     from paper_2405_15362_b200 import pipeblock as pb
     from paper_2405_15362_b200.executor import DeviceExecutor, ModelConfig, synthetic_batch
 
+    if os.environ.get("PB_BENCH_SHARE_GPU"):  # test mode: every rank on cuda:0 (one-GPU box)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PB_BENCH_SHARE_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mcfg = CONFIGS[args.model]
     p = args.gpus
     sched_name = args.schedule or ("zb-h1" if p == 1 else "v-half")
@@ -244,17 +249,19 @@ def main():
         if world > 1:
             dist.barrier()
 
+    coll_dev = "cpu" if os.environ.get("PB_BENCH_SHARE_GPU") else "cuda"
+
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
