@@ -19,6 +19,9 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
              int32_t b_mn, void* C, int32_t ldc, void* C2, const void* aux, int32_t ldaux, int32_t epi,
              int32_t accumulate, void* stream);
 
+/* Force the GEMM variant: 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2) per 256-row tile
+ * where M and N allow it, -1 = automatic (default). Process-wide; for tests and benchmarks. */
+int pbt_gemm_set_cta_group(int32_t cg);
 /* causal attention, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T] (base-2 LSE of scaled scores) */
 int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
 /* same on tcgen05/TMEM (the executor's forward attention); seq % 128 == 0 */

@@ -101,3 +101,6 @@ extern "C" int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dou
         cuda_check("pbt_attn_bwd_tc");
     });
 }
+extern "C" int pbt_gemm_set_cta_group(int32_t cg) {
+    return pbx::guard([&] { pbk::gemm_force_cta_group(cg); });
+}

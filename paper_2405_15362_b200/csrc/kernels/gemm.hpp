@@ -35,6 +35,8 @@ struct GemmArgs {
 void gemm(const GemmArgs& g, cudaStream_t s);
 int gemm_bn(const GemmArgs& g);
 int num_sms();
+// tests: force the 1-CTA (1) or CTA-pair (2) variant where shapes allow; -1 = automatic
+void gemm_force_cta_group(int cg);
 // 2-D bf16 tensor map [outer][inner], row stride ld elements, box_inner x box_outer, 128B swizzle
 CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                      uint32_t box_outer);

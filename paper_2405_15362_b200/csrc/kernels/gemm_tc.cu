@@ -30,12 +30,13 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kBRows = BN / CG;  // B rows (N) held by each CTA of the pair
     static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kBBytes = kBRows * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -49,10 +50,13 @@ struct KParams {
     int accumulate;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) per
+// 256 x BN tile; each CTA stages its 128 rows of A and BN/2 rows of B, the
+// leader issues tcgen05.mma.cta_group::2 (M=256) and commits to both CTAs.
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, KParams p) {
-    using C_ = Cfg<BN>;
+    using C_ = Cfg<BN, CG>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::kStages * C_::kStageBytes);
@@ -62,26 +66,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const uint32_t warp = warp_id();
-    const int num_m = p.M / BM, num_n = p.N / BN;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+    const bool leader = rank == 0;
+    const int num_m = p.M / (BM * CG), num_n = p.N / BN;
     const int num_tiles = num_m * num_n;
     const int num_k = p.K / BK;
+    const int cid = int(blockIdx.x) / CG, ncl = int(gridDim.x) / CG;
 
     if (warp == 0 && elect_one()) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
         for (int s = 0; s < C_::kStages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1);  // leader's expect_tx covers both CTAs' bytes
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp of each CTA
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<C_::kTmemCols>(tmem_slot);
+    if (warp == 1) tmem_alloc<C_::kTmemCols, CG>(tmem_slot);
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -90,60 +98,92 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-                const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+            for (int t = cid; t < num_tiles; t += ncl) {
+                const int m0 = (t % num_m) * BM * CG + int(rank) * BM, n0 = (t / num_m) * BN + int(rank) * C_::kBRows;
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], C_::kStageBytes);
                     uint8_t* sa = smem + stage * C_::kStageBytes;
                     uint8_t* sb = sa + C_::kABytes;
                     const int k0 = kb * BK;
-                    if constexpr (A_MN) {  // [K][M]: boxes of 64 M x 64 K
-                        tma_load_2d(sa, &tma_a, &full[stage], m0, k0);
-                        tma_load_2d(sa + 8192, &tma_a, &full[stage], m0 + 64, k0);
-                    } else {  // [M][K]: one box 64 K x 128 rows
-                        tma_load_2d(sa, &tma_a, &full[stage], k0, m0);
-                    }
-                    if constexpr (B_MN) {  // [K][N]: BN/64 boxes of 64 N x 64 K
+                    if constexpr (CG == 1) {
+                        mbar_expect_tx(&full[stage], C_::kStageBytes);
+                        if constexpr (A_MN) {
+                            tma_load_2d(sa, &tma_a, &full[stage], m0, k0);
+                            tma_load_2d(sa + 8192, &tma_a, &full[stage], m0 + 64, k0);
+                        } else {
+                            tma_load_2d(sa, &tma_a, &full[stage], k0, m0);
+                        }
+                        if constexpr (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
-                    } else {  // [N][K]
-                        tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
+                            for (int j = 0; j < C_::kBRows / 64; ++j)
+                                tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
+                        } else {
+                            tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
+                        }
+                    } else {
+                        // the peer's bytes may land before the leader arms this phase: the phase
+                        // cannot complete before the leader's arrive, and the previous phase is
+                        // complete (the peer waited on `empty`, released after it was consumed)
+                        const uint32_t bar = map_peer(smem_u32(&full[stage]), 0);
+                        if (leader) mbar_expect_tx(&full[stage], CG * C_::kStageBytes);
+                        if constexpr (A_MN) {
+                            tma_load_2d_2sm(sa, &tma_a, bar, m0, k0);
+                            tma_load_2d_2sm(sa + 8192, &tma_a, bar, m0 + 64, k0);
+                        } else {
+                            tma_load_2d_2sm(sa, &tma_a, bar, k0, m0);
+                        }
+                        if constexpr (B_MN) {
+#pragma unroll
+                            for (int j = 0; j < C_::kBRows / 64; ++j)
+                                tma_load_2d_2sm(sb + j * 8192, &tma_b, bar, n0 + 64 * j, k0);
+                        } else {
+                            tma_load_2d_2sm(sb, &tma_b, bar, k0, n0);
+                        }
                     }
                     if (++stage == C_::kStages) stage = 0, phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            mbar_wait(&tempty[acc], acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < num_k; ++kb) {
-                mbar_wait(&full[stage], phase);
+        // ------------------------------------------------------------ MMA issuer (leader CTA)
+        if (leader) {
+            constexpr uint32_t idesc = idesc_bf16(BM * CG, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cid; t < num_tiles; t += ncl) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t sa = smem_u32(smem + stage * C_::kStageBytes);
-                    const uint32_t sb = sa + C_::kABytes;
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t sa = smem_u32(smem + stage * C_::kStageBytes);
+                        const uint32_t sb = sa + C_::kABytes;
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
-                        tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        for (int k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
+                            const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
+                            if constexpr (CG == 1)
+                                tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                            else
+                                tc_mma2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        }
+                        if constexpr (CG == 1) {
+                            tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
+                            if (kb == num_k - 1) tc_commit(&tfull[acc]);
+                        } else {
+                            tc_commit2(&empty[stage], 0x3);
+                            if (kb == num_k - 1) tc_commit2(&tfull[acc], 0x3);
+                        }
                     }
-                    tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
-                    if (kb == num_k - 1) tc_commit(&tfull[acc]);
+                    __syncwarp();
+                    if (++stage == C_::kStages) stage = 0, phase ^= 1;
                 }
-                __syncwarp();
-                if (++stage == C_::kStages) stage = 0, phase ^= 1;
+                if (++acc == 2) acc = 0, acc_phase ^= 1;
             }
-            if (++acc == 2) acc = 0, acc_phase ^= 1;
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -151,8 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_in_tile = int(q * 32 + lane_id());
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+        for (int t = cid; t < num_tiles; t += ncl) {
+            const int m0 = (t % num_m) * BM * CG + int(rank) * BM, n0 = (t / num_m) * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = m0 + row_in_tile;
@@ -166,14 +206,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (EPI == EPI_F32) {
                     float* dst = reinterpret_cast<float*>(p.C) + size_t(row) * p.ldc + col;
                     float4* d4 = reinterpret_cast<float4*>(dst);
+                    if (p.accumulate) {
+                        // C += acc reduced in L2: no read round trip; one update per element per launch,
+                        // so the result is deterministic
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                        if (p.accumulate) {
-                            float4 old = d4[j];
-                            o.x += old.x, o.y += old.y, o.z += old.z, o.w += old.w;
-                        }
-                        d4[j] = o;
+                        for (int j = 0; j < 8; ++j)
+                            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + 4 * j),
+                                         "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                                         : "memory");
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                     }
                 } else {
                     if constexpr (EPI == EPI_RESID || EPI == EPI_DGELU) {
@@ -217,14 +260,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+            if (lane_id() == 0) {
+                if constexpr (CG == 1)
+                    mbar_arrive(&tempty[acc]);
+                else
+                    mbar_arrive_cluster(map_peer(smem_u32(&tempty[acc]), 0));
+            }
             if (++acc == 2) acc = 0, acc_phase ^= 1;
         }
     }
+    tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_free<C_::kTmemCols>(tmem_base);
+        tmem_free<C_::kTmemCols, CG>(tmem_base);
     }
 }
 
@@ -269,46 +319,65 @@ int sm_count() {
     return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 void launch(const GemmArgs& g, cudaStream_t s) {
-    using C_ = Cfg<BN>;
-    static bool attr = [] {
-        cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+    using C_ = Cfg<BN, CG>;
+    auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
+    static bool attr = [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+        if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         return true;
     }();
     (void)attr;
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
-    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, BN);
+    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate};
-    const int tiles = (g.M / BM) * (g.N / BN);
-    const int grid = tiles < sm_count() ? tiles : sm_count();
-    gemm_kernel<BN, A_MN, B_MN, EPI><<<grid, kThreads, C_::kSmem, s>>>(ta, tb, kp);
+    const int tiles = (g.M / (BM * CG)) * (g.N / BN);
+    const int slots = sm_count() / CG;
+    const int grid = (tiles < slots ? tiles : slots) * CG;
+    if constexpr (CG == 1) {
+        kern<<<grid, kThreads, C_::kSmem, s>>>(ta, tb, kp);
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = C_::kSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, ta, tb, kp);
+    }
 }
 
-template <int BN>
+template <int BN, int CG>
 void dispatch(const GemmArgs& g, cudaStream_t s) {
     if (!g.a_mn && !g.b_mn) {
         switch (g.epi) {
-            case EPI_STORE: return launch<BN, false, false, EPI_STORE>(g, s);
-            case EPI_GELU: return launch<BN, false, false, EPI_GELU>(g, s);
-            case EPI_RESID: return launch<BN, false, false, EPI_RESID>(g, s);
-            case EPI_F32: return launch<BN, false, false, EPI_F32>(g, s);
+            case EPI_STORE: return launch<BN, false, false, EPI_STORE, CG>(g, s);
+            case EPI_GELU: return launch<BN, false, false, EPI_GELU, CG>(g, s);
+            case EPI_RESID: return launch<BN, false, false, EPI_RESID, CG>(g, s);
+            case EPI_F32: return launch<BN, false, false, EPI_F32, CG>(g, s);
             default: break;
         }
     } else if (!g.a_mn && g.b_mn) {
         switch (g.epi) {
-            case EPI_STORE: return launch<BN, false, true, EPI_STORE>(g, s);
-            case EPI_DGELU: return launch<BN, false, true, EPI_DGELU>(g, s);
-            case EPI_RESID: return launch<BN, false, true, EPI_RESID>(g, s);
-            case EPI_F32: return launch<BN, false, true, EPI_F32>(g, s);
+            case EPI_STORE: return launch<BN, false, true, EPI_STORE, CG>(g, s);
+            case EPI_DGELU: return launch<BN, false, true, EPI_DGELU, CG>(g, s);
+            case EPI_RESID: return launch<BN, false, true, EPI_RESID, CG>(g, s);
+            case EPI_F32: return launch<BN, false, true, EPI_F32, CG>(g, s);
             default: break;
         }
     } else if (g.a_mn && g.b_mn) {
-        if (g.epi == EPI_F32) return launch<BN, true, true, EPI_F32>(g, s);
-        if (g.epi == EPI_STORE) return launch<BN, true, true, EPI_STORE>(g, s);
+        if (g.epi == EPI_F32) return launch<BN, true, true, EPI_F32, CG>(g, s);
+        if (g.epi == EPI_STORE) return launch<BN, true, true, EPI_STORE, CG>(g, s);
     } else {
-        if (g.epi == EPI_F32) return launch<BN, true, false, EPI_F32>(g, s);
-        if (g.epi == EPI_STORE) return launch<BN, true, false, EPI_STORE>(g, s);
+        if (g.epi == EPI_F32) return launch<BN, true, false, EPI_F32, CG>(g, s);
+        if (g.epi == EPI_STORE) return launch<BN, true, false, EPI_STORE, CG>(g, s);
     }
     throw std::invalid_argument("gemm: unsupported operand-major / epilogue combination");
 }
@@ -322,14 +391,21 @@ int gemm_bn(const GemmArgs& g) {
     return (tiles256 >= num_sms()) ? 256 : 128;
 }
 
+static int g_force_cg = -1;  // tests: -1 auto, 1 or 2 forced
+void gemm_force_cta_group(int cg) { g_force_cg = cg; }
+
 void gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M % BM || g.N % 128 || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
         throw std::invalid_argument("gemm: M%128, N%128, K%64 must be 0 (M=" + std::to_string(g.M) +
                                     " N=" + std::to_string(g.N) + " K=" + std::to_string(g.K) + ")");
-    if (gemm_bn(g) == 256)
-        dispatch<256>(g, s);
+    const bool pair_ok = g.M % 256 == 0 && g.N % 256 == 0;
+    const int cg = g_force_cg > 0 ? (pair_ok ? g_force_cg : 1) : (pair_ok ? 2 : 1);
+    if (cg == 2)
+        dispatch<256, 2>(g, s);
+    else if (gemm_bn(g) == 256)
+        dispatch<256, 1>(g, s);
     else
-        dispatch<128>(g, s);
+        dispatch<128, 1>(g, s);
 }
 
 }  // namespace pbk

@@ -105,3 +105,7 @@ def attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads):
     _lib.check(_lib.lib().pbt_attn_bwd_tc(_p(qkv), _p(out), _p(dout), _f(lse2), _f(dsum), _f(dq), _p(dqkv), batch,
                                           seq, heads, _s()))
     return dqkv
+
+
+def set_cta_group(cg: int) -> None:
+    _lib.check(_lib.lib().pbt_gemm_set_cta_group(cg))

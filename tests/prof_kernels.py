@@ -1,0 +1,23 @@
+"""One launch of each hot kernel at GPT-1.5B / seq 2048 / mbs 1 pass shapes (for ncu captures)."""
+import torch
+
+from tests import kernels as K
+
+T, h, H = 2048, 2048, 16
+torch.manual_seed(0)
+A = torch.randn(T, h, device="cuda").bfloat16()
+W1 = torch.randn(4 * h, h, device="cuda").bfloat16()
+U = torch.empty(T, 4 * h, device="cuda", dtype=torch.bfloat16)
+G = torch.empty_like(U)
+K.gemm(A, W1, U, epi=1, C2=G)                                   # F: fc1 + GELU
+dY = torch.randn(T, h, device="cuda").bfloat16()
+W2t = torch.randn(h, 4 * h, device="cuda").bfloat16()
+K.gemm(dY, W2t, U, b_mn=True, epi=3, aux=U)                     # B: dgl * gelu'
+dW = torch.zeros(h, 4 * h, device="cuda")
+K.gemm(dY, G, dW, a_mn=True, b_mn=True, epi=4, accumulate=1)   # W: dW2 += dY^T gelu(u)
+qkv = torch.randn(T, 3 * h, device="cuda").bfloat16()
+out, lse2 = K.attn_fwd_tc(qkv, 1, T, H)
+dout = torch.randn_like(out)
+K.attn_bwd_tc(qkv, out, dout, lse2, 1, T, H)
+torch.cuda.synchronize()
+print("ok")

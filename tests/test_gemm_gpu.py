@@ -15,7 +15,15 @@ def gelu(x):
     return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
 
-SHAPES = [(128, 128, 64), (256, 384, 128), (512, 1024, 512), (2048, 6144, 2048), (384, 2304, 768)]
+SHAPES = [(128, 128, 64), (256, 384, 128), (512, 1024, 512), (2048, 6144, 2048), (384, 2304, 768), (256, 256, 64),
+          (1024, 768, 320)]
+
+
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"], autouse=True)
+def cta_group(request):
+    K.set_cta_group(request.param)
+    yield request.param
+    K.set_cta_group(-1)
 
 
 @pytest.mark.parametrize("M,N,Kd", SHAPES)
