@@ -30,80 +30,66 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
     return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
 }
 
-// y = x * rsqrt(mean(x^2) + eps) * g ; one warp per row
-__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
-                                   __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h, float eps) {
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= T) return;
-    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h);
-    const int nch = h >> 3;
-    float ss = 0.f;
-    for (int c = lane; c < nch; c += 32) {
-        float f[8];
-        unpack8(xr[c], f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
-    }
-    ss = warp_sum(ss);
-    const float r = rsqrtf(ss / float(h) + eps);
-    if (lane == 0) rstd[row] = r;
-    const uint4* gr = reinterpret_cast<const uint4*>(g);
-    uint4* yr = reinterpret_cast<uint4*>(y + size_t(row) * h);
-    for (int c = lane; c < nch; c += 32) {
-        float f[8], w[8];
-        unpack8(xr[c], f);
-        unpack8(gr[c], w);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = f[i] * r * w[i];
-        yr[c] = pack8(f);
-    }
+// block-wide sum; every thread gets the result (blockDim multiple of 32, <= 1024)
+__device__ __forceinline__ float block_sum(float v, float* red) {
+    v = warp_sum(v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = lane < nw ? red[lane] : 0.f;
+    t = warp_sum(t);
+    __syncthreads();
+    return t;
 }
 
-// dx = dres + r*g*dy - x * r^3/h * sum(g*dy*x) ; one warp per row, no atomics
+// y = x * rsqrt(mean(x^2) + eps) * g ; one CTA per row, one 16-byte chunk per thread held in registers
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                   __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h, float eps) {
+    __shared__ float red[32];
+    const int row = blockIdx.x, c = threadIdx.x;
+    float f[8], w[8];
+    unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], f);
+    unpack8(reinterpret_cast<const uint4*>(g)[c], w);
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+    ss = block_sum(ss, red);
+    const float r = rsqrtf(ss / float(h) + eps);
+    if (c == 0) rstd[row] = r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = f[i] * r * w[i];
+    reinterpret_cast<uint4*>(y + size_t(row) * h)[c] = pack8(f);
+}
+
+// dx = dres + r*g*dy - x * r^3/h * sum(g*dy*x) ; one CTA per row
 __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                                    const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
                                    const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int T,
                                    int h) {
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= T) return;
-    const int nch = h >> 3;
-    const uint4* gr = reinterpret_cast<const uint4*>(g);
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + size_t(row) * h);
-    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h);
+    __shared__ float red[32];
+    const int row = blockIdx.x, c = threadIdx.x;
+    float a[8], b[8], w[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(dy + size_t(row) * h)[c], a);
+    unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], b);
+    unpack8(reinterpret_cast<const uint4*>(g)[c], w);
+    if (dres) {
+        unpack8(reinterpret_cast<const uint4*>(dres + size_t(row) * h)[c], o);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
+    }
     const float r = rstd[row];
     float dot = 0.f;
-    for (int c = lane; c < nch; c += 32) {
-        float a[8], b[8], w[8];
-        unpack8(dyr[c], a);
-        unpack8(xr[c], b);
-        unpack8(gr[c], w);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dot += w[i] * a[i] * b[i];
-    }
-    dot = warp_sum(dot);
+    for (int i = 0; i < 8; ++i) dot += w[i] * a[i] * b[i];
+    dot = block_sum(dot, red);
     const float k = dot * r * r * r / float(h);
-    uint4* dxr = reinterpret_cast<uint4*>(dx + size_t(row) * h);
-    const uint4* dres_r = dres ? reinterpret_cast<const uint4*>(dres + size_t(row) * h) : nullptr;
-    for (int c = lane; c < nch; c += 32) {
-        float a[8], b[8], w[8], o[8];
-        unpack8(dyr[c], a);
-        unpack8(xr[c], b);
-        unpack8(gr[c], w);
-        if (dres_r) {
-            unpack8(dres_r[c], o);
-        } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) o[i] = 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] += r * w[i] * a[i] - b[i] * k;
-        dxr[c] = pack8(o);
-    }
+    for (int i = 0; i < 8; ++i) o[i] += r * w[i] * a[i] - b[i] * k;
+    reinterpret_cast<uint4*>(dx + size_t(row) * h)[c] = pack8(o);
 }
 
-// dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t] ; thread = 8 columns x a slab of rows
+// dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t] ; thread = 8 columns x `rows_per_block` rows (loads batched)
 __global__ void rmsnorm_dgamma_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                                       const float* __restrict__ rstd, float* __restrict__ dgamma, int T, int h,
                                       int rows_per_block) {
@@ -111,7 +97,26 @@ __global__ void rmsnorm_dgamma_kernel(const __nv_bfloat16* __restrict__ dy, cons
     if (c * 8 >= h) return;
     const int r0 = blockIdx.y * rows_per_block, r1 = min(T, r0 + rows_per_block);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int row = r0; row < r1; ++row) {
+    int row = r0;
+    for (; row + 4 <= r1; row += 4) {
+        uint4 ua[4], ub[4];
+        float rr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            ua[u] = reinterpret_cast<const uint4*>(dy + size_t(row + u) * h)[c];
+            ub[u] = reinterpret_cast<const uint4*>(x + size_t(row + u) * h)[c];
+            rr[u] = rstd[row + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float a[8], b[8];
+            unpack8(ua[u], a);
+            unpack8(ub[u], b);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += a[i] * b[i] * rr[u];
+        }
+    }
+    for (; row < r1; ++row) {
         float a[8], b[8];
         unpack8(reinterpret_cast<const uint4*>(dy + size_t(row) * h)[c], a);
         unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], b);
@@ -275,18 +280,18 @@ int grid_for(size_t n, int per_thread, int block) {
 
 void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
                  cudaStream_t s) {
-    if (h % 8) throw std::invalid_argument("rmsnorm: h % 8");
-    rmsnorm_fwd_kernel<<<(T + 7) / 8, 256, 0, s>>>(x, g, y, rstd, T, h, 1e-5f);
+    if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
+    rmsnorm_fwd_kernel<<<T, h / 8, 0, s>>>(x, g, y, rstd, T, h, 1e-5f);
 }
 
 void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
                  const __nv_bfloat16* dres, __nv_bfloat16* dx, int T, int h, cudaStream_t s) {
-    rmsnorm_bwd_kernel<<<(T + 7) / 8, 256, 0, s>>>(dy, x, g, rstd, dres, dx, T, h);
+    if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
+    rmsnorm_bwd_kernel<<<T, h / 8, 0, s>>>(dy, x, g, rstd, dres, dx, T, h);
 }
 
 void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, int T, int h,
                     cudaStream_t s) {
-    // one thread per 8 columns x 16 rows: T/16 x h/2048 CTAs (>= 1 wave on 148 SMs at T=2048)
     const int rows = 16;
     const int threads = std::min(256, h / 8);
     dim3 grid((h / 8 + threads - 1) / threads, (T + rows - 1) / rows);
