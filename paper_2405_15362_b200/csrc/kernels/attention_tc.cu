@@ -74,8 +74,10 @@ __global__ void __launch_bounds__(192, 1)
 
     const uint32_t warp = warp_id();
     const int nqb = seq / BQ;
-    const int qb = nqb - 1 - int(blockIdx.x);  // heaviest tiles first
-    const int head = blockIdx.y, b = blockIdx.z;
+    // 1-D grid ordered heaviest causal tile first across all (head, sequence): LPT dispatch
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int qb = nqb - 1 - int(blockIdx.x) / (H * (T / seq));
+    const int head = hb % H, b = hb / H;
     const int row0 = b * seq + qb * BQ;        // first token row of this Q tile
     const int nkv = qb + 1;                    // causal: key tiles 0..qb
 
@@ -262,26 +264,31 @@ __global__ void __launch_bounds__(192, 1)
 // ------------------------------------------------------------------ backward
 // One CTA per (128-key tile kb, head, sequence), looping over query tiles qb >= kb:
 //   S^T  = K Q^T,  dP^T = V dO^T                       -> TMEM [0,128), [128,256)
-//   compute warps (thread = key row): P^T = exp2(S^T*c - lse2[q]), dS^T = P^T (dP^T - D[q])
-//                                     -> bf16 smem (128B-swizzled, rows = keys)
+//   8 compute warps (2 per SM sub-partition, column halves; thread = key row):
+//        P^T = exp2(S^T*c - lse2[q]),  dS^T = P^T (dP^T - D[q])   -> bf16 smem, 128B-swizzled
 //   dV += P^T dO,  dK += dS^T Q                          -> TMEM [256,384), [384,512)
-//   dQ_tile = dS K  (A = dS^T read MN-major)             -> TMEM [0,128), then red.global.add.v4.f32
+//   dQ_tile = dS K  (A = dS^T read MN-major)             -> TMEM [0,128)
+//        -> fp32 smem (reusing the P^T/dS^T buffers) -> TMA bulk reduce-add into dq_acc
 struct BwdSmem {
     static constexpr int k = 0;
     static constexpr int v = k + kTile;
     static constexpr int q = v + kTile;
     static constexpr int dO = q + kTile;
-    static constexpr int pt = dO + kTile;
+    static constexpr int pt = dO + kTile;   // P^T, then (with dst) the 64 KB fp32 dQ staging tile
     static constexpr int dst = pt + kTile;
-    static constexpr int lse = dst + kTile;      // [2][2][128] floats
+    static constexpr int lse = dst + kTile;  // [2][256] floats: lse2 | D
     static constexpr int bars = lse + 2048;
     static constexpr int total = bars + 256 + 1024;
 };
+constexpr int kBwdThreads = 320;
 
-__global__ void __launch_bounds__(192, 1)
+__device__ __forceinline__ void bar_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const float* __restrict__ lse2, const float* __restrict__ dsum, float* __restrict__ dq_acc,
-                       __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
+                       const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
+                       const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T,
+                       float scale) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::bars);
@@ -298,15 +305,18 @@ __global__ void __launch_bounds__(192, 1)
 
     const uint32_t warp = warp_id();
     const int nqb = seq / BQ;
-    const int kb = int(blockIdx.x);  // kb = 0 has the most query tiles: dispatched first
-    const int head = blockIdx.y, b = blockIdx.z;
+    // 1-D grid, kb = 0 (most query tiles) of every (head, sequence) dispatched first
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int kb = int(blockIdx.x) / (H * (T / seq));
+    const int head = hb % H, b = hb / H;
     const int tok0 = b * seq;
     const int nq = nqb - kb;
 
     if (warp == 0 && elect_one()) {
         tma_prefetch(&tm_qkv);
         tma_prefetch(&tm_do);
-        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 6) ? 4 : 1);
+        tma_prefetch(&tm_dq);
+        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 6) ? 8 : 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -388,23 +398,27 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
     } else {
         const uint32_t q4 = warp & 3;
+        const int hf = int(warp - 2) >> 2;  // column half handled by this warp
         const int r = int(q4 * 32 + lane_id());
         const uint32_t lane_base = (q4 * 32) << 16;
         const float sl2 = scale * kLog2e;
         uint8_t* spt = sm + BwdSmem::pt;
         uint8_t* sdst = sm + BwdSmem::dst;
-        const int key = kb * BK + r;  // key index within the sequence
+        const bool issuer = threadIdx.x == 64;  // warp 2, lane 0: TMA reduce-add of dQ
+        const int key = kb * BK + r;           // key index within the sequence
         for (int i = 0; i < nq; ++i) {
             const int qb = kb + i;
+            if (issuer && i > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             float* Lb = sL + (i & 1) * 256;
-            Lb[r] = lse2[size_t(head) * T + tok0 + qb * BQ + r];
-            Lb[128 + r] = dsum[size_t(head) * T + tok0 + qb * BQ + r];
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            Lb[hf * 128 + r] = hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r]
+                                       : dsum[size_t(head) * T + tok0 + qb * BQ + r];
+            bar_sync_compute();  // lse/D staged; previous dQ tile drained from the staging buffer
             mbar_wait(s_full, i & 1);
             tc_fence_after();
             const bool diag = (qb == kb);
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c = hf * 2 + cc;
                 float sv[32], dp[32];
                 tmem_ld32(tmem + lane_base + c * 32, sv);
                 tmem_ld32(tmem + lane_base + 128 + c * 32, dp);
@@ -433,31 +447,46 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(ds_full);
-            // dQ tile: thread = query row r
-            mbar_wait(dq_full, i & 1);
+            // dQ tile (thread = query row r): TMEM -> fp32 smem (4 swizzled [128][32] chunks) -> TMA reduce-add
+            mbar_wait(dq_full, i & 1);  // also: every MMA reading P^T / dS^T has retired
             tc_fence_after();
-            float* dqrow = dq_acc + size_t(tok0 + qb * BQ + r) * (H * D) + head * D;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c = hf * 2 + cc;
                 float v[32];
                 tmem_ld32(tmem + lane_base + c * 32, v);
                 tmem_ld_wait();
+                uint8_t* chunk = spt + c * 16384 + r * 128;
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c * 32 + e * 4),
-                                 "f"(v[4 * e]), "f"(v[4 * e + 1]), "f"(v[4 * e + 2]), "f"(v[4 * e + 3])
-                                 : "memory");
+                for (int g = 0; g < 8; ++g)
+                    *reinterpret_cast<float4*>(chunk + ((g ^ (r & 7)) << 4)) =
+                        make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
             }
             tc_fence_before();
             __syncwarp();
-            if (lane_id() == 0) mbar_arrive(s_free);
+            if (lane_id() == 0) mbar_arrive(s_free);  // TMEM [0,256) free for the next S^T / dP^T
+            fence_async_smem();
+            bar_sync_compute();
+            if (issuer) {
+                const int row = tok0 + qb * BQ;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tm_dq)),
+                        "r"(smem_u32(spt + c * 16384)), "r"(head * D + c * 32), "r"(row)
+                        : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
         }
-        // dV, dK rows (thread = key row)
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // dV, dK rows (thread = key row, column half hf)
         mbar_wait(dkv_full, 0);
         tc_fence_after();
         const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = hf * 2 + cc;
             float v[32], k[32];
             tmem_ld32(tmem + lane_base + 256 + c * 32, v);
             tmem_ld32(tmem + lane_base + 384 + c * 32, k);
@@ -497,9 +526,11 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     const int T = batch * seq;
     const CUtensorMap tq = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
     const CUtensorMap td = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 128);
-    dim3 grid(seq / BK, heads, batch);
-    attn_bwd_tc_kernel<<<grid, 192, BwdSmem::total, s>>>(tq, td, lse2, dsum, dq_acc, dqkv, seq, heads, T,
-                                                        0.08838834764831845f);
+    const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
+                                       uint64_t(heads) * D, 32, 128);
+    dim3 grid(seq / BK * heads * batch);
+    attn_bwd_tc_kernel<<<grid, kBwdThreads, BwdSmem::total, s>>>(tq, td, tdq, lse2, dsum, dqkv, seq, heads, T,
+                                                                0.08838834764831845f);
     attn_dq_store(dq_acc, dqkv, heads, T, s);
 }
 
@@ -513,7 +544,7 @@ void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int 
     (void)once;
     const int T = batch * seq;
     const CUtensorMap tm = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
-    dim3 grid(seq / BQ, heads, batch);
+    dim3 grid(seq / BQ * heads * batch);
     attn_fwd_tc_kernel<<<grid, 192, FwdSmem::total, s>>>(tm, out, lse2, seq, heads, T, 0.08838834764831845f);
 }
 
