@@ -134,6 +134,7 @@ typedef struct pb_model_cfg {
 #define PB_FLAG_SERIAL 1     /* device-synchronise after every pass (race check mode) */
 #define PB_FLAG_TIMELINE 2   /* record per-pass CUDA events (TimedSchedule output) */
 #define PB_FLAG_GEMM_TIMING 4 /* CUDA events around every GEMM launch (roofline of the dominant kernel) */
+#define PB_FLAG_KERNEL_TIMING 8 /* CUDA events around every launch, per-kernel report (pb_exec_kernel_report) */
 
 typedef struct pb_exec_stats {
     double loss;            /* mean CE over all tokens of the step (last-stage device; NaN elsewhere) */
@@ -171,6 +172,8 @@ int pb_exec_connect_ipc(pb_exec* e, const void* const* blobs, const size_t* lens
  * timeline: NULL or an array of this device's pass count (canonical order). */
 int pb_exec_step(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32_t inputs_on_host,
                  pb_timed_pass* timeline, size_t timeline_n, pb_exec_stats* stats);
+/* JSON {"label": [ms, launches], ...} of the last PB_FLAG_KERNEL_TIMING step. */
+int pb_exec_kernel_report(pb_exec* e, char* buf, size_t cap, size_t* len);
 /* Enqueue-only variant for CUDA-event timing by the caller: no host sync. */
 int pb_exec_step_async(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32_t inputs_on_host);
 int pb_exec_sync(pb_exec* e, pb_timed_pass* timeline, size_t timeline_n, pb_exec_stats* stats);

@@ -58,7 +58,7 @@ EXPORTS = [
     "pb_schedule_emit", "pb_schedule_info", "pb_schedule_topology", "pb_schedule_passes", "pb_schedule_exact_peak",
     "pb_simulate", "pb_account", "pb_schedule_destroy", "pb_exec_create", "pb_exec_connect_local",
     "pb_exec_export", "pb_exec_connect_ipc", "pb_exec_step", "pb_exec_step_async", "pb_exec_sync",
-    "pb_exec_num_passes", "pb_exec_set_flags", "pb_exec_stream", "pb_exec_param_count", "pb_exec_param_info", "pb_exec_param_get",
+    "pb_exec_num_passes", "pb_exec_set_flags", "pb_exec_kernel_report", "pb_exec_stream", "pb_exec_param_count", "pb_exec_param_info", "pb_exec_param_get",
     "pb_exec_param_set", "pb_exec_zero_grads", "pb_exec_destroy",
 ]
 

@@ -25,6 +25,7 @@ extern "C" int pb_exec_create(const pb_model_cfg* cfg, const pb_schedule* plan, 
         e->timeline = (cfg->flags & PB_FLAG_TIMELINE) != 0;
         e->serial = (cfg->flags & PB_FLAG_SERIAL) != 0;
         e->gemm_timing = (cfg->flags & PB_FLAG_GEMM_TIMING) != 0;
+        e->kernel_timing = (cfg->flags & PB_FLAG_KERNEL_TIMING) != 0;
         if (e->plan.topo.devices == 1) e->connect_local({e}, nullptr);
         *out = new pb_exec{e};
     });
@@ -85,6 +86,7 @@ extern "C" int pb_exec_set_flags(pb_exec* h, int32_t flags) {
         e.timeline = (flags & PB_FLAG_TIMELINE) != 0;
         e.serial = (flags & PB_FLAG_SERIAL) != 0;
         e.gemm_timing = (flags & PB_FLAG_GEMM_TIMING) != 0;
+        e.kernel_timing = (flags & PB_FLAG_KERNEL_TIMING) != 0;
     });
 }
 
@@ -154,4 +156,14 @@ extern "C" void pb_exec_destroy(pb_exec* h) {
     if (!h) return;
     delete h->e;
     delete h;
+}
+
+extern "C" int pb_exec_kernel_report(pb_exec* h, char* buf, size_t cap, size_t* len) {
+    return pbx::guard([&] {
+        const std::string& r = X(h).kernel_report;
+        if (len) *len = r.size();
+        if (!buf) return;
+        if (cap < r.size() + 1) throw pbx::Space("report buffer too small");
+        std::memcpy(buf, r.c_str(), r.size() + 1);
+    });
 }

@@ -57,7 +57,13 @@ extern "C" int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, con
                                void* dx, float* dgamma, int32_t T, int32_t h, void* stream) {
     return pbx::guard([&] {
         pbk::rmsnorm_bwd(BF(dy), BF(x), BF(g), rstd, BF(dres), BFM(dx), T, h, ST(stream));
-        if (dgamma) pbk::rmsnorm_dgamma(BF(dy), BF(x), rstd, dgamma, T, h, ST(stream));
+        if (dgamma) {
+            float* scratch = nullptr;
+            if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), size_t((T + 15) / 16) * h * 4, ST(stream)) != cudaSuccess)
+                throw pbx::CudaError("scratch allocation failed");
+            pbk::rmsnorm_dgamma(BF(dy), BF(x), rstd, dgamma, scratch, T, h, ST(stream));
+            cudaFreeAsync(scratch, ST(stream));
+        }
         cuda_check("pbt_rmsnorm_bwd");
     });
 }

@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <stdexcept>
 #include <string>
 
@@ -209,6 +210,7 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
 
     nslots = plan.slots[dev];
     pool = static_cast<uint8_t*>(dmalloc(slot_bytes * size_t(std::max(nslots, 1)), "activation pool"));
+    build_w_groups();
     msg_bytes = align_up(size_t(T) * h * 2, 1024);
     nout = std::max(plan.outboxes[dev], 1);
     outbox = static_cast<uint8_t*>(dmalloc(msg_bytes * size_t(nout), "outbox"));
@@ -246,9 +248,11 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
 Exec::~Exec() {
     cudaSetDevice(cuda);
     cudaDeviceSynchronize();
+    for (auto& kv : wgroups) pbk::gemm_group_destroy(kv.second);
     for (auto* v : {&ev_start, &ev_end, &ev_pull, &ev_free})
         for (auto e : *v) cudaEventDestroy(e);
     for (auto e : gev) cudaEventDestroy(e);
+    for (auto e : kev) cudaEventDestroy(e);
     cudaEventDestroy(ev_step0);
     cudaEventDestroy(ev_step1);
     for (auto& p : peers)
@@ -269,6 +273,32 @@ __nv_bfloat16* Exec::bf(int slot, size_t off) const {
 float* Exec::f32(int slot, size_t off) const { return reinterpret_cast<float*>(pool + size_t(slot) * slot_bytes + off); }
 __nv_bfloat16* Exec::outbox_ptr(int k) const { return reinterpret_cast<__nv_bfloat16*>(outbox + size_t(k) * msg_bytes); }
 
+template <typename Fn>
+void Exec::timed(const char* label, Fn&& fn) {
+    if (!kernel_timing) {
+        fn();
+        return;
+    }
+    int id = -1;
+    for (size_t i = 0; i < klabels.size(); ++i)
+        if (klabels[i] == label) id = int(i);
+    if (id < 0) {
+        klabels.push_back(label);
+        id = int(klabels.size()) - 1;
+    }
+    if (kev_used + 2 > kev.size()) {
+        const size_t old = kev.size();
+        kev.resize(old + 1024);
+        for (size_t i = old; i < kev.size(); ++i) ck(cudaEventCreate(&kev[i]), "event");
+    }
+    if (kev_label.size() < kev.size() / 2) kev_label.resize(kev.size() / 2);
+    ck(cudaEventRecord(kev[kev_used], cs), "event");
+    fn();
+    ck(cudaEventRecord(kev[kev_used + 1], cs), "event");
+    kev_label[kev_used / 2] = id;
+    kev_used += 2;
+}
+
 void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __nv_bfloat16* B, bool b_mn, void* C,
                 int epi, const __nv_bfloat16* aux, void* C2, int accumulate) {
     pbk::GemmArgs g;
@@ -278,7 +308,11 @@ void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __
     g.C = C, g.ldc = N, g.C2 = C2;
     g.aux = aux, g.ldaux = N;
     g.epi = epi, g.accumulate = accumulate;
-    if (gemm_timing) {
+    const char* glabel = a_mn ? "gemm_W" : (b_mn ? "gemm_B" : "gemm_F");
+    if (kernel_timing) {
+        timed(glabel, [&] { pbk::gemm(g, cs); });
+        gemm_flops_acc += 2.0 * double(M) * double(N) * double(K);
+    } else if (gemm_timing) {
         if (gev_used + 2 > gev.size()) {
             gev.resize(gev.size() + 512);
             for (size_t i = gev.size() - 512; i < gev.size(); ++i) ck(cudaEventCreate(&gev[i]), "event");
@@ -293,12 +327,66 @@ void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __
     ++launches;
 }
 
+// All weight-gradient GEMMs of one W pass (every layer of the stage) as one grouped launch.
+void Exec::build_w_groups() {
+    if (std::getenv("PB_NO_WGROUP")) return;
+    for (int s : stages) {
+        const StageLayout& L = layout.at(s);
+        const StageParams& P = sparams.at(s);
+        for (int slot = 0; slot < nslots; ++slot) {
+            std::vector<pbk::GemmArgs> v;
+            double fl = 0;
+            auto add = [&](int M, int N, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C) {
+                pbk::GemmArgs g;
+                g.M = M, g.N = N, g.K = T;
+                g.A = A, g.a_mn = true, g.lda = M;
+                g.B = B, g.b_mn = true, g.ldb = N;
+                g.C = C, g.ldc = N, g.epi = pbk::EPI_F32, g.accumulate = 1;
+                v.push_back(g);
+                fl += 2.0 * M * N * T;
+            };
+            for (int l = Lc - 1; l >= 0; --l) {
+                const auto& y = L.layer[l];
+                const auto& w = P.layers[l];
+                add(h, 4 * h, bf(slot, L.dx[l + 1]), bf(slot, y.gl), G(w.w2));
+                add(4 * h, h, bf(slot, y.u), bf(slot, y.b), G(w.w1));
+                add(h, h, bf(slot, y.dx1), bf(slot, y.o), G(w.wo));
+                add(3 * h, h, bf(slot, y.dqkv), bf(slot, y.a), G(w.wqkv));
+            }
+            bool ok = true;
+            for (const auto& g : v) ok = ok && pbk::gemm_group_ok(g);
+            if (!ok) continue;
+            wgroups[{s, slot}] = pbk::gemm_group_create(v.data(), int(v.size()));
+            wgroup_flops[{s, slot}] = fl;
+        }
+    }
+}
+
+void Exec::run_gemm_timed(const char* label, double flops, const std::function<void()>& fn) {
+    if (kernel_timing) {
+        timed(label, fn);
+        gemm_flops_acc += flops;
+    } else if (gemm_timing) {
+        if (gev_used + 2 > gev.size()) {
+            gev.resize(gev.size() + 512);
+            for (size_t i = gev.size() - 512; i < gev.size(); ++i) ck(cudaEventCreate(&gev[i]), "event");
+        }
+        ck(cudaEventRecord(gev[gev_used++], cs), "event");
+        fn();
+        ck(cudaEventRecord(gev[gev_used++], cs), "event");
+        gemm_flops_acc += flops;
+    } else {
+        fn();
+    }
+    ++launches;
+}
+
 void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
     __nv_bfloat16* x0 = bf(slot, L.x[0]);
     if (s == 1) {
-        pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, cs);
+        timed("embed_fwd", [&] { pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, cs); });
         ++launches;
     }
     for (int l = 0; l < Lc; ++l) {
@@ -306,21 +394,21 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         const auto& w = P.layers[l];
         __nv_bfloat16* x = bf(slot, L.x[l]);
         __nv_bfloat16* xo = (l == Lc - 1 && s < S) ? out : bf(slot, L.x[l + 1]);
-        pbk::rmsnorm_fwd(x, W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs);
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(x, W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs); });
         gemm(T, 3 * h, h, bf(slot, y.a), false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE);
-        pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs);
+        timed("attn_fwd", [&] { pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs); });
         gemm(T, h, h, bf(slot, y.o), false, W(w.wo), false, bf(slot, y.x1), pbk::EPI_RESID, x);
-        pbk::rmsnorm_fwd(bf(slot, y.x1), W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs);
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, y.x1), W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs); });
         gemm(T, 4 * h, h, bf(slot, y.b), false, W(w.w1), false, bf(slot, y.u), pbk::EPI_GELU, nullptr,
              bf(slot, y.gl));
         gemm(T, h, 4 * h, bf(slot, y.gl), false, W(w.w2), false, xo, pbk::EPI_RESID, bf(slot, y.x1));
         launches += 3;
     }
     if (s == S) {
-        pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), W(P.gf), bf(slot, L.hf), f32(slot, L.rstdf), T, h, cs);
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), W(P.gf), bf(slot, L.hf), f32(slot, L.rstdf), T, h, cs); });
         gemm(T, V, h, bf(slot, L.hf), false, W(P.head), false, bf(slot, L.logits), pbk::EPI_STORE);
-        pbk::cross_entropy(bf(slot, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
-                           cs);
+        timed("cross_entropy", [&] { pbk::cross_entropy(bf(slot, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
+                           cs); });
         launches += 2;
     }
 }
@@ -332,9 +420,9 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
     if (s == S) {
         // dhf = dlogits . Whead ; dx_L = rmsnorm_bwd(dhf)
         gemm(T, h, V, bf(slot, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
-        pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), W(P.gf), f32(slot, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
-                         cs);
-        pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), f32(slot, L.rstdf), G(P.gf), T, h, cs);
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), W(P.gf), f32(slot, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
+                         cs); });
+        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), f32(slot, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
         launches += 2;
     }
     for (int l = Lc - 1; l >= 0; --l) {
@@ -345,14 +433,14 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         // du = (dy . W2) * gelu'(u), written over u
         gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u));
         gemm(T, h, 4 * h, bf(slot, y.u), false, W(w.w1), true, scratch, pbk::EPI_STORE);
-        pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs);
-        pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), T, h, cs);
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs); });
+        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), dq_acc, T, h, cs); });
         gemm(T, h, h, bf(slot, y.dx1), false, W(w.wo), true, scratch, pbk::EPI_STORE);
-        pbk::attn_bwd_tc(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
-                      seq, H, cs);
+        timed("attn_bwd", [&] { pbk::attn_bwd_tc(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
+                      seq, H, cs); });
         gemm(T, h, 3 * h, bf(slot, y.dqkv), false, W(w.wqkv), true, scratch, pbk::EPI_STORE);
-        pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs);
-        pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), T, h, cs);
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs); });
+        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), dq_acc, T, h, cs); });
         launches += 8;
     }
 }
@@ -360,6 +448,10 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
 void Exec::pass_weight(int s, int mb, int slot) {
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
+    auto grp = wgroups.find({s, slot});
+    if (grp != wgroups.end()) {
+        run_gemm_timed("gemm_W", wgroup_flops.at({s, slot}), [&] { pbk::gemm_group_run(grp->second, cs); });
+    } else
     for (int l = Lc - 1; l >= 0; --l) {
         const auto& y = L.layer[l];
         const auto& w = P.layers[l];
@@ -371,7 +463,7 @@ void Exec::pass_weight(int s, int mb, int slot) {
     if (s == S)
         gemm(V, h, T, bf(slot, L.logits), true, bf(slot, L.hf), true, G(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
     if (s == 1) {
-        pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, cs);
+        timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, cs); });
         ++launches;
     }
 }
@@ -400,6 +492,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     launches = 0;
     peer_bytes = 0;
     gev_used = 0;
+    kev_used = 0;
     gemm_flops_acc = 0;
     const size_t nin = size_t(m) * T * 4;
     const auto kind = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
@@ -508,8 +601,10 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     }
     if (cfg.optimizer) {
         ++adam_step;
-        pbk::adamw(master, wts, grads, adam_m, adam_v, n_params, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
-                   cfg.weight_decay, adam_step, cs);
+        timed("adamw", [&] {
+            pbk::adamw(master, wts, grads, adam_m, adam_v, n_params, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
+                       cfg.weight_decay, adam_step, cs);
+        });
         ++launches;
     }
     if (has_last) ck(cudaMemcpyAsync(loss_host, loss_dev, 4, cudaMemcpyDeviceToHost, cs), "loss");
@@ -560,6 +655,22 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
             gms += t;
         }
         st->gemm_ms = gms;
+        if (kernel_timing) {
+            std::vector<double> ms(klabels.size(), 0.0);
+            std::vector<int64_t> cnt(klabels.size(), 0);
+            for (size_t i = 0; i + 1 < kev_used; i += 2) {
+                float t = 0;
+                ck(cudaEventElapsedTime(&t, kev[i], kev[i + 1]), "elapsed");
+                ms[kev_label[i / 2]] += t;
+                cnt[kev_label[i / 2]] += 1;
+            }
+            std::string r = "{";
+            for (size_t i = 0; i < klabels.size(); ++i) {
+                if (i) r += ",";
+                r += "\"" + klabels[i] + "\":[" + std::to_string(ms[i]) + "," + std::to_string(cnt[i]) + "]";
+            }
+            kernel_report = r + "}";
+        }
         st->gemm_flops = gemm_flops_acc;
         st->gemm_launches = int64_t(gev_used / 2);
     }

@@ -88,10 +88,11 @@ class Exec {
     __nv_bfloat16* wts = nullptr;
     size_t n_params = 0;
     cudaStream_t cs = nullptr, xs = nullptr;
-    bool timeline = true, serial = false, connected = false, pending = false, gemm_timing = false;
+    bool timeline = true, serial = false, connected = false, pending = false, gemm_timing = false, kernel_timing = false;
     int adam_step = 0;
 
     int64_t steps_done = 0;
+    std::string kernel_report;
 
   private:
     void build_layout();
@@ -110,6 +111,10 @@ class Exec {
     uint32_t* ack_flag(uint32_t* base, int k) const;
     uint32_t* ready_flag(uint32_t* base, int src, int k) const;
 
+    void build_w_groups();
+    void run_gemm_timed(const char* label, double flops, const std::function<void()>& fn);
+    std::map<std::pair<int, int>, pbk::GemmGroup> wgroups;  // (stage, slot) -> grouped W GEMMs
+    std::map<std::pair<int, int>, double> wgroup_flops;
     std::map<int, StageLayout> layout;
     std::map<int, StageParams> sparams;
     size_t slot_bytes = 0, msg_bytes = 0, nflags = 0;
@@ -130,6 +135,13 @@ class Exec {
     std::vector<cudaEvent_t> gev;
     size_t gev_used = 0;
     double gemm_flops_acc = 0;
+    // PB_FLAG_KERNEL_TIMING: event pairs around every launch, aggregated per label
+    std::vector<cudaEvent_t> kev;
+    std::vector<int> kev_label;
+    size_t kev_used = 0;
+    std::vector<std::string> klabels;
+    template <typename Fn>
+    void timed(const char* label, Fn&& fn);
 };
 
 std::shared_ptr<LocalGroup> make_group(const std::vector<Exec*>& all);

@@ -234,6 +234,8 @@ __global__ void __launch_bounds__(128, 2)
 // Dsum[h][t] = sum_d dO * O ; also zero the fp32 dQ accumulator.
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
                                     float* __restrict__ dsum, float* __restrict__ dq_acc, int H, int T) {
+    pdl_wait();
+    pdl_launch();
     const int t = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int head = warp; head < H; head += blockDim.x >> 5) {
@@ -423,6 +425,8 @@ __global__ void __launch_bounds__(128, 1)
 
 __global__ void attn_dq_store_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int H,
                                      float scale) {
+    pdl_wait();
+    pdl_launch();
     const int t = blockIdx.x;
     for (int c = threadIdx.x * 4; c < H * D; c += blockDim.x * 4) {
         float4 v = *reinterpret_cast<const float4*>(dq_acc + size_t(t) * H * D + c);
@@ -447,11 +451,11 @@ void attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int bat
 
 void attn_bwd_pre(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* dsum, float* dq_acc, int heads, int T,
                   cudaStream_t s) {
-    attn_bwd_pre_kernel<<<T, 256, 0, s>>>(dout, out, dsum, dq_acc, heads, T);
+    launch_k(attn_bwd_pre_kernel, dim3(T), dim3(256), 0, s, 1, dout, out, dsum, dq_acc, heads, T);
 }
 
 void attn_dq_store(const float* dq_acc, __nv_bfloat16* dqkv, int heads, int T, cudaStream_t s) {
-    attn_dq_store_kernel<<<T, 256, 0, s>>>(dq_acc, dqkv, heads, 0.08838834764831845f);
+    launch_k(attn_dq_store_kernel, dim3(T), dim3(256), 0, s, 1, dq_acc, dqkv, heads, 0.08838834764831845f);
 }
 
 void attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,

@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;  // cols [0,128) S0, [128,256) S1, [256,384) O
+    pdl_wait();
+    pdl_launch();
 
     if (warp == 0) {
         if (elect_one()) {
@@ -324,6 +326,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
 
     if (warp == 0) {
         if (elect_one()) {
@@ -529,8 +533,8 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
                                        uint64_t(heads) * D, 32, 128);
     dim3 grid(seq / BK * heads * batch);
-    attn_bwd_tc_kernel<<<grid, kBwdThreads, BwdSmem::total, s>>>(tq, td, tdq, lse2, dsum, dqkv, seq, heads, T,
-                                                                0.08838834764831845f);
+    launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
+             static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
     attn_dq_store(dq_acc, dqkv, heads, T, s);
 }
 
@@ -545,7 +549,8 @@ void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int 
     const int T = batch * seq;
     const CUtensorMap tm = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
     dim3 grid(seq / BQ * heads * batch);
-    attn_fwd_tc_kernel<<<grid, 192, FwdSmem::total, s>>>(tm, out, lse2, seq, heads, T, 0.08838834764831845f);
+    launch_k(attn_fwd_tc_kernel, grid, dim3(192), FwdSmem::total, s, 1, tm, out, lse2, seq, heads, T,
+             0.08838834764831845f);
 }
 
 }  // namespace pbk

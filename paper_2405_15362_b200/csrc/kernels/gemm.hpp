@@ -33,6 +33,21 @@ struct GemmArgs {
 };
 
 void gemm(const GemmArgs& g, cudaStream_t s);
+
+// Grouped weight-gradient GEMMs: independent dW (+)= dY^T X problems (A and B MN-major,
+// fp32 epilogue) run as ONE persistent CTA-pair launch over their concatenated tiles,
+// so the W pass of a whole stage pays one ramp and one tail.  Descriptor table lives
+// in device memory; built once per (stage, activation slot).
+struct GemmGroup {
+    void* table = nullptr;  // device GroupProblem[n]
+    int n = 0;
+    int total_tiles = 0;
+    int accumulate = 1;
+};
+GemmGroup gemm_group_create(const GemmArgs* problems, int n);
+void gemm_group_run(const GemmGroup& g, cudaStream_t s);
+void gemm_group_destroy(GemmGroup& g);
+bool gemm_group_ok(const GemmArgs& g);  // eligible for a group
 int gemm_bn(const GemmArgs& g);
 int num_sms();
 // tests: force the 1-CTA (1) or CTA-pair (2) variant where shapes allow; -1 = automatic

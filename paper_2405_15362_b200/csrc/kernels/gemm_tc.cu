@@ -16,6 +16,8 @@
 //   W  dW += dY^T . X  A=[K][M] (MN-major)  B=[K][N] (MN-major)
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -41,6 +43,12 @@ struct Cfg {
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+struct alignas(128) GroupProblem {
+    CUtensorMap ta, tb;
+    void* C;
+    int M, N, K, ldc, tile0, ntiles, num_m, pad;
+};
+
 struct KParams {
     int M, N, K;
     void* C;
@@ -48,7 +56,29 @@ struct KParams {
     const __nv_bfloat16* aux;
     int ldc, ldaux;
     int accumulate;
+    const GroupProblem* group;  // grouped launch: tiles come from this table
+    int ngroup, total_tiles;
 };
+
+// Resolves tile t of the launch: its problem's descriptors, origin, K blocks, output.
+struct TileRef {
+    const CUtensorMap* ta;
+    const CUtensorMap* tb;
+    void* C;
+    int m_blk, n_blk, num_k, ldc;
+};
+template <int BN, int CG>
+__device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int t,
+                                                int& cursor) {
+    if (p.group == nullptr) {
+        const int num_m = p.M / (BM * CG);
+        return TileRef{ta, tb, p.C, t % num_m, t / num_m, p.K / BK, p.ldc};
+    }
+    while (t >= p.group[cursor].tile0 + p.group[cursor].ntiles) ++cursor;  // tiles visited in increasing order
+    const GroupProblem& g = p.group[cursor];
+    const int lt = t - g.tile0;
+    return TileRef{&g.ta, &g.tb, g.C, lt % g.num_m, lt / g.num_m, g.K / BK, g.ldc};
+}
 
 // CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) per
 // 256 x BN tile; each CTA stages its 128 rows of A and BN/2 rows of B, the
@@ -68,14 +98,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = warp_id();
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
-    const int num_m = p.M / (BM * CG), num_n = p.N / BN;
-    const int num_tiles = num_m * num_n;
-    const int num_k = p.K / BK;
+    const int num_tiles = p.group ? p.total_tiles : (p.M / (BM * CG)) * (p.N / BN);
     const int cid = int(blockIdx.x) / CG, ncl = int(gridDim.x) / CG;
 
     if (warp == 0 && elect_one()) {
-        tma_prefetch(&tma_a);
-        tma_prefetch(&tma_b);
+        if (!p.group) {
+            tma_prefetch(&tma_a);
+            tma_prefetch(&tma_b);
+        }
         for (int s = 0; s < C_::kStages; ++s) {
             mbar_init(&full[s], 1);  // leader's expect_tx covers both CTAs' bytes
             mbar_init(&empty[s], 1);
@@ -92,14 +122,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (CG == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            int cursor = 0;
             for (int t = cid; t < num_tiles; t += ncl) {
-                const int m0 = (t % num_m) * BM * CG + int(rank) * BM, n0 = (t / num_m) * BN + int(rank) * C_::kBRows;
+                const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
+                const CUtensorMap* pa = tr.ta;
+                const CUtensorMap* pb = tr.tb;
+                const int num_k = tr.num_k;
+                const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN + int(rank) * C_::kBRows;
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * C_::kStageBytes;
@@ -108,17 +145,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (CG == 1) {
                         mbar_expect_tx(&full[stage], C_::kStageBytes);
                         if constexpr (A_MN) {
-                            tma_load_2d(sa, &tma_a, &full[stage], m0, k0);
-                            tma_load_2d(sa + 8192, &tma_a, &full[stage], m0 + 64, k0);
+                            tma_load_2d(sa, pa, &full[stage], m0, k0);
+                            tma_load_2d(sa + 8192, pa, &full[stage], m0 + 64, k0);
                         } else {
-                            tma_load_2d(sa, &tma_a, &full[stage], k0, m0);
+                            tma_load_2d(sa, pa, &full[stage], k0, m0);
                         }
                         if constexpr (B_MN) {
 #pragma unroll
                             for (int j = 0; j < C_::kBRows / 64; ++j)
-                                tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
+                                tma_load_2d(sb + j * 8192, pb, &full[stage], n0 + 64 * j, k0);
                         } else {
-                            tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
+                            tma_load_2d(sb, pb, &full[stage], k0, n0);
                         }
                     } else {
                         // the peer's bytes may land before the leader arms this phase: the phase
@@ -127,17 +164,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t bar = map_peer(smem_u32(&full[stage]), 0);
                         if (leader) mbar_expect_tx(&full[stage], CG * C_::kStageBytes);
                         if constexpr (A_MN) {
-                            tma_load_2d_2sm(sa, &tma_a, bar, m0, k0);
-                            tma_load_2d_2sm(sa + 8192, &tma_a, bar, m0 + 64, k0);
+                            tma_load_2d_2sm(sa, pa, bar, m0, k0);
+                            tma_load_2d_2sm(sa + 8192, pa, bar, m0 + 64, k0);
                         } else {
-                            tma_load_2d_2sm(sa, &tma_a, bar, k0, m0);
+                            tma_load_2d_2sm(sa, pa, bar, k0, m0);
                         }
                         if constexpr (B_MN) {
 #pragma unroll
                             for (int j = 0; j < C_::kBRows / 64; ++j)
-                                tma_load_2d_2sm(sb + j * 8192, &tma_b, bar, n0 + 64 * j, k0);
+                                tma_load_2d_2sm(sb + j * 8192, pb, bar, n0 + 64 * j, k0);
                         } else {
-                            tma_load_2d_2sm(sb, &tma_b, bar, k0, n0);
+                            tma_load_2d_2sm(sb, pb, bar, k0, n0);
                         }
                     }
                     if (++stage == C_::kStages) stage = 0, phase ^= 1;
@@ -152,7 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            int cursor = 0;
             for (int t = cid; t < num_tiles; t += ncl) {
+                const int num_k = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor).num_k;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -191,8 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_in_tile = int(q * 32 + lane_id());
         int acc = 0;
         uint32_t acc_phase = 0;
+        int cursor = 0;
         for (int t = cid; t < num_tiles; t += ncl) {
-            const int m0 = (t % num_m) * BM * CG + int(rank) * BM, n0 = (t / num_m) * BN;
+            const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
+            const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN;
+            void* const Cout = tr.C;
+            const int ldc = tr.ldc;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = m0 + row_in_tile;
@@ -204,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_wait();
                 const int col = n0 + c;
                 if constexpr (EPI == EPI_F32) {
-                    float* dst = reinterpret_cast<float*>(p.C) + size_t(row) * p.ldc + col;
+                    float* dst = reinterpret_cast<float*>(Cout) + size_t(row) * ldc + col;
                     float4* d4 = reinterpret_cast<float4*>(dst);
                     if (p.accumulate) {
                         // C += acc reduced in L2: no read round trip; one update per element per launch,
@@ -336,27 +379,11 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     (void)attr;
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
-    KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate};
+    KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0};
     const int tiles = (g.M / (BM * CG)) * (g.N / BN);
     const int slots = sm_count() / CG;
     const int grid = (tiles < slots ? tiles : slots) * CG;
-    if constexpr (CG == 1) {
-        kern<<<grid, kThreads, C_::kSmem, s>>>(ta, tb, kp);
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = C_::kSmem;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, kern, ta, tb, kp);
-    }
+    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, CG, ta, tb, kp);
 }
 
 template <int BN, int CG>
@@ -391,9 +418,72 @@ void dispatch(const GemmArgs& g, cudaStream_t s) {
 
 int num_sms() { return sm_count(); }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PB_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int gemm_bn(const GemmArgs& g) {
     const int tiles256 = (g.N % 256 == 0) ? (g.M / BM) * (g.N / 256) : 0;
     return (tiles256 >= num_sms()) ? 256 : 128;
+}
+
+bool gemm_group_ok(const GemmArgs& g) {
+    return g.a_mn && g.b_mn && g.epi == EPI_F32 && g.M % 256 == 0 && g.N % 256 == 0 && g.K % BK == 0;
+}
+
+GemmGroup gemm_group_create(const GemmArgs* probs, int n) {
+    std::vector<GroupProblem> t(size_t(std::max(n, 1)));
+    int tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        const GemmArgs& g = probs[i];
+        if (!gemm_group_ok(g) || g.accumulate != probs[0].accumulate)
+            throw std::invalid_argument("gemm group: problems must be MN/MN fp32 with M, N % 256 == 0");
+        GroupProblem& q = t[i];
+        q.ta = make_map(g.A, g.M, g.K, g.lda, 64, 64);
+        q.tb = make_map(g.B, g.N, g.K, g.ldb, 64, 64);
+        q.C = g.C;
+        q.M = g.M, q.N = g.N, q.K = g.K, q.ldc = g.ldc;
+        q.num_m = g.M / 256;
+        q.tile0 = tiles;
+        q.ntiles = (g.M / 256) * (g.N / 256);
+        tiles += q.ntiles;
+    }
+    GemmGroup out;
+    if (cudaMalloc(&out.table, sizeof(GroupProblem) * t.size()) != cudaSuccess)
+        throw std::runtime_error("gemm group: table allocation failed");
+    if (cudaMemcpy(out.table, t.data(), sizeof(GroupProblem) * t.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("gemm group: table upload failed");
+    out.n = n;
+    out.total_tiles = tiles;
+    out.accumulate = probs[0].accumulate;
+    return out;
+}
+
+void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
+    if (g.n == 0) return;
+    using C_ = Cfg<256, 2>;
+    auto kern = gemm_kernel<256, true, true, EPI_F32, 2>;
+    static bool attr = [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+        return true;
+    }();
+    (void)attr;
+    KParams kp{0, 0, 0, nullptr, nullptr, nullptr, 0, 0, g.accumulate,
+               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles};
+    const int slots = sm_count() / 2;
+    const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
+    CUtensorMap dummy{};
+    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, 2, dummy, dummy, kp);
+}
+
+void gemm_group_destroy(GemmGroup& g) {
+    if (g.table) cudaFree(g.table);
+    g.table = nullptr;
+    g.n = 0;
 }
 
 static int g_force_cg = -1;  // tests: -1 auto, 1 or 2 forced

@@ -45,6 +45,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // y = x * rsqrt(mean(x^2) + eps) * g ; one CTA per row, one 16-byte chunk per thread held in registers
 __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                                    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h, float eps) {
+    pdl_wait();
+    pdl_launch();
     __shared__ float red[32];
     const int row = blockIdx.x, c = threadIdx.x;
     float f[8], w[8];
@@ -66,6 +68,8 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const _
                                    const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
                                    const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int T,
                                    int h) {
+    pdl_wait();
+    pdl_launch();
     __shared__ float red[32];
     const int row = blockIdx.x, c = threadIdx.x;
     float a[8], b[8], w[8], o[8];
@@ -89,10 +93,13 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const _
     reinterpret_cast<uint4*>(dx + size_t(row) * h)[c] = pack8(o);
 }
 
-// dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t] ; thread = 8 columns x `rows_per_block` rows (loads batched)
-__global__ void rmsnorm_dgamma_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                                      const float* __restrict__ rstd, float* __restrict__ dgamma, int T, int h,
-                                      int rows_per_block) {
+// dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t], deterministic two-stage column reduction:
+// stage 1: thread = 8 columns x `rows_per_block` rows -> partial[row_block][h] (no atomics)
+__global__ void rmsnorm_dgamma_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                              const float* __restrict__ rstd, float* __restrict__ partial, int T,
+                                              int h, int rows_per_block) {
+    pdl_wait();
+    pdl_launch();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;  // 8-column chunk
     if (c * 8 >= h) return;
     const int r0 = blockIdx.y * rows_per_block, r1 = min(T, r0 + rows_per_block);
@@ -124,12 +131,38 @@ __global__ void rmsnorm_dgamma_kernel(const __nv_bfloat16* __restrict__ dy, cons
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += a[i] * b[i] * r;
     }
+    float4* dst = reinterpret_cast<float4*>(partial + size_t(blockIdx.y) * h + c * 8);
+    dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+// stage 2: dgamma[j] += sum over row blocks; block = 32 columns x 8 row groups, fixed reduction order
+__global__ void rmsnorm_dgamma_sum_kernel(const float* __restrict__ partial, float* __restrict__ dgamma, int nb,
+                                          int h) {
+    pdl_wait();
+    pdl_launch();
+    __shared__ float red[8][33];
+    const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + cl;
+    float s = 0.f;
+    if (j < h) {
+#pragma unroll 4
+        for (int b = g; b < nb; b += 8) s += partial[size_t(b) * h + j];
+    }
+    red[g][cl] = s;
+    __syncthreads();
+    if (g == 0 && j < h) {
+        float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) atomicAdd(dgamma + c * 8 + i, acc[i]);
+        for (int k = 0; k < 8; ++k) t += red[k][cl];
+        dgamma[j] += t;
+    }
 }
 
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ emb,
                                  __nv_bfloat16* __restrict__ x, int T, int h) {
+    pdl_wait();
+    pdl_launch();
     const int row = blockIdx.x;
     const uint4* src = reinterpret_cast<const uint4*>(emb + size_t(tok[row]) * h);
     uint4* dst = reinterpret_cast<uint4*>(x + size_t(row) * h);
@@ -138,6 +171,8 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
                                  float* __restrict__ demb, int T, int h) {
+    pdl_wait();
+    pdl_launch();
     const int row = blockIdx.x;
     float* dst = demb + size_t(tok[row]) * h;
     const uint4* src = reinterpret_cast<const uint4*>(dx + size_t(row) * h);
@@ -152,6 +187,8 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 // one block per row: loss += (lse - z[label]) * scale ; z <- (softmax(z) - onehot) * scale  (bf16, in place)
 __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ logits, const int32_t* __restrict__ labels,
                                                  float* __restrict__ loss, int V, float scale) {
+    pdl_wait();
+    pdl_launch();
     __shared__ float red[32];
     const int row = blockIdx.x;
     __nv_bfloat16* z = logits + size_t(row) * V;
@@ -215,6 +252,8 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
 __global__ void adamw_kernel(float* __restrict__ w, __nv_bfloat16* __restrict__ wb, float* __restrict__ gr,
                              float* __restrict__ m, float* __restrict__ v, size_t n, float lr, float b1, float b2,
                              float eps, float wd, float bc1, float bc2) {
+    pdl_wait();
+    pdl_launch();
     size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
     const size_t stride = size_t(gridDim.x) * blockDim.x * 4;
     for (; i < n; i += stride) {
@@ -240,6 +279,8 @@ __global__ void adamw_kernel(float* __restrict__ w, __nv_bfloat16* __restrict__ 
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, size_t n) {
+    pdl_wait();
+    pdl_launch();
     size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
     const size_t stride = size_t(gridDim.x) * blockDim.x * 4;
     for (; i < n; i += stride) {
@@ -256,6 +297,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 __global__ void init_normal_kernel(float* __restrict__ w, size_t n, uint64_t seed, float std, float constant) {
+    pdl_wait();
+    pdl_launch();
     size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t stride = size_t(gridDim.x) * blockDim.x;
     for (; i < n; i += stride) {
@@ -281,45 +324,48 @@ int grid_for(size_t n, int per_thread, int block) {
 void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
                  cudaStream_t s) {
     if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
-    rmsnorm_fwd_kernel<<<T, h / 8, 0, s>>>(x, g, y, rstd, T, h, 1e-5f);
+    launch_k(rmsnorm_fwd_kernel, dim3(T), dim3(h / 8), 0, s, 1, x, g, y, rstd, T, h, 1e-5f);
 }
 
 void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
                  const __nv_bfloat16* dres, __nv_bfloat16* dx, int T, int h, cudaStream_t s) {
     if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
-    rmsnorm_bwd_kernel<<<T, h / 8, 0, s>>>(dy, x, g, rstd, dres, dx, T, h);
+    launch_k(rmsnorm_bwd_kernel, dim3(T), dim3(h / 8), 0, s, 1, dy, x, g, rstd, dres, dx, T, h);
 }
 
-void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, int T, int h,
-                    cudaStream_t s) {
+void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, float* scratch,
+                    int T, int h, cudaStream_t s) {
     const int rows = 16;
     const int threads = std::min(256, h / 8);
-    dim3 grid((h / 8 + threads - 1) / threads, (T + rows - 1) / rows);
-    rmsnorm_dgamma_kernel<<<grid, threads, 0, s>>>(dy, x, rstd, dgamma, T, h, rows);
+    const int nb = (T + rows - 1) / rows;
+    dim3 grid((h / 8 + threads - 1) / threads, nb);
+    launch_k(rmsnorm_dgamma_partial_kernel, grid, dim3(threads), 0, s, 1, dy, x, rstd, scratch, T, h, rows);
+    launch_k(rmsnorm_dgamma_sum_kernel, dim3((h + 31) / 32), dim3(256), 0, s, 1, static_cast<const float*>(scratch),
+             dgamma, nb, h);
 }
 
 void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s) {
-    embed_fwd_kernel<<<T, 128, 0, s>>>(tok, emb, x, T, h);
+    launch_k(embed_fwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, emb, x, T, h);
 }
 void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, cudaStream_t s) {
-    embed_bwd_kernel<<<T, 128, 0, s>>>(tok, dx, demb, T, h);
+    launch_k(embed_bwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, dx, demb, T, h);
 }
 void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale,
                    cudaStream_t s) {
     if (V % 8) throw std::invalid_argument("cross_entropy: V % 8");
-    ce_kernel<<<T, 512, 0, s>>>(logits, labels, loss, V, scale);
+    launch_k(ce_kernel, dim3(T), dim3(512), 0, s, 1, logits, labels, loss, V, scale);
 }
 void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
            float eps, float wd, int step, cudaStream_t s) {
     if (n % 4) throw std::invalid_argument("adamw: n % 4");
     const float bc1 = 1.f - powf(b1, float(step)), bc2 = 1.f - powf(b2, float(step));
-    adamw_kernel<<<grid_for(n, 4, 256), 256, 0, s>>>(w, wb, g, m, v, n, lr, b1, b2, eps, wd, bc1, bc2);
+    launch_k(adamw_kernel, dim3(grid_for(n, 4, 256)), dim3(256), 0, s, 1, w, wb, g, m, v, n, lr, b1, b2, eps, wd, bc1, bc2);
 }
 void f32_to_bf16(const float* src, __nv_bfloat16* dst, size_t n, cudaStream_t s) {
-    f32_to_bf16_kernel<<<grid_for(n, 4, 256), 256, 0, s>>>(src, dst, n);
+    launch_k(f32_to_bf16_kernel, dim3(grid_for(n, 4, 256)), dim3(256), 0, s, 1, src, dst, n);
 }
 void init_normal(float* w, size_t n, uint64_t seed, float std, float constant, cudaStream_t s) {
-    init_normal_kernel<<<grid_for(n, 1, 256), 256, 0, s>>>(w, n, seed, std, constant);
+    launch_k(init_normal_kernel, dim3(grid_for(n, 1, 256)), dim3(256), 0, s, 1, w, n, seed, std, constant);
 }
 
 }  // namespace pbk

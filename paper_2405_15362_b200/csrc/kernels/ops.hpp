@@ -30,9 +30,9 @@ void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* 
 // dx = dres (may be null) + d/dx rmsnorm(x)*g applied to dy
 void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
                  const __nv_bfloat16* dres, __nv_bfloat16* dx, int T, int h, cudaStream_t s);
-// dgamma (fp32) += sum_t dy * x * rstd
-void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, int T, int h,
-                    cudaStream_t s);
+// dgamma (fp32) += sum_t dy * x * rstd ; deterministic; scratch >= ceil(T/16) * h floats
+void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, float* scratch,
+                    int T, int h, cudaStream_t s);
 void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s);
 void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, cudaStream_t s);
 // loss (fp32 scalar) += scale * sum_rows CE ; logits <- scale * (softmax - onehot), in place

@@ -29,6 +29,7 @@ from ._lib import KINDS, check, lib, pb_exec_stats, pb_model_cfg, pb_timed_pass
 PB_FLAG_SERIAL = 1
 PB_FLAG_TIMELINE = 2
 PB_FLAG_GEMM_TIMING = 4
+PB_FLAG_KERNEL_TIMING = 8
 
 
 @dataclass
@@ -162,11 +163,20 @@ class DeviceExecutor:
         check(lib().pb_exec_sync(self._h, self._tl, self.num_passes, C.byref(st)))
         return self.timeline(), StepStats.of(st)
 
-    def set_flags(self, timeline: bool = True, serial: bool = False, gemm_timing: bool = False) -> None:
+    def set_flags(self, timeline: bool = True, serial: bool = False, gemm_timing: bool = False,
+                  kernel_timing: bool = False) -> None:
         flags = ((PB_FLAG_TIMELINE if timeline else 0) | (PB_FLAG_SERIAL if serial else 0)
-                 | (PB_FLAG_GEMM_TIMING if gemm_timing else 0))
+                 | (PB_FLAG_GEMM_TIMING if gemm_timing else 0) | (PB_FLAG_KERNEL_TIMING if kernel_timing else 0))
         check(lib().pb_exec_set_flags(self._h, flags))
         self.cfg = __import__("dataclasses").replace(self.cfg, timeline=timeline, serial=serial, gemm_timing=gemm_timing)
+
+    def kernel_report(self) -> Dict[str, list]:
+        import json
+        n = C.c_size_t()
+        check(lib().pb_exec_kernel_report(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().pb_exec_kernel_report(self._h, buf, n.value + 1, C.byref(n)))
+        return json.loads(buf.value.decode() or "{}")
 
     def timeline(self) -> List[pb.TimedPass]:
         if not self.cfg.timeline:
