@@ -112,6 +112,70 @@ int pb_account(const pb_topology* topo, const pb_timed_pass* passes, size_t n, p
                double* peak);
 void pb_schedule_destroy(pb_schedule* s);
 
+/* ------------------------------------------------------------------ analysis
+ * Stable-phase growth of the schedule's building block (growth.hpp), the
+ * adaptive V-family search (search.hpp) and Gantt rendering (render.hpp).
+ * Growth needs a schedule that carries its block (built by pb_schedule_build
+ * or pb_search, or parsed from a document with a "block"). */
+typedef struct pb_growth_report { /* GrowthReport (growth.hpp:13-22) */
+    int32_t cycle_length;
+    double growth;           /* time gained per period */
+    double max_work;
+    double repeating_bubble; /* max(0, growth - max_work) */
+    int32_t linear_bubble;   /* O(n) bubble */
+    int32_t tie;
+} pb_growth_report;
+/* growth_rate (growth.hpp:141-187).  work: `devices` entries or NULL; witness:
+ * the maximal chain, one "F(stage s, slot k)@periodP" per line (len = bytes needed). */
+int pb_growth_rate(const pb_schedule* s, const pb_profile* prof, pb_growth_report* out, double* work, char* witness,
+                   size_t cap, size_t* len);
+int pb_growth_rate_unrolled(const pb_schedule* s, const pb_profile* prof, int32_t periods, double* out); /* :132 */
+int pb_vhalf_condition(const pb_profile* prof, int32_t* out);                                           /* :190 */
+int pb_lower_bound(int64_t n, int64_t d, int64_t k, int64_t* out);                                      /* :195 */
+int pb_min_memory_for_od_bubble(int32_t d, double* out);                                                /* :202 */
+
+typedef struct pb_search_spec { /* SearchSpec (search.hpp:15-25) */
+    int32_t devices;
+    int32_t microbatches; /* 0 = 3 * devices */
+    pb_profile profile;
+    double memory_limit; /* units of m */
+    int64_t delta_max, tau_max;
+} pb_search_spec;
+typedef struct pb_search_params { /* SearchParams (search.hpp:27-42) */
+    int32_t K;
+    int64_t d0_lo, d1_lo, d0_hi, d1_hi, tau1, tau2, tau3;
+} pb_search_params;
+typedef struct pb_search_result { /* SearchResult scalars (search.hpp:44-56) */
+    int32_t feasible;
+    pb_search_params best;
+    double bubble_rate, exact_peak;
+    int64_t enumerated, evaluated;
+    double family_min_peak;
+    int32_t turn_devices_exercised;
+} pb_search_result;
+typedef struct pb_frontier_point { /* FrontierPoint (search.hpp:58-64) */
+    double limit;
+    int32_t feasible;
+    double bubble_rate, exact_peak;
+    pb_search_params best;
+} pb_frontier_point;
+/* search (search.hpp:235).  message: the infeasibility text ("" when feasible).
+ * schedule (optional): the winner assembled at spec->microbatches, executable by
+ * pb_exec_create unchanged; NULL when infeasible. */
+int pb_search(const pb_search_spec* spec, pb_search_result* out, char* message, size_t cap, size_t* len,
+              pb_schedule** schedule);
+int pb_frontier(const pb_search_spec* spec, const double* limits, size_t n, pb_frontier_point* out); /* :240 */
+
+enum { PB_RENDER_SVG = 0, PB_RENDER_ASCII = 1 };
+/* render_svg / render_ascii (render.hpp:83,177) of the schedule's document. */
+int pb_render(const pb_schedule* s, int32_t format, const char* title, int32_t ascii_max_width, int32_t ascii_color,
+              char* buf, size_t cap, size_t* len);
+/* A measured timeline as a "time" ScheduleDocument (document_from_timed, document.hpp:413), emitted as JSON or rendered. */
+int pb_timed_emit(const pb_topology* topo, const pb_timed_pass* passes, size_t n, int32_t microbatches, char* buf,
+                  size_t cap, size_t* len);
+int pb_timed_render(const pb_topology* topo, const pb_timed_pass* passes, size_t n, int32_t microbatches,
+                    int32_t format, const char* title, int32_t ascii_max_width, char* buf, size_t cap, size_t* len);
+
 /* ------------------------------------------------------------------ executor
  * GPT-style decoder stack (pre-norm RMSNorm, causal MHA with head_dim 128,
  * GELU MLP 4h, residual, untied embedding / LM head, mean cross-entropy),

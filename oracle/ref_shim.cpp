@@ -9,6 +9,9 @@
 //   build_entry (gallery.hpp:499) -> assemble (assemble.hpp:405)
 //   exact_peak (memory.hpp:63), simulate (simulate.hpp:22)
 //   document_from_grid + emit (document.hpp:188,403)
+// plus the analysis side through one JSON request/response call:
+//   growth_rate (growth.hpp:141), search/frontier (search.hpp:235,240),
+//   render_svg/render_ascii (render.hpp:83,177) of grid and simulated-time documents
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -17,6 +20,9 @@
 #include "pipeblock/assemble.hpp"
 #include "pipeblock/document.hpp"
 #include "pipeblock/gallery.hpp"
+#include "pipeblock/growth.hpp"
+#include "pipeblock/render.hpp"
+#include "pipeblock/search.hpp"
 #include "pipeblock/memory.hpp"
 #include "pipeblock/simulate.hpp"
 
@@ -120,6 +126,84 @@ double ref_time_pipeline(const char* entry, int d, int n, int iters, double f, d
     auto t1 = std::chrono::steady_clock::now();
     if (sink < 0) return -1;
     return std::chrono::duration<double>(t1 - t0).count() / iters;
+}
+
+
+// ref_analysis(request JSON) -> response JSON (or {"error": what}).
+int ref_analysis(const char* request, char* buf, size_t cap, size_t* len) {
+    using nlohmann::ordered_json;
+    ordered_json out;
+    try {
+        auto rq = ordered_json::parse(request);
+        std::string op = rq.at("op");
+        auto prof = [&] {
+            auto p = rq.value("profile", std::vector<double>{1, 1, 1, 0});
+            return RunTimeProfile{p[0], p[1], p[2], p[3]};
+        };
+        if (op == "growth") {
+            auto blk = build_entry(rq.at("entry").get<std::string>(), rq.at("d").get<int>()).block;
+            auto g = growth_rate(blk, prof());
+            out = {{"cycle_length", g.cycle_length}, {"growth", g.growth}, {"work", g.work_per_period},
+                   {"max_work", g.max_work}, {"repeating_bubble", g.repeating_bubble},
+                   {"linear_bubble", g.linear_bubble}, {"tie", g.tie}, {"witness", g.witness},
+                   {"unrolled3", growth_rate_unrolled(blk, prof(), 3)}};
+        } else if (op == "search" || op == "frontier") {
+            SearchSpec sp;
+            sp.d = rq.at("d");
+            sp.n = rq.value("n", 0);
+            sp.profile = prof();
+            sp.memory_limit = rq.value("limit", 0.0);
+            sp.delta_max = rq.value("delta_max", 6LL);
+            sp.tau_max = rq.value("tau_max", 6LL);
+            auto P = [](const SearchParams& b) {
+                return std::vector<long long>{b.K, b.d0_lo, b.d1_lo, b.d0_hi, b.d1_hi, b.tau1, b.tau2, b.tau3};
+            };
+            if (op == "search") {
+                auto r = search(sp);
+                out = {{"feasible", r.feasible}, {"message", r.message}, {"best", P(r.best)}, {"best_str", r.best.str()},
+                       {"bubble_rate", r.bubble_rate}, {"exact_peak", r.exact_peak},
+                       {"enumerated", r.candidates_enumerated}, {"evaluated", r.candidates_evaluated},
+                       {"family_min_peak", r.family_min_peak}, {"turn", r.turn_devices_exercised}};
+                if (r.feasible) {
+                    std::vector<std::vector<long long>> ps;
+                    for (const auto& q : r.schedule.passes)
+                        ps.push_back({q.device, q.stage, int(q.kind), q.microbatch, q.start, q.duration});
+                    out["passes"] = ps;
+                }
+            } else {
+                auto pts = frontier(sp, rq.at("limits").get<std::vector<double>>());
+                out = ordered_json::array();
+                for (const auto& q : pts)
+                    out.push_back({{"limit", q.limit}, {"feasible", q.feasible}, {"bubble_rate", q.bubble_rate},
+                                   {"exact_peak", q.exact_peak}, {"best", P(q.best)}});
+            }
+        } else if (op == "render") {
+            auto build = build_entry(rq.at("entry").get<std::string>(), rq.at("d").get<int>());
+            auto g = assemble(build, rq.at("n").get<int>());
+            RenderOptions ro;
+            ro.ascii_max_width = rq.value("max_width", 200);
+            ro.ascii_color = rq.value("color", false);
+            ro.title = rq.value("title", std::string());
+            ScheduleDocument doc;
+            if (rq.value("timed", false)) {
+                doc = document_from_timed(simulate(g, prof()).schedule);
+                out["emit"] = emit(doc);
+            } else {
+                doc = document_from_grid(g);
+                doc.metadata.source_block = build.entry;
+            }
+            out["svg"] = render_svg(doc, ro);
+            out["ascii"] = render_ascii(doc, ro);
+        } else {
+            throw std::invalid_argument("unknown op " + op);
+        }
+    } catch (const std::exception& e) {
+        out = {{"error", e.what()}};
+    }
+    std::string t = out.dump();
+    *len = t.size();
+    if (buf && cap >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
 }
 
 }  // extern "C"

@@ -84,3 +84,14 @@ def reemit(text: str, strict: bool = False):
 
 def time_pipeline(entry: str, d: int, n: int, iters: int = 3, prof=(1.0, 1.0, 1.0)) -> float:
     return lib().ref_time_pipeline(entry.encode(), d, n, iters, *prof)
+
+
+def analysis(**request):
+    """Reference growth / search / frontier / render through one JSON call (ref_shim.cpp ref_analysis)."""
+    import json
+    text = json.dumps(request).encode()
+    ln = C.c_size_t()
+    lib().ref_analysis(text, None, 0, C.byref(ln))
+    buf = C.create_string_buffer(ln.value + 1)
+    lib().ref_analysis(text, buf, ln.value + 1, C.byref(ln))
+    return json.loads(buf.value.decode())

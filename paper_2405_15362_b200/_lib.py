@@ -103,3 +103,34 @@ def check(rc: int) -> None:
     if rc == PB_EDOC:
         raise DocumentError(rc, msg)
     raise PipeblockError(rc, msg)
+
+
+class pb_growth_report(C.Structure):
+    _fields_ = [("cycle_length", C.c_int32), ("growth", C.c_double), ("max_work", C.c_double),
+                ("repeating_bubble", C.c_double), ("linear_bubble", C.c_int32), ("tie", C.c_int32)]
+
+
+class pb_search_spec(C.Structure):
+    _fields_ = [("devices", C.c_int32), ("microbatches", C.c_int32), ("profile", pb_profile),
+                ("memory_limit", C.c_double), ("delta_max", C.c_int64), ("tau_max", C.c_int64)]
+
+
+class pb_search_params(C.Structure):
+    _fields_ = [("K", C.c_int32), ("d0_lo", C.c_int64), ("d1_lo", C.c_int64), ("d0_hi", C.c_int64),
+                ("d1_hi", C.c_int64), ("tau1", C.c_int64), ("tau2", C.c_int64), ("tau3", C.c_int64)]
+
+
+class pb_search_result(C.Structure):
+    _fields_ = [("feasible", C.c_int32), ("best", pb_search_params), ("bubble_rate", C.c_double),
+                ("exact_peak", C.c_double), ("enumerated", C.c_int64), ("evaluated", C.c_int64),
+                ("family_min_peak", C.c_double), ("turn_devices_exercised", C.c_int32)]
+
+
+class pb_frontier_point(C.Structure):
+    _fields_ = [("limit", C.c_double), ("feasible", C.c_int32), ("bubble_rate", C.c_double),
+                ("exact_peak", C.c_double), ("best", pb_search_params)]
+
+
+EXPORTS += ["pb_growth_rate", "pb_growth_rate_unrolled", "pb_vhalf_condition", "pb_lower_bound",
+            "pb_min_memory_for_od_bubble", "pb_search", "pb_frontier", "pb_render", "pb_timed_emit",
+            "pb_timed_render"]

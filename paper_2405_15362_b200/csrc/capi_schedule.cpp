@@ -190,3 +190,154 @@ extern "C" void pb_schedule_destroy(pb_schedule* s) { delete s; }
 namespace pbx {
 const Grid& schedule_grid(const pb_schedule* s) { return s->grid; }
 }  // namespace pbx
+
+// ============================================================ analysis
+namespace {
+
+void put_text(const std::string& t, char* buf, size_t cap, size_t* len) {
+    if (len) *len = t.size();
+    if (!buf) return;
+    if (cap < t.size() + 1) throw pbx::Space("text buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+}
+
+Profile profile_from_c(const pb_profile* p) {
+    if (!p) throw std::invalid_argument("null profile");
+    return Profile{p->f, p->b, p->w, p->comm};
+}
+
+const Block& block_of(const pb_schedule* s) {
+    if (!s) throw std::invalid_argument("null schedule");
+    if (!s->doc.block) throw std::invalid_argument("schedule carries no building block (made from passes)");
+    return *s->doc.block;
+}
+
+SearchSpec spec_from_c(const pb_search_spec* c) {
+    if (!c) throw std::invalid_argument("null search spec");
+    SearchSpec s;
+    s.d = c->devices;
+    s.n = c->microbatches;
+    s.profile = profile_from_c(&c->profile);
+    s.memory_limit = c->memory_limit;
+    s.delta_max = c->delta_max;
+    s.tau_max = c->tau_max;
+    return s;
+}
+
+pb_search_params params_to_c(const SearchParams& p) {
+    return {p.K, p.d0_lo, p.d1_lo, p.d0_hi, p.d1_hi, p.tau1, p.tau2, p.tau3};
+}
+
+Timed timed_from_c(const pb_topology* topo, const pb_timed_pass* passes, size_t n, int32_t microbatches) {
+    if (n && !passes) throw std::invalid_argument("null passes");
+    Timed t;
+    t.topo = topo_from_c(topo);
+    t.microbatches = microbatches;
+    for (size_t i = 0; i < n; ++i) {
+        const auto& p = passes[i];
+        if (p.device < 1 || p.device > t.topo.devices) throw std::invalid_argument("device out of range");
+        if (p.kind < 0 || p.kind > 3) throw std::invalid_argument("kind must be 0..3");
+        t.ops.push_back({p.device, p.stage, Kind(p.kind), p.microbatch, p.start, p.duration});
+    }
+    return t;
+}
+
+}  // namespace
+
+extern "C" int pb_growth_rate(const pb_schedule* s, const pb_profile* prof, pb_growth_report* out, double* work,
+                              char* witness, size_t cap, size_t* len) {
+    return pbx::guard([&] {
+        Growth g = growth_rate(block_of(s), profile_from_c(prof));
+        if (out) *out = {g.cycle_length, g.growth, g.max_work, g.repeating_bubble, int32_t(g.linear_bubble), int32_t(g.tie)};
+        if (work) std::memcpy(work, g.work_per_period.data(), g.work_per_period.size() * sizeof(double));
+        std::string w;
+        for (const auto& x : g.witness) w += x + "\n";
+        put_text(w, witness, cap, len);
+    });
+}
+
+extern "C" int pb_growth_rate_unrolled(const pb_schedule* s, const pb_profile* prof, int32_t periods, double* out) {
+    return pbx::guard([&] {
+        if (!out || periods < 1) throw std::invalid_argument("bad argument");
+        *out = growth_rate_unrolled(block_of(s), profile_from_c(prof), periods);
+    });
+}
+
+extern "C" int pb_vhalf_condition(const pb_profile* prof, int32_t* out) {
+    return pbx::guard([&] {
+        if (!out) throw std::invalid_argument("null argument");
+        *out = vhalf_condition(profile_from_c(prof));
+    });
+}
+
+extern "C" int pb_lower_bound(int64_t n, int64_t d, int64_t k, int64_t* out) {
+    return pbx::guard([&] {
+        if (!out) throw std::invalid_argument("null argument");
+        *out = makespan_lower_bound(n, d, k);
+    });
+}
+
+extern "C" int pb_min_memory_for_od_bubble(int32_t d, double* out) {
+    return pbx::guard([&] {
+        if (!out) throw std::invalid_argument("null argument");
+        *out = min_memory_for_od_bubble(d);
+    });
+}
+
+extern "C" int pb_search(const pb_search_spec* spec, pb_search_result* out, char* message, size_t cap, size_t* len,
+                         pb_schedule** schedule) {
+    return pbx::guard([&] {
+        if (!out) throw std::invalid_argument("null argument");
+        SearchSpec sp = spec_from_c(spec);
+        SearchResult r = search(sp);
+        *out = {int32_t(r.feasible), params_to_c(r.best), r.bubble_rate, r.exact_peak, r.enumerated, r.evaluated,
+                r.family_min_peak, int32_t(r.turn_devices_exercised)};
+        put_text(r.message, message, cap, len);
+        if (schedule) {
+            *schedule = nullptr;
+            if (r.feasible) {
+                Document d = document_for_assembly(r.build, r.schedule, true, true);
+                *schedule = finish(std::move(r.schedule), std::move(d));
+            }
+        }
+    });
+}
+
+extern "C" int pb_frontier(const pb_search_spec* spec, const double* limits, size_t n, pb_frontier_point* out) {
+    return pbx::guard([&] {
+        if (n && (!limits || !out)) throw std::invalid_argument("null argument");
+        auto pts = frontier(spec_from_c(spec), std::vector<double>(limits, limits + n));
+        for (size_t i = 0; i < pts.size(); ++i)
+            out[i] = {pts[i].limit, int32_t(pts[i].feasible), pts[i].bubble_rate, pts[i].exact_peak,
+                      params_to_c(pts[i].best)};
+    });
+}
+
+extern "C" int pb_render(const pb_schedule* s, int32_t format, const char* title, int32_t ascii_max_width,
+                         int32_t ascii_color, char* buf, size_t cap, size_t* len) {
+    return pbx::guard([&] {
+        if (!s) throw std::invalid_argument("null schedule");
+        RenderOptions o;
+        if (title) o.title = title;
+        if (ascii_max_width > 0) o.ascii_max_width = ascii_max_width;
+        o.ascii_color = ascii_color != 0;
+        put_text(format == PB_RENDER_ASCII ? render_ascii(s->doc, o) : render_svg(s->doc, o), buf, cap, len);
+    });
+}
+
+extern "C" int pb_timed_emit(const pb_topology* topo, const pb_timed_pass* passes, size_t n, int32_t microbatches,
+                             char* buf, size_t cap, size_t* len) {
+    return pbx::guard([&] { put_text(emit_document(document_for_timed(timed_from_c(topo, passes, n, microbatches))), buf, cap, len); });
+}
+
+extern "C" int pb_timed_render(const pb_topology* topo, const pb_timed_pass* passes, size_t n, int32_t microbatches,
+                               int32_t format, const char* title, int32_t ascii_max_width, char* buf, size_t cap,
+                               size_t* len) {
+    return pbx::guard([&] {
+        Document d = document_for_timed(timed_from_c(topo, passes, n, microbatches));
+        RenderOptions o;
+        if (title) o.title = title;
+        if (ascii_max_width > 0) o.ascii_max_width = ascii_max_width;
+        put_text(format == PB_RENDER_ASCII ? render_ascii(d, o) : render_svg(d, o), buf, cap, len);
+    });
+}

@@ -23,6 +23,8 @@
 
 #include <cstdint>
 #include <functional>
+#include <limits>
+#include <tuple>
 #include <map>
 #include <optional>
 #include <stdexcept>
@@ -215,5 +217,92 @@ Document parse_document(const std::string& text, bool strict = false);
 std::string emit_document(const Document& d);
 Document document_for_assembly(const Build& b, const Grid& g, bool sq, bool re);
 Document document_for_timed(const Timed& t);
+
+// ---- growth (growth.hpp) — vanalysis.cpp ----
+struct Growth {  // growth.hpp:13-22
+    int cycle_length = 0;
+    double growth = 0.0;
+    std::vector<double> work_per_period;
+    double max_work = 0.0;
+    double repeating_bubble = 0.0;
+    bool linear_bubble = false;
+    bool tie = false;
+    std::vector<std::string> witness;
+};
+Growth growth_rate(const Block& blk, const Profile& prof);
+double growth_rate_unrolled(const Block& blk, const Profile& prof, int periods);
+bool vhalf_condition(const Profile& p);
+int64_t makespan_lower_bound(int64_t n, int64_t d, int64_t k);  // growth.hpp:195 lower_bound
+double min_memory_for_od_bubble(int d);
+
+// ---- adaptive search (search.hpp) — vanalysis.cpp ----
+struct SearchSpec {  // search.hpp:15-25
+    int d = 0;
+    int n = 0;  // 0 -> 3d
+    Profile profile;
+    double memory_limit = 0.0;  // units of m
+    int64_t delta_max = 6, tau_max = 6;
+    int eval_n() const { return n > 0 ? n : 3 * d; }
+};
+struct SearchParams {  // search.hpp:27-42
+    int K = 1;
+    int64_t d0_lo = 1, d1_lo = 1, d0_hi = 1, d1_hi = 1;
+    int64_t tau1 = 1, tau2 = 1, tau3 = 1;
+    auto key() const { return std::tie(K, d0_lo, d1_lo, d0_hi, d1_hi, tau1, tau2, tau3); }
+    std::string str() const;
+    VEdges edges(int d) const;
+};
+struct SearchResult {  // search.hpp:44-56
+    bool feasible = false;
+    std::string message;
+    SearchParams best;
+    Build build;
+    Grid schedule;
+    double bubble_rate = 1.0, exact_peak = 0.0;
+    int64_t enumerated = 0, evaluated = 0;
+    double family_min_peak = 0.0;
+    bool turn_devices_exercised = false;
+};
+struct FrontierPoint {
+    double limit = 0.0;
+    bool feasible = false;
+    double bubble_rate = 1.0, exact_peak = 0.0;
+    SearchParams best;
+};
+class Family {  // search.hpp:121-206 FamilyEvaluation
+  public:
+    struct Eval {
+        SearchParams params;
+        double peak = 0.0, bubble = 1.0;
+    };
+    explicit Family(const SearchSpec& spec);
+    int64_t enumerated() const { return enumerated_; }
+    int64_t evaluated() const { return int64_t(evals_.size()); }
+    double family_min_peak() const { return min_peak_; }
+    std::optional<Eval> best_under(double limit) const;
+    Block rebuild(const SearchParams& p) const;
+    Build build_of(const SearchParams& p) const;
+
+  private:
+    static constexpr int64_t kInterval = 6;
+    SearchSpec spec_;
+    int64_t enumerated_ = 0;
+    double min_peak_ = std::numeric_limits<double>::infinity();
+    std::vector<Eval> evals_;
+};
+SearchResult search_with(const Family& fam, const SearchSpec& spec);
+SearchResult search(const SearchSpec& spec);
+std::vector<FrontierPoint> frontier(const SearchSpec& spec, const std::vector<double>& limits);
+
+// ---- render (render.hpp) — vanalysis.cpp ----
+struct RenderOptions {
+    bool stamp = false;
+    std::string title;
+    int ascii_max_width = 200;
+    bool ascii_color = false;
+    std::vector<char> highlight;
+};
+std::string render_svg(const Document& doc, const RenderOptions& opt = {});
+std::string render_ascii(const Document& doc, const RenderOptions& opt = {});
 
 }  // namespace vsched

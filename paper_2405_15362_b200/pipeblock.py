@@ -8,6 +8,10 @@ Names, argument meaning and error behaviour follow the reference headers:
     simulate(schedule, profile)        simulate.hpp:22-86
     validate_schedule(...)             assemble.hpp:138-183 (done on every construction)
     parse(text, strict) / emit(doc)    document.hpp:188-401
+    growth_rate / vhalf_condition ...  growth.hpp:132-205
+    search / frontier                  search.hpp:208-259
+    render_svg / render_ascii          render.hpp:83-256
+    emit_timed / render_timed          document_from_timed (document.hpp:413) + emit / render
 
 Errors raise ScheduleError (the reference's std::invalid_argument) or
 DocumentError (pipeblock::DocumentError) carrying the same messages.
@@ -18,12 +22,16 @@ import ctypes as C
 from dataclasses import dataclass
 from typing import List, NamedTuple, Optional, Sequence
 
-from ._lib import (KINDS, DocumentError, PipeblockError, ScheduleError, check, lib, pb_pass, pb_profile,
-                   pb_sim_stats, pb_timed_pass, pb_topology)
+from ._lib import (KINDS, DocumentError, PipeblockError, ScheduleError, check, lib, pb_frontier_point,
+                   pb_growth_report, pb_pass, pb_profile, pb_search_result, pb_search_spec, pb_sim_stats,
+                   pb_timed_pass, pb_topology)
 
 __all__ = ["GridPass", "TimedPass", "Topology", "RunTimeProfile", "BlockBuild", "GridSchedule", "SimResult",
            "build_entry", "assemble", "exact_peak", "simulate", "account", "parse", "emit", "schedule_from_passes",
-           "fnv1a64", "ScheduleError", "DocumentError", "PipeblockError"]
+           "fnv1a64", "ScheduleError", "DocumentError", "PipeblockError", "GrowthReport", "growth_rate",
+           "growth_rate_unrolled", "vhalf_condition", "lower_bound", "min_memory_for_od_bubble", "SearchSpec",
+           "SearchParams", "SearchResult", "FrontierPoint", "search", "frontier", "render_svg", "render_ascii",
+           "emit_timed", "render_timed"]
 
 
 class GridPass(NamedTuple):  # model.hpp:162-176 (ScheduledPassT<long long>)
@@ -221,3 +229,183 @@ def account(topology: Topology, passes: Sequence[TimedPass]) -> SimResult:
     check(lib().pb_account(C.byref(topo), arr, len(passes), C.byref(st), busy, peak))
     return SimResult(sorted(passes, key=lambda p: (p.device, p.start, p.stage, p.microbatch)), st.makespan,
                      list(busy), [st.makespan - b for b in busy], [], st.bubble_rate, list(peak))
+
+
+# ---------------------------------------------------------------- analysis
+def _text(fn, *args) -> str:
+    n = C.c_size_t()
+    check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(fn(*args, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def _prof(p: RunTimeProfile) -> pb_profile:
+    return pb_profile(p.f, p.b, p.w, p.comm)
+
+
+@dataclass
+class GrowthReport:  # growth.hpp:13-22
+    cycle_length: int
+    growth: float
+    work_per_period: List[float]
+    max_work: float
+    repeating_bubble: float
+    linear_bubble: bool
+    tie: bool
+    witness: List[str]
+
+
+def _block_schedule(x) -> GridSchedule:
+    # a BlockBuild names a gallery block; one instance carries it (growth needs the block only)
+    return assemble(x, 1, False, False) if isinstance(x, BlockBuild) else x
+
+
+def growth_rate(block, profile: RunTimeProfile = RunTimeProfile()) -> GrowthReport:
+    """growth_rate(blk, profile) (growth.hpp:141-187); `block` is a BlockBuild or a GridSchedule carrying one."""
+    s = _block_schedule(block)
+    rep = pb_growth_report()
+    work = (C.c_double * s.topology.devices)()
+    prof = _prof(profile)
+    wit = _text(lambda *a: lib().pb_growth_rate(s.handle, C.byref(prof), C.byref(rep), work, *a))
+    return GrowthReport(rep.cycle_length, rep.growth, list(work), rep.max_work, rep.repeating_bubble,
+                        bool(rep.linear_bubble), bool(rep.tie), wit.splitlines())
+
+
+def growth_rate_unrolled(block, profile: RunTimeProfile, periods: int) -> float:
+    s = _block_schedule(block)
+    out = C.c_double()
+    prof = _prof(profile)
+    check(lib().pb_growth_rate_unrolled(s.handle, C.byref(prof), periods, C.byref(out)))
+    return out.value
+
+
+def vhalf_condition(profile: RunTimeProfile) -> bool:
+    out = C.c_int32()
+    prof = _prof(profile)
+    check(lib().pb_vhalf_condition(C.byref(prof), C.byref(out)))
+    return bool(out.value)
+
+
+def lower_bound(n: int, d: int, k: int) -> int:
+    out = C.c_int64()
+    check(lib().pb_lower_bound(n, d, k, C.byref(out)))
+    return out.value
+
+
+def min_memory_for_od_bubble(d: int) -> float:
+    out = C.c_double()
+    check(lib().pb_min_memory_for_od_bubble(d, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class SearchSpec:  # search.hpp:15-25
+    d: int
+    n: int = 0
+    profile: RunTimeProfile = RunTimeProfile()
+    memory_limit: float = 0.0
+    delta_max: int = 6
+    tau_max: int = 6
+
+    def _c(self):
+        return pb_search_spec(self.d, self.n, _prof(self.profile), self.memory_limit, self.delta_max, self.tau_max)
+
+
+class SearchParams(NamedTuple):  # search.hpp:27-42
+    K: int
+    d0_lo: int
+    d1_lo: int
+    d0_hi: int
+    d1_hi: int
+    tau1: int
+    tau2: int
+    tau3: int
+
+    @staticmethod
+    def _from(c) -> "SearchParams":
+        return SearchParams(c.K, c.d0_lo, c.d1_lo, c.d0_hi, c.d1_hi, c.tau1, c.tau2, c.tau3)
+
+    def str(self) -> str:
+        return (f"K={self.K} d0=({self.d0_lo},{self.d0_hi}) d1=({self.d1_lo},{self.d1_hi}) "
+                f"tau=({self.tau1},{self.tau2},{self.tau3})")
+
+
+@dataclass
+class SearchResult:  # search.hpp:44-56
+    feasible: bool
+    message: str
+    best: SearchParams
+    schedule: Optional[GridSchedule]
+    bubble_rate: float
+    exact_peak: float
+    candidates_enumerated: int
+    candidates_evaluated: int
+    family_min_peak: float
+    turn_devices_exercised: bool
+
+
+def search(spec: SearchSpec) -> SearchResult:
+    """search(spec) (search.hpp:235); the winner's schedule runs on the executor unchanged."""
+    r = pb_search_result()
+    h = C.c_void_p()
+    c = spec._c()
+    msg = _text(lambda *a: lib().pb_search(C.byref(c), C.byref(r), *a[:3], C.byref(h)) if a[0] is not None
+                else lib().pb_search(C.byref(c), C.byref(r), *a, None))
+    return SearchResult(bool(r.feasible), msg, SearchParams._from(r.best), GridSchedule(h) if h.value else None,
+                        r.bubble_rate, r.exact_peak, r.enumerated, r.evaluated, r.family_min_peak,
+                        bool(r.turn_devices_exercised))
+
+
+@dataclass
+class FrontierPoint:  # search.hpp:58-64
+    limit: float
+    feasible: bool
+    bubble_rate: float
+    exact_peak: float
+    best: SearchParams
+
+
+def frontier(spec: SearchSpec, limits: Sequence[float]) -> List[FrontierPoint]:
+    c = spec._c()
+    arr = (C.c_double * max(1, len(limits)))(*limits)
+    out = (pb_frontier_point * max(1, len(limits)))()
+    check(lib().pb_frontier(C.byref(c), arr, len(limits), out))
+    return [FrontierPoint(p.limit, bool(p.feasible), p.bubble_rate, p.exact_peak, SearchParams._from(p.best))
+            for p in out[:len(limits)]]
+
+
+PB_RENDER_SVG, PB_RENDER_ASCII = 0, 1
+
+
+def render_svg(schedule: GridSchedule, title: str = "") -> str:
+    """render_svg(document) (render.hpp:83-172) of the schedule's document."""
+    return _text(lambda *a: lib().pb_render(schedule.handle, PB_RENDER_SVG, title.encode(), 0, 0, *a))
+
+
+def render_ascii(schedule: GridSchedule, max_width: int = 200, color: bool = False) -> str:
+    """render_ascii(document) (render.hpp:177-256)."""
+    return _text(lambda *a: lib().pb_render(schedule.handle, PB_RENDER_ASCII, None, max_width, int(color), *a))
+
+
+def _timed_c(passes: Sequence[TimedPass]):
+    arr = (pb_timed_pass * max(len(passes), 1))()
+    for i, p in enumerate(passes):
+        arr[i] = pb_timed_pass(p.device, p.stage, KINDS.index(p.kind), p.microbatch, p.start, p.duration)
+    return arr
+
+
+def emit_timed(topology: Topology, passes: Sequence[TimedPass], microbatches: int) -> str:
+    """emit(document_from_timed(...)) (document.hpp:188,413): a measured timeline as a 'time' document."""
+    topo, keep = topology._c()
+    arr = _timed_c(passes)
+    return _text(lambda *a: lib().pb_timed_emit(C.byref(topo), arr, len(passes), microbatches, *a))
+
+
+def render_timed(topology: Topology, passes: Sequence[TimedPass], microbatches: int, fmt: str = "svg",
+                 title: str = "", max_width: int = 200) -> str:
+    topo, keep = topology._c()
+    arr = _timed_c(passes)
+    f = PB_RENDER_ASCII if fmt == "ascii" else PB_RENDER_SVG
+    return _text(lambda *a: lib().pb_timed_render(C.byref(topo), arr, len(passes), microbatches, f, title.encode(),
+                                                  max_width, *a))
