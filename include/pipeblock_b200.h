@@ -252,6 +252,24 @@ int pb_exec_param_info(const pb_exec* e, int32_t i, char* name, size_t cap, int6
 int pb_exec_param_get(pb_exec* e, int32_t i, int32_t which /*0 weight bf16->f32, 1 grad f32*/, float* host);
 int pb_exec_param_set(pb_exec* e, int32_t i, const float* host); /* rounds to bf16, sets fp32 master */
 int pb_exec_zero_grads(pb_exec* e);
+
+/* The host-side execution plan of one pipeline device — a pure function of the
+ * schedule, so every rank derives its peers' outbox layout without talking
+ * (csrc/exec/plan.hpp).  Needs no GPU. */
+typedef struct pb_plan_op {
+    int32_t stage, kind, microbatch;
+    int32_t slot;        /* activation-pool slot of (stage, microbatch) on this device */
+    int64_t start;       /* grid cell */
+    int32_t recv_from;   /* 0, or the device whose outbox this op pulls its input from */
+    int32_t recv_outbox; /* outbox slot on recv_from */
+    uint32_t recv_gen;   /* generation of that outbox slot within the step */
+    int32_t send_to;     /* 0, or the device that consumes this op's output */
+    int32_t send_outbox; /* outbox slot on this device */
+    uint32_t send_gen;
+} pb_plan_op;
+/* Passes of `device` in grid order; *slots = activation slots (= exact_peak), *outboxes = outbox slots. */
+int pb_plan_device(const pb_schedule* s, int32_t device, pb_plan_op* out, size_t cap, size_t* n, int32_t* slots,
+                   int32_t* outboxes);
 void pb_exec_destroy(pb_exec* e);
 
 #ifdef __cplusplus

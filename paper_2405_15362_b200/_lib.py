@@ -134,3 +134,12 @@ class pb_frontier_point(C.Structure):
 EXPORTS += ["pb_growth_rate", "pb_growth_rate_unrolled", "pb_vhalf_condition", "pb_lower_bound",
             "pb_min_memory_for_od_bubble", "pb_search", "pb_frontier", "pb_render", "pb_timed_emit",
             "pb_timed_render"]
+
+
+class pb_plan_op(C.Structure):
+    _fields_ = [("stage", C.c_int32), ("kind", C.c_int32), ("microbatch", C.c_int32), ("slot", C.c_int32),
+                ("start", C.c_int64), ("recv_from", C.c_int32), ("recv_outbox", C.c_int32), ("recv_gen", C.c_uint32),
+                ("send_to", C.c_int32), ("send_outbox", C.c_int32), ("send_gen", C.c_uint32)]
+
+
+EXPORTS += ["pb_plan_device"]

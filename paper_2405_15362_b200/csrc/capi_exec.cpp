@@ -167,3 +167,43 @@ extern "C" int pb_exec_kernel_report(pb_exec* h, char* buf, size_t cap, size_t* 
         std::memcpy(buf, r.c_str(), r.size() + 1);
     });
 }
+
+// Host-side execution plan of one pipeline device (no GPU needed): what a rank
+// runs, in grid order, and which peer messages it pulls / publishes.
+#include "exec/plan.hpp"
+extern "C" int pb_plan_device(const pb_schedule* s, int32_t device, pb_plan_op* out, size_t cap, size_t* n,
+                              int32_t* slots, int32_t* outboxes) {
+    return pbx::guard([&] {
+        if (!s) throw std::invalid_argument("null schedule");
+        pbx::ExecPlan p = pbx::make_plan(pbx::schedule_grid(s));
+        if (device < 1 || device > p.topo.devices) throw std::invalid_argument("device out of range");
+        const auto& ids = p.dev_ops[device];
+        if (n) *n = ids.size();
+        if (slots) *slots = p.slots[device];
+        if (outboxes) *outboxes = p.outboxes[device];
+        if (!out) return;
+        if (cap < ids.size()) throw pbx::Space("plan buffer too small");
+        for (size_t k = 0; k < ids.size(); ++k) {
+            const pbx::PlanOp& q = p.ops[ids[k]];
+            pb_plan_op r{};
+            r.stage = q.op.stage;
+            r.kind = int32_t(q.op.kind);
+            r.microbatch = q.op.mb;
+            r.start = q.op.start;
+            r.slot = q.slot;
+            if (q.in_msg >= 0) {
+                const pbx::Msg& m = p.msgs[q.in_msg];
+                r.recv_from = m.src_dev;
+                r.recv_outbox = m.outbox;
+                r.recv_gen = m.gen;
+            }
+            if (q.out_msg >= 0) {
+                const pbx::Msg& m = p.msgs[q.out_msg];
+                r.send_to = m.dst_dev;
+                r.send_outbox = m.outbox;
+                r.send_gen = m.gen;
+            }
+            out[k] = r;
+        }
+    });
+}
