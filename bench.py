@@ -351,8 +351,17 @@ def main():
     if g_ms > 0:
         achieved = g_fl / (g_ms / 1e3) / 1e12
         pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        traffic, tnote = None, None
+        tp = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_gemm_traffic.json")) \
+            if os.path.isdir(os.path.join(ROOT, "profiles")) else []
+        if tp:
+            with open(os.path.join(ROOT, "profiles", tp[-1])) as f:
+                tj = json.load(f)
+            traffic = tj["dram_bytes"]
+            tnote = (f"DRAM read+write bytes per launch of {tj['kernel']} from profiles/{tp[-1]}; "
+                     f"algorithmic bytes of that launch {tj['algorithmic_bytes']}")
         roof = {"bound": "tensor", "kernel": "gemm_kernel (tcgen05, csrc/kernels/gemm_tc.cu)", "achieved": achieved,
-                "peak": pk, "unit": "TFLOP/s", "frac": achieved / pk, "traffic": None,
+                "peak": pk, "unit": "TFLOP/s", "frac": achieved / pk, "traffic": traffic, "traffic_note": tnote,
                 "peak_kind": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
                 "gemm_share_of_device_time": g_ms / sum(g[3] for g in gall),
                 "launches": g_n, "flops_per_step": g_fl,

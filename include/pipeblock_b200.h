@@ -107,6 +107,10 @@ int pb_schedule_exact_peak(const pb_schedule* s, double* per_device);
 /* simulate (simulate.hpp:22-86). out: n passes (canonical order) or NULL; per-device arrays may be NULL. */
 int pb_simulate(const pb_schedule* s, const pb_profile* prof, pb_timed_pass* out, size_t n, pb_sim_stats* stats,
                 double* busy, double* idle_total, double* idle_span, double* peak);
+/* simulate() with one duration per pass (canonical order, n = pass count) and a
+ * per-crossing latency `comm`: replays measured pass times in grid order. */
+int pb_replay(const pb_schedule* s, const double* durations, size_t n, double comm, pb_timed_pass* out,
+              pb_sim_stats* stats, double* busy, double* idle_total, double* idle_span, double* peak);
 /* The same accounting over measured passes (bubble = 1 - sum busy / (d * makespan), simulate.hpp:81-82). */
 int pb_account(const pb_topology* topo, const pb_timed_pass* passes, size_t n, pb_sim_stats* stats, double* busy,
                double* peak);
@@ -199,6 +203,9 @@ typedef struct pb_model_cfg {
 #define PB_FLAG_TIMELINE 2   /* record per-pass CUDA events (TimedSchedule output) */
 #define PB_FLAG_GEMM_TIMING 4 /* CUDA events around every GEMM launch (roofline of the dominant kernel) */
 #define PB_FLAG_KERNEL_TIMING 8 /* CUDA events around every launch, per-kernel report (pb_exec_kernel_report) */
+#define PB_FLAG_ISOLATE 16   /* in-process group: one pass at a time over all devices (a group-wide GPU
+                                token taken after the pass's cross-device waits), each synchronised —
+                                clean stand-alone per-pass times for pb_replay */
 
 typedef struct pb_exec_stats {
     double loss;            /* mean CE over all tokens of the step (last-stage device; NaN elsewhere) */

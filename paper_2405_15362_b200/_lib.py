@@ -143,3 +143,5 @@ class pb_plan_op(C.Structure):
 
 
 EXPORTS += ["pb_plan_device"]
+
+EXPORTS += ["pb_replay"]

@@ -26,6 +26,7 @@ extern "C" int pb_exec_create(const pb_model_cfg* cfg, const pb_schedule* plan, 
         e->serial = (cfg->flags & PB_FLAG_SERIAL) != 0;
         e->gemm_timing = (cfg->flags & PB_FLAG_GEMM_TIMING) != 0;
         e->kernel_timing = (cfg->flags & PB_FLAG_KERNEL_TIMING) != 0;
+        e->isolate = (cfg->flags & PB_FLAG_ISOLATE) != 0;
         if (e->plan.topo.devices == 1) e->connect_local({e}, nullptr);
         *out = new pb_exec{e};
     });
@@ -87,6 +88,7 @@ extern "C" int pb_exec_set_flags(pb_exec* h, int32_t flags) {
         e.serial = (flags & PB_FLAG_SERIAL) != 0;
         e.gemm_timing = (flags & PB_FLAG_GEMM_TIMING) != 0;
         e.kernel_timing = (flags & PB_FLAG_KERNEL_TIMING) != 0;
+        e.isolate = (flags & PB_FLAG_ISOLATE) != 0;
     });
 }
 
@@ -116,11 +118,10 @@ extern "C" int pb_exec_param_get(pb_exec* h, int32_t i, int32_t which, float* ho
         const auto& t = e.ptensors[i];
         cudaSetDevice(e.cuda);
         cudaStreamSynchronize(e.cs);
-        if (which == 0) {
-            std::vector<__nv_bfloat16> tmp(t.numel);
-            if (cudaMemcpy(tmp.data(), e.wts + t.off, t.numel * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (which == 0) {  // the bf16 weight the model computes with (masters rounded; gamma-folded copies aside)
+            if (cudaMemcpy(host, e.master + t.off, t.numel * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
                 throw pbx::CudaError("param copy failed");
-            for (size_t k = 0; k < t.numel; ++k) host[k] = __bfloat162float(tmp[k]);
+            for (size_t k = 0; k < t.numel; ++k) host[k] = __bfloat162float(__float2bfloat16_rn(host[k]));
         } else {
             if (cudaMemcpy(host, (which == 1 ? e.grads : e.master) + t.off, t.numel * 4, cudaMemcpyDeviceToHost) !=
                 cudaSuccess)
@@ -139,6 +140,7 @@ extern "C" int pb_exec_param_set(pb_exec* h, int32_t i, const float* host) {
         if (cudaMemcpy(e.master + t.off, host, t.numel * 4, cudaMemcpyHostToDevice) != cudaSuccess)
             throw pbx::CudaError("param copy failed");
         pbk::f32_to_bf16(e.master + t.off, e.wts + t.off, (t.numel + 3) / 4 * 4, e.cs);
+        e.refold();
         cudaStreamSynchronize(e.cs);
     });
 }

@@ -169,6 +169,15 @@ extern "C" int pb_simulate(const pb_schedule* s, const pb_profile* prof, pb_time
     });
 }
 
+extern "C" int pb_replay(const pb_schedule* s, const double* durations, size_t n, double comm, pb_timed_pass* out,
+                         pb_sim_stats* st, double* busy, double* idle_t, double* idle_s, double* peak) {
+    return pbx::guard([&] {
+        if (!s || (n && !durations)) throw std::invalid_argument("null argument");
+        SimResult r = replay(s->grid, std::vector<double>(durations, durations + n), comm);
+        fill_stats(r, out, out ? n : 0, st, busy, idle_t, idle_s, peak);
+    });
+}
+
 extern "C" int pb_account(const pb_topology* topo, const pb_timed_pass* passes, size_t n, pb_sim_stats* st,
                           double* busy, double* peak) {
     return pbx::guard([&] {

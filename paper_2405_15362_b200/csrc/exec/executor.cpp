@@ -207,6 +207,27 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
     for (const auto& t : ptensors)
         pbk::init_normal(master + t.off, t.numel, cfg.seed * 1000003ull + uint64_t(t.id), t.std, t.constant, cs);
     pbk::f32_to_bf16(master, wts, n_params, cs);
+    fold = std::getenv("PB_NO_FOLD") == nullptr;
+    if (fold) {
+        size_t off = 0;
+        for (int s : stages) {
+            const StageParams& P = sparams.at(s);
+            for (const auto& lp : P.layers) {
+                folds.push_back({lp.wqkv, lp.g1, 3 * h, h, off});
+                off += align_up(size_t(3) * h * h, 64);
+                folds.push_back({lp.w1, lp.g2, 4 * h, h, off});
+                off += align_up(size_t(4) * h * h, 64);
+            }
+            if (s == S) {
+                folds.push_back({P.head, P.gf, V, h, off});
+                off += align_up(size_t(V) * h, 64);
+            }
+        }
+        for (size_t i = 0; i < folds.size(); ++i) fold_of[folds[i].w] = i;
+        gfold = static_cast<float*>(dmalloc(std::max<size_t>(off, 64) * 4, "folded grads"));
+        ck(cudaMemsetAsync(gfold, 0, std::max<size_t>(off, 64) * 4, cs), "memset");
+        refold();
+    }
 
     nslots = plan.slots[dev];
     pool = static_cast<uint8_t*>(dmalloc(slot_bytes * size_t(std::max(nslots, 1)), "activation pool"));
@@ -264,6 +285,26 @@ Exec::~Exec() {
     if (loss_host) cudaFreeHost(loss_host);
     cudaStreamDestroy(cs);
     cudaStreamDestroy(xs);
+}
+
+// ------------------------------------------------------------------ gamma folding
+float* Exec::GW(size_t p) const {
+    auto it = fold_of.find(p);
+    return it == fold_of.end() ? G(p) : gfold + folds[it->second].off;
+}
+
+void Exec::refold() {
+    for (const auto& f : folds)
+        pbk::fold_weight(master + ptensors[f.w].off, master + ptensors[f.g].off, wts + ptensors[f.w].off, f.rows,
+                         f.cols, cs);
+    launches += int64_t(folds.size());
+}
+
+void Exec::fold_grads() {
+    for (const auto& f : folds)
+        pbk::fold_grad(gfold + f.off, master + ptensors[f.w].off, master + ptensors[f.g].off, G(f.w), G(f.g), dq_acc,
+                       size_t(T) * h, f.rows, f.cols, cs);
+    launches += 2 * int64_t(folds.size());
 }
 
 // ------------------------------------------------------------------ passes
@@ -349,9 +390,9 @@ void Exec::build_w_groups() {
                 const auto& y = L.layer[l];
                 const auto& w = P.layers[l];
                 add(h, 4 * h, bf(slot, L.dx[l + 1]), bf(slot, y.gl), G(w.w2));
-                add(4 * h, h, bf(slot, y.u), bf(slot, y.b), G(w.w1));
+                add(4 * h, h, bf(slot, y.u), bf(slot, y.b), GW(w.w1));
                 add(h, h, bf(slot, y.dx1), bf(slot, y.o), G(w.wo));
-                add(3 * h, h, bf(slot, y.dqkv), bf(slot, y.a), G(w.wqkv));
+                add(3 * h, h, bf(slot, y.dqkv), bf(slot, y.a), GW(w.wqkv));
             }
             bool ok = true;
             for (const auto& g : v) ok = ok && pbk::gemm_group_ok(g);
@@ -394,18 +435,18 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         const auto& w = P.layers[l];
         __nv_bfloat16* x = bf(slot, L.x[l]);
         __nv_bfloat16* xo = (l == Lc - 1 && s < S) ? out : bf(slot, L.x[l + 1]);
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(x, W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs); });
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(x, fold ? nullptr : W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs); });
         gemm(T, 3 * h, h, bf(slot, y.a), false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE);
         timed("attn_fwd", [&] { pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs); });
         gemm(T, h, h, bf(slot, y.o), false, W(w.wo), false, bf(slot, y.x1), pbk::EPI_RESID, x);
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, y.x1), W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs); });
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, y.x1), fold ? nullptr : W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs); });
         gemm(T, 4 * h, h, bf(slot, y.b), false, W(w.w1), false, bf(slot, y.u), pbk::EPI_GELU, nullptr,
              bf(slot, y.gl));
         gemm(T, h, 4 * h, bf(slot, y.gl), false, W(w.w2), false, xo, pbk::EPI_RESID, bf(slot, y.x1));
         launches += 3;
     }
     if (s == S) {
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), W(P.gf), bf(slot, L.hf), f32(slot, L.rstdf), T, h, cs); });
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), bf(slot, L.hf), f32(slot, L.rstdf), T, h, cs); });
         gemm(T, V, h, bf(slot, L.hf), false, W(P.head), false, bf(slot, L.logits), pbk::EPI_STORE);
         timed("cross_entropy", [&] { pbk::cross_entropy(bf(slot, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
                            cs); });
@@ -420,10 +461,10 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
     if (s == S) {
         // dhf = dlogits . Whead ; dx_L = rmsnorm_bwd(dhf)
         gemm(T, h, V, bf(slot, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), W(P.gf), f32(slot, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), f32(slot, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
                          cs); });
-        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), f32(slot, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
-        launches += 2;
+        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), f32(slot, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
+        launches += fold ? 1 : 2;
     }
     for (int l = Lc - 1; l >= 0; --l) {
         const auto& y = L.layer[l];
@@ -433,15 +474,15 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         // du = (dy . W2) * gelu'(u), written over u
         gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u));
         gemm(T, h, 4 * h, bf(slot, y.u), false, W(w.w1), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs); });
-        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), dq_acc, T, h, cs); });
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), fold ? nullptr : W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs); });
+        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), dq_acc, T, h, cs); });
         gemm(T, h, h, bf(slot, y.dx1), false, W(w.wo), true, scratch, pbk::EPI_STORE);
         timed("attn_bwd", [&] { pbk::attn_bwd_tc(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
                       seq, H, cs); });
         gemm(T, h, 3 * h, bf(slot, y.dqkv), false, W(w.wqkv), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs); });
-        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), dq_acc, T, h, cs); });
-        launches += 8;
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), fold ? nullptr : W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs); });
+        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), dq_acc, T, h, cs); });
+        launches += fold ? 6 : 8;
     }
 }
 
@@ -456,12 +497,12 @@ void Exec::pass_weight(int s, int mb, int slot) {
         const auto& y = L.layer[l];
         const auto& w = P.layers[l];
         gemm(h, 4 * h, T, bf(slot, L.dx[l + 1]), true, bf(slot, y.gl), true, G(w.w2), pbk::EPI_F32, nullptr, nullptr, 1);
-        gemm(4 * h, h, T, bf(slot, y.u), true, bf(slot, y.b), true, G(w.w1), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(4 * h, h, T, bf(slot, y.u), true, bf(slot, y.b), true, GW(w.w1), pbk::EPI_F32, nullptr, nullptr, 1);
         gemm(h, h, T, bf(slot, y.dx1), true, bf(slot, y.o), true, G(w.wo), pbk::EPI_F32, nullptr, nullptr, 1);
-        gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, y.a), true, G(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, y.a), true, GW(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
     }
     if (s == S)
-        gemm(V, h, T, bf(slot, L.logits), true, bf(slot, L.hf), true, G(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(V, h, T, bf(slot, L.logits), true, bf(slot, L.hf), true, GW(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
     if (s == 1) {
         timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, cs); });
         ++launches;
@@ -489,6 +530,8 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
             return true;
         });
     }
+    // concurrent passes of devices sharing this GPU: whole-tile GEMMs only (no stream-K spin waits)
+    pbk::gemm_allow_stream_k(isolate || !shares_gpu);
     launches = 0;
     peer_bytes = 0;
     gev_used = 0;
@@ -520,6 +563,8 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
         if (trace)
             std::fprintf(stderr, "[dev %d] op %zu %s(s%d,mb%d)@%lld slot %d in %d out %d\n", dev, j,
                          vsched::kind_name(o.kind), o.stage, o.mb, (long long)o.start, po.slot, po.in_msg, po.out_msg);
+        const bool iso = isolate && group;
+        std::unique_lock<std::mutex> gpu_token(group ? group->iso_mu : local_iso_mu, std::defer_lock);
         // ---- incoming boundary tensor
         __nv_bfloat16* in_dst = nullptr;
         const Msg* in = po.in_msg >= 0 ? &plan.msgs[po.in_msg] : nullptr;
@@ -562,6 +607,9 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
                 wait_value(cs, ack_flag(flags, out->outbox), gen_total(*out) - 1);
             }
         }
+        // isolate: every cross-device wait above is host-side, so taking the group's GPU token
+        // only now keeps the schedule deadlock-free while passes run one at a time
+        if (iso) gpu_token.lock();
         if (timeline) ck(cudaEventRecord(ev_start[j], cs), "event");
         if (in && in->local())
             ck(cudaMemcpyAsync(in_dst, outbox_ptr(in->outbox), size_t(T) * h * 2, cudaMemcpyDeviceToDevice, cs),
@@ -594,11 +642,23 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
             --live;
             ck(cudaEventRecord(ev_free[j], cs), "event");
         }
-        if (serial) {
+        if (serial || iso) {
             ck(cudaStreamSynchronize(xs), "serial");
             ck(cudaStreamSynchronize(cs), "serial");
         }
+        if (iso) {
+            gpu_token.unlock();
+            {
+                std::lock_guard<std::mutex> lk(group->mu);
+                if (group->iso_step != t) group->iso_step = t, group->iso_done = 0;
+                ++group->iso_done;
+            }
+            group->cv.notify_all();
+        }
     }
+    if (isolate && group)  // keep the optimizer off the isolated pass window
+        group->wait([&] { return group->iso_step == t && group->iso_done == int64_t(plan.ops.size()); });
+    if (fold) timed("fold_grad", [&] { fold_grads(); });
     if (cfg.optimizer) {
         ++adam_step;
         timed("adamw", [&] {
@@ -606,6 +666,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
                        cfg.weight_decay, adam_step, cs);
         });
         ++launches;
+        if (fold) timed("fold_weight", [&] { refold(); });
     }
     if (has_last) ck(cudaMemcpyAsync(loss_host, loss_dev, 4, cudaMemcpyDeviceToHost, cs), "loss");
     ck(cudaEventRecord(ev_step1, cs), "event");
@@ -713,6 +774,8 @@ std::shared_ptr<LocalGroup> make_group(const std::vector<Exec*>& all) {
 void Exec::connect_local(const std::vector<Exec*>& all, std::shared_ptr<LocalGroup> grp) {
     if (int(all.size()) != plan.topo.devices) throw std::invalid_argument("connect: need one exec per device");
     group = std::move(grp);
+    for (Exec* e : all)
+        if (e != this && e->cuda == cuda) shares_gpu = true;
     for (Exec* e : all) {
         if (e->plan.ops.size() != plan.ops.size()) throw std::invalid_argument("connect: executors run different plans");
         peers[e->dev] = Peer{e->outbox, e->flags, false};

@@ -39,6 +39,14 @@ struct PTensor {
     int id;
     float std, constant;
 };
+// RMSNorm gamma folded into the projection that consumes the normalised rows:
+// the GEMM operand is bf16(W diag g), its gradient dW' accumulates in `gfold`, and
+// dW / dg are recovered once per step (executor.cpp fold_grads).
+struct FoldPair {
+    size_t w, g;  // ptensor indices
+    int rows, cols;
+    size_t off;   // into gfold
+};
 struct Peer {
     void* outbox = nullptr;
     uint32_t* flags = nullptr;
@@ -54,6 +62,9 @@ struct LocalGroup {
     std::vector<cudaEvent_t> ready_ev[2], ack_ev[2];  // per message
     std::vector<int64_t> ready_step, ack_step;        // last step whose record is enqueued
     std::vector<int64_t> enqueued;                    // per device: steps fully enqueued
+    // PB_FLAG_ISOLATE: one pass at a time on the whole group (GPU token), passes done this step
+    std::mutex iso_mu;
+    int64_t iso_step = -1, iso_done = 0;
     void wait(const std::function<bool()>& pred) {
         std::unique_lock<std::mutex> lk(mu);
         cv.wait(lk, pred);
@@ -88,7 +99,8 @@ class Exec {
     __nv_bfloat16* wts = nullptr;
     size_t n_params = 0;
     cudaStream_t cs = nullptr, xs = nullptr;
-    bool timeline = true, serial = false, connected = false, pending = false, gemm_timing = false, kernel_timing = false;
+    bool shares_gpu = false;  // another pipeline device of the group runs on the same GPU
+    bool timeline = true, serial = false, isolate = false, connected = false, pending = false, gemm_timing = false, kernel_timing = false;
     int adam_step = 0;
 
     int64_t steps_done = 0;
@@ -112,6 +124,15 @@ class Exec {
     uint32_t* ready_flag(uint32_t* base, int src, int k) const;
 
     void build_w_groups();
+    float* GW(size_t p) const;  // where the W pass accumulates tensor p's gradient (dW' if folded)
+    void fold_grads();
+  public:
+    void refold();  // wts of folded pairs <- bf16(W diag g) from the masters
+  private:
+    bool fold = true;
+    std::vector<FoldPair> folds;
+    std::map<size_t, size_t> fold_of;  // ptensor index of W -> folds index
+    float* gfold = nullptr;
     void run_gemm_timed(const char* label, double flops, const std::function<void()>& fn);
     std::map<std::pair<int, int>, pbk::GemmGroup> wgroups;  // (stage, slot) -> grouped W GEMMs
     std::map<std::pair<int, int>, double> wgroup_flops;
@@ -131,6 +152,7 @@ class Exec {
     std::vector<Peer> peers;
     std::vector<int> pos_of;
     std::shared_ptr<LocalGroup> group;
+    std::mutex local_iso_mu;
     int64_t launches = 0, peer_bytes = 0;
     std::vector<cudaEvent_t> gev;
     size_t gev_used = 0;

@@ -8,10 +8,12 @@
 //   warps 2-5  softmax: thread = query row = TMEM lane; reads its S row with
 //              tcgen05.ld, online softmax in registers (no shuffles), writes P
 //              (bf16, 128B-swizzled K-major) to smem for the PV MMA.
-// S_{j+1} is computed while the softmax of S_j runs (two S buffers).  The
+// S_{j+1} is computed while the softmax of S_j runs (two S buffers), and P is
+// double-buffered in smem so the softmax of tile j overlaps PV_{j-1}.  The
 // running max is rescaled lazily: O (in TMEM) is only rescaled when a row's
 // max grows by more than 2^8, which keeps the result exact (O and the row sum
 // share the same stale max) and avoids a TMEM round trip per tile.
+#include <cstdlib>
 #include <stdexcept>
 
 #include "ops.hpp"
@@ -32,8 +34,8 @@ struct FwdSmem {
     static constexpr int q = 0;
     static constexpr int k0 = kTile;
     static constexpr int v0 = k0 + kStages * kTile;
-    static constexpr int p = v0 + kStages * kTile;
-    static constexpr int bars = p + kTile;
+    static constexpr int p = v0 + kStages * kTile;  // [2] P buffers
+    static constexpr int bars = p + 2 * kTile;
     static constexpr int total = bars + 256 + 1024;
 };
 
@@ -67,10 +69,10 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* kv_empty = bars + 3;  // [2]
     uint64_t* s_full = bars + 5;    // [2]
     uint64_t* s_free = bars + 7;    // [2]
-    uint64_t* p_full = bars + 9;
-    uint64_t* p_empty = bars + 10;
-    uint64_t* o_full = bars + 11;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* p_full = bars + 9;    // [2]
+    uint64_t* p_empty = bars + 11;  // [2]
+    uint64_t* o_full = bars + 13;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
     const uint32_t warp = warp_id();
     const int nqb = seq / BQ;
@@ -90,8 +92,10 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(&s_full[i], 1);
             mbar_init(&s_free[i], 4);
         }
-        mbar_init(p_full, 4);
-        mbar_init(p_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&p_full[i], 4);
+            mbar_init(&p_empty[i], 1);
+        }
         mbar_init(o_full, 1);
         fence_barrier_init();
     }
@@ -129,18 +133,20 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t sp = smem_u32(sm + FwdSmem::p);
         mbar_wait(q_full, 0);
         auto issue_pv = [&](int j) {  // O += P_j V_j
-            mbar_wait(p_full, j & 1);
+            const int pb = j & 1;
+            mbar_wait(&p_full[pb], (j >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t sv = smem_u32(sm + FwdSmem::v0 + (j & 1) * kTile);
+                const uint32_t spj = sp + pb * kTile;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = sdesc(sp + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t ad = sdesc(spj + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
                     const uint64_t bd = sdesc(sv + kk * 2048, 16384, 1024);
                     tc_mma(tmem + 256, ad, bd, idesc_o, (j | kk) != 0);
                 }
                 tc_commit(&kv_empty[j & 1]);
-                tc_commit(p_empty);
+                tc_commit(&p_empty[pb]);
             }
             __syncwarp();
         };
@@ -172,8 +178,8 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t lane_base = (q4 * 32) << 16;
         const float sl2 = scale * kLog2e;
         float m_used = -INFINITY, l = 0.f;
-        uint8_t* sp = sm + FwdSmem::p;
         for (int j = 0; j < nkv; ++j) {
+            uint8_t* sp = sm + FwdSmem::p + (j & 1) * kTile;
             const int st = j & 1;
             mbar_wait(&s_full[st], (j >> 1) & 1);
             tc_fence_after();
@@ -195,11 +201,16 @@ __global__ void __launch_bounds__(192, 1)
             }
             const float m_new = fmaxf(m_used, mx);
             bool rescale = (j > 0) && (m_new > m_used + 8.f);
-            if (j > 0) {
-                mbar_wait(p_empty, (j - 1) & 1);  // PV_{j-1} done: P smem free, O stable
+            const bool any_rescale = __any_sync(0xffffffff, rescale);
+            if (any_rescale) {  // O must be stable: PV_{j-1} done
+                mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
             }
-            if (__any_sync(0xffffffff, rescale)) {
+            if (j >= 2) {  // P buffer j&1 free: PV_{j-2} done
+                mbar_wait(&p_empty[j & 1], ((j - 2) >> 1) & 1);
+                tc_fence_after();
+            }
+            if (any_rescale) {
                 const float f = rescale ? exp2f(m_used - m_new) : 1.f;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(192, 1)
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane_id() == 0) mbar_arrive(p_full);
+            if (lane_id() == 0) mbar_arrive(&p_full[j & 1]);
         }
         // epilogue: O / l -> bf16
         mbar_wait(o_full, 0);
@@ -516,6 +527,267 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
+
+// ------------------------------------------------------------------ backward v3
+// Same decomposition as attn_bwd_tc_kernel (CTA per key tile, loop over query tiles), with
+//   * P^T kept in TMEM (bf16 pairs written over the consumed S^T columns) and fed to the
+//     dV MMA as the A operand straight from TMEM, which frees 32 KB of smem for
+//   * double-buffered Q / dO tiles: the TMA of tile i+1 overlaps tile i,
+//   * dQ drained from TMEM with red.global.add.v4.f32 (no fp32 smem staging).
+struct Bwd3Smem {
+    static constexpr int k = 0;
+    static constexpr int v = k + kTile;
+    static constexpr int q = v + kTile;       // [2]
+    static constexpr int dO = q + 2 * kTile;  // [2]
+    static constexpr int dst = dO + 2 * kTile;
+    static constexpr int lse = dst + kTile;   // [2][256] floats: lse2 | D
+    static constexpr int bars = lse + 2048;
+    static constexpr int total = bars + 256 + 1024;
+};
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                        float* __restrict__ dq_acc, const float* __restrict__ lse2, const float* __restrict__ dsum,
+                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd3Smem::bars);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* qdo_full = bars + 1;   // [2]
+    uint64_t* qdo_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;
+    uint64_t* ds_full = bars + 6;    // 8 compute warps
+    uint64_t* dq_full = bars + 7;
+    uint64_t* s_free = bars + 8;     // 8 compute warps
+    uint64_t* dkv_full = bars + 9;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    float* sL = reinterpret_cast<float*>(sm + Bwd3Smem::lse);
+
+    const uint32_t warp = warp_id();
+    const int nqb = seq / BQ;
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int kb = int(blockIdx.x) / (H * (T / seq));
+    const int head = hb % H, b = hb / H;
+    const int tok0 = b * seq;
+    const int nq = nqb - kb;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm_qkv);
+        tma_prefetch(&tm_do);
+        for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 8 : 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;  // [0,128) S^T -> P^T (bf16, cols 0-63) -> dQ ; [128,256) dP^T ; dV ; dK
+    pdl_wait();
+    pdl_launch();
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const int ck = H * D + head * D, cv = 2 * H * D + head * D, cq = head * D;
+            const int kr = tok0 + kb * BK;
+            mbar_expect_tx(kv_full, 2 * kTile);
+            tma_load_2d(sm + Bwd3Smem::k, &tm_qkv, kv_full, ck, kr);
+            tma_load_2d(sm + Bwd3Smem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
+            tma_load_2d(sm + Bwd3Smem::v, &tm_qkv, kv_full, cv, kr);
+            tma_load_2d(sm + Bwd3Smem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i & 1;
+                if (i >= 2) mbar_wait(&qdo_empty[st], ((i - 2) >> 1) & 1);
+                const int qr = tok0 + (kb + i) * BQ;
+                uint8_t* qs = sm + Bwd3Smem::q + st * kTile;
+                uint8_t* ds = sm + Bwd3Smem::dO + st * kTile;
+                mbar_expect_tx(&qdo_full[st], 2 * kTile);
+                tma_load_2d(qs, &tm_qkv, &qdo_full[st], cq, qr);
+                tma_load_2d(qs + 16384, &tm_qkv, &qdo_full[st], cq + 64, qr);
+                tma_load_2d(ds, &tm_do, &qdo_full[st], head * D, qr);
+                tma_load_2d(ds + 16384, &tm_do, &qdo_full[st], head * D + 64, qr);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
+        constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
+        const uint32_t sk = smem_u32(sm + Bwd3Smem::k), sv = smem_u32(sm + Bwd3Smem::v);
+        const uint32_t sdst = smem_u32(sm + Bwd3Smem::dst);
+        mbar_wait(kv_full, 0);
+        for (int i = 0; i < nq; ++i) {
+            const int st = i & 1;
+            const uint32_t sq = smem_u32(sm + Bwd3Smem::q + st * kTile);
+            const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + st * kTile);
+            mbar_wait(&qdo_full[st], (i >> 1) & 1);
+            if (i > 0) mbar_wait(s_free, (i - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
+                }
+                tc_commit(s_full);
+            }
+            __syncwarp();
+            mbar_wait(ds_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step)
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 256, tmem + kk * 8, sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
+                // dK += dS^T Q
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
+                           (i | kk) != 0);
+                }
+                tc_commit(&qdo_empty[st]);  // Q, dO of this tile consumed
+                // dQ = dS K -> TMEM [0,128) (after the dV MMA has read P^T there: in-order pipe)
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma(tmem + 0, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
+                           id_mnmn, kk != 0);
+                tc_commit(dq_full);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) tc_commit(dkv_full);
+        __syncwarp();
+    } else {
+        const uint32_t q4 = warp & 3;
+        const int hf = int(warp - 2) >> 2;  // query half (columns of S^T) handled by this warp
+        const int r = int(q4 * 32 + lane_id());
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const float sl2 = scale * kLog2e;
+        uint8_t* sdst = sm + Bwd3Smem::dst;
+        const int key = kb * BK + r;
+        for (int i = 0; i < nq; ++i) {
+            const int qb = kb + i;
+            float* Lb = sL + (i & 1) * 256;
+            Lb[hf * 128 + r] = hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r]
+                                       : dsum[size_t(head) * T + tok0 + qb * BQ + r];
+            bar_sync_compute();  // lse / D of this tile staged
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            const bool diag = (qb == kb);
+            float sv[64], dp[64];
+            tmem_ld32(tmem + lane_base + hf * 64, *reinterpret_cast<float(*)[32]>(&sv[0]));
+            tmem_ld32(tmem + lane_base + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
+            tmem_ld32(tmem + lane_base + 128 + hf * 64, *reinterpret_cast<float(*)[32]>(&dp[0]));
+            tmem_ld32(tmem + lane_base + 128 + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&dp[32]));
+            tmem_ld_wait();
+            // every S^T column read before P^T is written over columns [0,64)
+            tc_fence_before();
+            bar_sync_compute();
+            tc_fence_after();
+            uint32_t pk[32];
+#pragma unroll
+            for (int e2 = 0; e2 < 32; ++e2) {
+                float pv[2], dsv[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int e = 2 * e2 + u;
+                    const int ql = hf * 64 + e;
+                    float v = exp2f(sv[e] * sl2 - Lb[ql]);
+                    if (diag && key > qb * BQ + ql) v = 0.f;
+                    pv[u] = v;
+                    dsv[u] = v * (dp[e] - Lb[128 + ql]);
+                }
+                pk[e2] = pack_bf16(pv[0], pv[1]);
+                dp[2 * e2] = dsv[0];
+                dp[2 * e2 + 1] = dsv[1];
+            }
+            tmem_st32u(tmem + lane_base + hf * 32, pk);
+#pragma unroll
+            for (int e8 = 0; e8 < 8; ++e8) {
+                const int col = hf * 64 + e8 * 8;
+                *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
+                    make_uint4(pack_bf16(dp[e8 * 8], dp[e8 * 8 + 1]), pack_bf16(dp[e8 * 8 + 2], dp[e8 * 8 + 3]),
+                               pack_bf16(dp[e8 * 8 + 4], dp[e8 * 8 + 5]), pack_bf16(dp[e8 * 8 + 6], dp[e8 * 8 + 7]));
+            }
+            tmem_st_wait();
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(ds_full);
+            // dQ tile (thread = query row r, column half hf) -> fp32 atomics into dq_acc
+            mbar_wait(dq_full, i & 1);
+            tc_fence_after();
+            float* dqrow = dq_acc + size_t(tok0 + qb * BQ + r) * (H * D) + head * D;
+#pragma unroll 1
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c = hf * 2 + cc;
+                float v[32];
+                tmem_ld32(tmem + lane_base + c * 32, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c * 32 + 4 * j),
+                                 "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                                 : "memory");
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(s_free);  // TMEM [0,256) free for the next S^T / dP^T
+        }
+        // dV, dK rows (thread = key row, column half hf)
+        mbar_wait(dkv_full, 0);
+        tc_fence_after();
+        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = hf * 2 + cc;
+            float v[32], k[32];
+            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
+            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
+            tmem_ld_wait();
+            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
+            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                dv[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
+                                   pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
+                dk[e] = make_uint4(pack_bf16(k[8 * e] * scale, k[8 * e + 1] * scale),
+                                   pack_bf16(k[8 * e + 2] * scale, k[8 * e + 3] * scale),
+                                   pack_bf16(k[8 * e + 4] * scale, k[8 * e + 5] * scale),
+                                   pack_bf16(k[8 * e + 6] * scale, k[8 * e + 7] * scale));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<512>(tmem);
+    }
+}
+
 }  // namespace
 
 void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
@@ -524,6 +796,7 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     attn_bwd_pre(dout, out, dsum, dq_acc, heads, batch * seq, s);
     static bool once = [] {
         cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::total);
+        cudaFuncSetAttribute(attn_bwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd3Smem::total);
         return true;
     }();
     (void)once;
@@ -533,8 +806,16 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
                                        uint64_t(heads) * D, 32, 128);
     dim3 grid(seq / BK * heads * batch);
-    launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
-             static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
+    static const bool v2 = [] {
+        const char* e = std::getenv("PB_ATTN_BWD");
+        return e && e[0] == '2';
+    }();
+    if (v2)
+        launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
+                 static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
+    else
+        launch_k(attn_bwd_tc3_kernel, grid, dim3(kBwdThreads), Bwd3Smem::total, s, 1, tq, td, dq_acc, lse2,
+                 static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
     attn_dq_store(dq_acc, dqkv, heads, T, s);
 }
 

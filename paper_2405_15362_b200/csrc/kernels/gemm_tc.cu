@@ -17,6 +17,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <vector>
 #include <stdexcept>
 #include <string>
@@ -58,6 +60,13 @@ struct KParams {
     int accumulate;
     const GroupProblem* group;  // grouped launch: tiles come from this table
     int ngroup, total_tiles;
+    // stream-K (non-grouped launches): pair c owns k-block units [c*U/P, (c+1)*U/P) of the
+    // tile-major (tile, k-block) space; partial tiles meet in `sk_ws` (one 128 x BN fp32
+    // slot per CTA, written by the pair's first segment) under per-CTA epoch flags
+    float* sk_ws;
+    uint32_t* sk_flag;
+    uint32_t sk_epoch;
+    int sk;
 };
 
 // Resolves tile t of the launch: its problem's descriptors, origin, K blocks, output.
@@ -79,6 +88,42 @@ __device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensor
     const int lt = t - g.tile0;
     return TileRef{&g.ta, &g.tb, g.C, lt % g.num_m, lt / g.num_m, g.K / BK, g.ldc};
 }
+
+// Work of one CTA (pair) as segments (tile, k-blocks [kb0, kb1)): whole tiles
+// round-robin, or a contiguous stream-K range of (tile, k-block) units.
+struct SegIter {
+    long long u, u1;  // stream-K
+    int nk;
+    int t, step, num_tiles;  // whole tiles
+    bool sk;
+    __device__ SegIter(const KParams& p, int num_tiles_, int cid, int ncl) {
+        sk = p.sk != 0;
+        num_tiles = num_tiles_;
+        t = cid;
+        step = ncl;
+        nk = p.K / BK;
+        const long long U = (long long)num_tiles * nk;
+        u = U * cid / ncl;
+        u1 = U * (cid + 1) / ncl;
+    }
+    __device__ bool next(int& tile, int& kb0, int& kb1) {
+        if (!sk) {
+            if (t >= num_tiles) return false;
+            tile = t;
+            kb0 = 0;
+            kb1 = -1;  // whole tile (resolved per problem)
+            t += step;
+            return true;
+        }
+        if (u >= u1) return false;
+        tile = int(u / nk);
+        const long long end = u1 < (long long)(tile + 1) * nk ? u1 : (long long)(tile + 1) * nk;
+        kb0 = int(u - (long long)tile * nk);
+        kb1 = int(end - (long long)tile * nk);
+        u = end;
+        return true;
+    }
+};
 
 // CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) per
 // 256 x BN tile; each CTA stages its 128 rows of A and BN/2 rows of B, the
@@ -131,13 +176,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int cursor = 0;
-            for (int t = cid; t < num_tiles; t += ncl) {
+            SegIter it(p, num_tiles, cid, ncl);
+            int t, kb0, kb1;
+            while (it.next(t, kb0, kb1)) {
                 const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
                 const CUtensorMap* pa = tr.ta;
                 const CUtensorMap* pb = tr.tb;
-                const int num_k = tr.num_k;
+                const int num_k = kb1 < 0 ? tr.num_k : kb1;
                 const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN + int(rank) * C_::kBRows;
-                for (int kb = 0; kb < num_k; ++kb) {
+                for (int kb = kb0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * C_::kStageBytes;
                     uint8_t* sb = sa + C_::kABytes;
@@ -190,12 +237,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             int cursor = 0;
-            for (int t = cid; t < num_tiles; t += ncl) {
-                const int num_k = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor).num_k;
+            SegIter it(p, num_tiles, cid, ncl);
+            int t, kb0, kb1;
+            while (it.next(t, kb0, kb1)) {
+                const int num_k = kb1 < 0 ? resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor).num_k : kb1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < num_k; ++kb) {
+                for (int kb = kb0; kb < num_k; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (elect_one()) {
@@ -205,10 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int k = 0; k < BK / 16; ++k) {
                             const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
                             const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
+                            const bool accum = kb != kb0 || k != 0;
                             if constexpr (CG == 1)
-                                tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                                tc_mma(d_tmem, ad, bd, idesc, accum);
                             else
-                                tc_mma2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                                tc_mma2(d_tmem, ad, bd, idesc, accum);
                         }
                         if constexpr (CG == 1) {
                             tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
@@ -231,7 +281,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int cursor = 0;
-        for (int t = cid; t < num_tiles; t += ncl) {
+        SegIter it(p, num_tiles, cid, ncl);
+        int t, kb0, kb1;
+        const int nk = p.K / BK;
+        const long long U = (long long)num_tiles * nk;
+        while (it.next(t, kb0, kb1)) {
             const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
             const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN;
             void* const Cout = tr.C;
@@ -240,11 +294,62 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int row = m0 + row_in_tile;
             const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
+            if (kb1 >= 0 && kb0 > 0) {
+                // stream-K contributor (this pair's first segment): park the partial tile, publish
+                float* slot = p.sk_ws + (size_t(cid) * CG + rank) * (BM * BN) + size_t(row_in_tile) * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    float v[32];
+                    tmem_ld32(tbase + c, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        __stcg(reinterpret_cast<float4*>(slot + c) + j,
+                               make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane_id() == 0) {
+                    if constexpr (CG == 1)
+                        mbar_arrive(&tempty[acc]);
+                    else
+                        mbar_arrive_cluster(map_peer(smem_u32(&tempty[acc]), 0));
+                }
+                __threadfence();
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
+                if (warp == 2 && lane_id() == 0)
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flag + size_t(cid) * CG + rank),
+                                 "r"(p.sk_epoch)
+                                 : "memory");
+                if (++acc == 2) acc = 0, acc_phase ^= 1;
+                continue;
+            }
+            // stream-K owner of a split tile: pairs cid+1 .. whose ranges start inside this tile contributed
+            int c_last = cid;
+            if (kb1 >= 0 && kb1 < nk) {
+                while (c_last + 1 < ncl && U * (c_last + 1) / ncl < (long long)(t + 1) * nk) ++c_last;
+                for (int c = cid + 1; c <= c_last; ++c) {
+                    const uint32_t* f = p.sk_flag + size_t(c) * CG + rank;
+                    uint32_t e;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(f) : "memory");
+                    } while (e != p.sk_epoch);
+                }
+            }
 #pragma unroll 1
             for (int c = 0; c < BN; c += 32) {
                 float v[32];
                 tmem_ld32(tbase + c, v);
                 tmem_ld_wait();
+                for (int cc = cid + 1; cc <= c_last; ++cc) {
+                    const float4* src = reinterpret_cast<const float4*>(
+                        p.sk_ws + (size_t(cc) * CG + rank) * (BM * BN) + size_t(row_in_tile) * BN + c);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 a = __ldcg(src + j);
+                        v[4 * j] += a.x, v[4 * j + 1] += a.y, v[4 * j + 2] += a.z, v[4 * j + 3] += a.w;
+                    }
+                }
                 const int col = n0 + c;
                 if constexpr (EPI == EPI_F32) {
                     float* dst = reinterpret_cast<float*>(Cout) + size_t(row) * ldc + col;
@@ -367,6 +472,43 @@ int sm_count() {
     return n;
 }
 
+// Stream-K scratch, one per (device, stream): GEMMs on one stream are ordered, so a
+// launch's partial tiles and epoch flags are never shared with a concurrent launch.
+struct SkWorkspace {
+    float* ws = nullptr;
+    uint32_t* flags = nullptr;
+    uint32_t epoch = 0;
+};
+SkWorkspace& sk_workspace(cudaStream_t s) {
+    // one 128 x 256 fp32 partial tile per CTA of a full-GPU launch (the largest BN)
+    const size_t floats = size_t(sm_count()) * BM * 256;
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, SkWorkspace> all;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    SkWorkspace& w = all[{dev, s}];
+    if (!w.ws) {
+        if (cudaMalloc(&w.ws, floats * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&w.flags, 1024 * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMemset(w.flags, 0, 1024 * sizeof(uint32_t)) != cudaSuccess)
+            throw std::runtime_error("gemm: stream-K workspace allocation failed");
+    }
+    return w;
+}
+// Stream-K owners spin on their contributors, which is safe only while every CTA of the launch
+// can be resident: launches from OTHER streams on the same GPU could hold the SMs a contributor
+// needs while their own owners spin.  Callers that share a GPU across concurrently running
+// streams turn it off for their thread (gemm_allow_stream_k).
+thread_local bool t_sk_allowed = true;
+bool sk_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PB_STREAMK");
+        return !(e && e[0] == '0');
+    }();
+    return on && t_sk_allowed;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 void launch(const GemmArgs& g, cudaStream_t s) {
     using C_ = Cfg<BN, CG>;
@@ -379,10 +521,23 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     (void)attr;
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
-    KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0};
+    KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
+               nullptr, nullptr, 0, 0};
     const int tiles = (g.M / (BM * CG)) * (g.N / BN);
     const int slots = sm_count() / CG;
-    const int grid = (tiles < slots ? tiles : slots) * CG;
+    int grid = (tiles < slots ? tiles : slots) * CG;
+    // stream-K when whole tiles would leave a ragged last wave (and a k split is possible)
+    // (>= 2 k-blocks of work per pair, so no pair's range is empty: an owner waits on every pair
+    // whose range starts inside its tile)
+    if (sk_enabled() && tiles % slots != 0 && tiles < 8 * slots && g.K / BK >= 4 &&
+        (long long)tiles * (g.K / BK) >= 2LL * slots) {
+        SkWorkspace& w = sk_workspace(s);
+        kp.sk = 1;
+        kp.sk_ws = w.ws;
+        kp.sk_flag = w.flags;
+        kp.sk_epoch = ++w.epoch;
+        grid = slots * CG;
+    }
     launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, CG, ta, tb, kp);
 }
 
@@ -473,7 +628,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     }();
     (void)attr;
     KParams kp{0, 0, 0, nullptr, nullptr, nullptr, 0, 0, g.accumulate,
-               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles};
+               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, nullptr, 0, 0};
     const int slots = sm_count() / 2;
     const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
     CUtensorMap dummy{};
@@ -485,6 +640,8 @@ void gemm_group_destroy(GemmGroup& g) {
     g.table = nullptr;
     g.n = 0;
 }
+
+void gemm_allow_stream_k(bool on) { t_sk_allowed = on; }
 
 static int g_force_cg = -1;  // tests: -1 auto, 1 or 2 forced
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }

@@ -42,16 +42,16 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return t;
 }
 
-// y = x * rsqrt(mean(x^2) + eps) * g ; one CTA per row, one 16-byte chunk per thread held in registers
+// y = x * rsqrt(mean(x^2) + eps) * g (g null: 1) ; one CTA per row, one 16-byte chunk per thread held in registers
 __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                                    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h, float eps) {
     pdl_wait();
     pdl_launch();
     __shared__ float red[32];
     const int row = blockIdx.x, c = threadIdx.x;
-    float f[8], w[8];
+    float f[8], w[8] = {1, 1, 1, 1, 1, 1, 1, 1};
     unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], f);
-    unpack8(reinterpret_cast<const uint4*>(g)[c], w);
+    if (g) unpack8(reinterpret_cast<const uint4*>(g)[c], w);
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
@@ -72,10 +72,10 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const _
     pdl_launch();
     __shared__ float red[32];
     const int row = blockIdx.x, c = threadIdx.x;
-    float a[8], b[8], w[8], o[8];
+    float a[8], b[8], w[8] = {1, 1, 1, 1, 1, 1, 1, 1}, o[8];
     unpack8(reinterpret_cast<const uint4*>(dy + size_t(row) * h)[c], a);
     unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], b);
-    unpack8(reinterpret_cast<const uint4*>(g)[c], w);
+    if (g) unpack8(reinterpret_cast<const uint4*>(g)[c], w);
     if (dres) {
         unpack8(reinterpret_cast<const uint4*>(dres + size_t(row) * h)[c], o);
     } else {
@@ -278,6 +278,47 @@ __global__ void adamw_kernel(float* __restrict__ w, __nv_bfloat16* __restrict__ 
     }
 }
 
+// RMSNorm gamma folded into the following projection (Y = (x^ * g) W^T = x^ (W diag g)^T):
+// Wb[i][j] = bf16(W[i][j] * g[j]) for a row-major [rows][cols] weight.
+__global__ void fold_weight_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                                   __nv_bfloat16* __restrict__ wb, size_t n, int cols) {
+    pdl_wait();
+    pdl_launch();
+    size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    const size_t stride = size_t(gridDim.x) * blockDim.x * 4;
+    for (; i < n; i += stride) {
+        const float4 a = *reinterpret_cast<const float4*>(w + i);
+        const float4 b = *reinterpret_cast<const float4*>(g + (i % size_t(cols)));
+        *reinterpret_cast<uint2*>(wb + i) = make_uint2(pack_bf16(a.x * b.x, a.y * b.y), pack_bf16(a.z * b.z, a.w * b.w));
+    }
+}
+
+// Gradients of a folded pair from dW' (the accumulated gradient w.r.t. W diag g), once per step:
+//   dW += dW' * g[j],  dg[j] += sum_i dW'[i][j] * W[i][j],  dW' <- 0.
+// Stage 1: thread = 4 columns x `rows_per_block` rows -> partial[row_block][cols] (deterministic).
+__global__ void fold_grad_partial_kernel(float* __restrict__ dwp, const float* __restrict__ w,
+                                         const float* __restrict__ g, float* __restrict__ dw,
+                                         float* __restrict__ partial, int rows, int cols, int rows_per_block) {
+    pdl_wait();
+    pdl_launch();
+    const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c4 * 4 >= cols) return;
+    const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+    const float4 gg = reinterpret_cast<const float4*>(g)[c4];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = r0; r < r1; ++r) {
+        const size_t o = size_t(r) * cols + size_t(c4) * 4;
+        float4 d = *reinterpret_cast<float4*>(dwp + o);
+        const float4 a = *reinterpret_cast<const float4*>(w + o);
+        float4 t = *reinterpret_cast<float4*>(dw + o);
+        acc.x += d.x * a.x, acc.y += d.y * a.y, acc.z += d.z * a.z, acc.w += d.w * a.w;
+        t.x += d.x * gg.x, t.y += d.y * gg.y, t.z += d.z * gg.z, t.w += d.w * gg.w;
+        *reinterpret_cast<float4*>(dw + o) = t;
+        *reinterpret_cast<float4*>(dwp + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    reinterpret_cast<float4*>(partial + size_t(blockIdx.y) * cols)[c4] = acc;
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, size_t n) {
     pdl_wait();
     pdl_launch();
@@ -360,6 +401,23 @@ void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, 
     if (n % 4) throw std::invalid_argument("adamw: n % 4");
     const float bc1 = 1.f - powf(b1, float(step)), bc2 = 1.f - powf(b2, float(step));
     launch_k(adamw_kernel, dim3(grid_for(n, 4, 256)), dim3(256), 0, s, 1, w, wb, g, m, v, n, lr, b1, b2, eps, wd, bc1, bc2);
+}
+void fold_weight(const float* w, const float* g, __nv_bfloat16* wb, int rows, int cols, cudaStream_t s) {
+    if (cols % 4) throw std::invalid_argument("fold_weight: cols % 4");
+    const size_t n = size_t(rows) * cols;
+    launch_k(fold_weight_kernel, dim3(grid_for(n, 4, 256)), dim3(256), 0, s, 1, w, g, wb, n, cols);
+}
+void fold_grad(float* dwp, const float* w, const float* g, float* dw, float* dg, float* scratch, size_t scratch_floats,
+               int rows, int cols, cudaStream_t s) {
+    if (cols % 128) throw std::invalid_argument("fold_grad: cols % 128");
+    int rpb = 64;
+    while (size_t((rows + rpb - 1) / rpb) * cols > scratch_floats) rpb *= 2;
+    const int nb = (rows + rpb - 1) / rpb;
+    const int threads = std::min(128, cols / 4);
+    dim3 grid((cols / 4 + threads - 1) / threads, nb);
+    launch_k(fold_grad_partial_kernel, grid, dim3(threads), 0, s, 1, dwp, w, g, dw, scratch, rows, cols, rpb);
+    launch_k(rmsnorm_dgamma_sum_kernel, dim3((cols + 31) / 32), dim3(256), 0, s, 1, static_cast<const float*>(scratch),
+             dg, nb, cols);
 }
 void f32_to_bf16(const float* src, __nv_bfloat16* dst, size_t n, cudaStream_t s) {
     launch_k(f32_to_bf16_kernel, dim3(grid_for(n, 4, 256)), dim3(256), 0, s, 1, src, dst, n);

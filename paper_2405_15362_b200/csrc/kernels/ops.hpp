@@ -25,6 +25,7 @@ void attn_bwd_pre(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* ds
                   cudaStream_t s);
 void attn_dq_store(const float* dq_acc, __nv_bfloat16* dqkv, int heads, int T, cudaStream_t s);
 
+// g may be null (unit gamma: the gamma is folded into the next projection)
 void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
                  cudaStream_t s);
 // dx = dres (may be null) + d/dx rmsnorm(x)*g applied to dy
@@ -41,6 +42,11 @@ void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, in
 void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
            float eps, float wd, int step, cudaStream_t s);
 void f32_to_bf16(const float* src, __nv_bfloat16* dst, size_t n, cudaStream_t s);
+// gamma folding (executor.cpp): wb = bf16(w * g[col]) ; and once per step
+// dw += dwp * g[col], dg[col] += sum_rows dwp * w, dwp <- 0 (deterministic; scratch fp32)
+void fold_weight(const float* w, const float* g, __nv_bfloat16* wb, int rows, int cols, cudaStream_t s);
+void fold_grad(float* dwp, const float* w, const float* g, float* dw, float* dg, float* scratch, size_t scratch_floats,
+               int rows, int cols, cudaStream_t s);
 void init_normal(float* w, size_t n, uint64_t seed, float std, float constant, cudaStream_t s);
 
 }  // namespace pbk

@@ -771,13 +771,23 @@ SimResult account(const Timed& t) {  // simulate.hpp:257-282
 // simulate.hpp:22-86: order-preserving replay; a cross-device prerequisite
 // adds the hop latency.
 SimResult simulate(const Grid& g, const Profile& prof) {
+    std::vector<double> dur(g.ops.size());
+    for (size_t i = 0; i < g.ops.size(); ++i) dur[i] = prof.of(g.ops[i].kind);
+    return replay(g, dur, prof.comm);
+}
+
+// simulate.hpp:44-56 with one duration per pass (canonical order) instead of
+// one per kind: every pass starts when its device is free and its
+// prerequisites have ended (+comm across devices), in grid start order.
+SimResult replay(const Grid& g, const std::vector<double>& dur, double comm) {
+    if (dur.size() != g.ops.size()) throw std::invalid_argument("replay: one duration per pass required");
     Timed t;
     t.topo = g.topo;
     t.microbatches = g.microbatches;
     t.ops.resize(g.ops.size());
     for (size_t i = 0; i < g.ops.size(); ++i) {
         const auto& o = g.ops[i];
-        t.ops[i] = {o.device, o.stage, o.kind, o.mb, 0.0, prof.of(o.kind)};
+        t.ops[i] = {o.device, o.stage, o.kind, o.mb, 0.0, dur[i]};
     }
     Lookup<int64_t> look(g);
     std::vector<double> free_at(size_t(g.topo.devices) + 1, 0.0);
@@ -788,7 +798,7 @@ SimResult simulate(const Grid& g, const Profile& prof) {
         for (size_t d : look.deps(g, o)) {
             if (!done[d]) throw std::invalid_argument("simulate: prerequisite not ordered first");
             double r = t.ops[d].end();
-            if (g.ops[d].device != o.device) r += prof.comm;
+            if (g.ops[d].device != o.device) r += comm;
             at = std::max(at, r);
         }
         t.ops[i].start = at;

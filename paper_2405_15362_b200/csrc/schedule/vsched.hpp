@@ -187,6 +187,9 @@ struct SimResult {
     std::vector<double> peak;
 };
 SimResult simulate(const Grid& g, const Profile& prof);
+// simulate() with one duration per pass (canonical order) — replays measured
+// per-pass times (e.g. from an isolated-pass executor run) in grid order.
+SimResult replay(const Grid& g, const std::vector<double>& dur, double comm);
 // Same accounting as simulate() over already-timed passes (used for measured
 // timelines): makespan, busy, idle, bubble = 1 - sum busy / (d * makespan).
 SimResult account(const Timed& t);

@@ -30,6 +30,7 @@ PB_FLAG_SERIAL = 1
 PB_FLAG_TIMELINE = 2
 PB_FLAG_GEMM_TIMING = 4
 PB_FLAG_KERNEL_TIMING = 8
+PB_FLAG_ISOLATE = 16
 
 
 @dataclass
@@ -164,9 +165,10 @@ class DeviceExecutor:
         return self.timeline(), StepStats.of(st)
 
     def set_flags(self, timeline: bool = True, serial: bool = False, gemm_timing: bool = False,
-                  kernel_timing: bool = False) -> None:
+                  kernel_timing: bool = False, isolate: bool = False) -> None:
         flags = ((PB_FLAG_TIMELINE if timeline else 0) | (PB_FLAG_SERIAL if serial else 0)
-                 | (PB_FLAG_GEMM_TIMING if gemm_timing else 0) | (PB_FLAG_KERNEL_TIMING if kernel_timing else 0))
+                 | (PB_FLAG_GEMM_TIMING if gemm_timing else 0) | (PB_FLAG_KERNEL_TIMING if kernel_timing else 0)
+                 | (PB_FLAG_ISOLATE if isolate else 0))
         check(lib().pb_exec_set_flags(self._h, flags))
         self.cfg = __import__("dataclasses").replace(self.cfg, timeline=timeline, serial=serial, gemm_timing=gemm_timing)
 
@@ -266,6 +268,10 @@ class PipelineExecutor:
         stats = {dv: results[dv][1] for dv in results}
         sim = pb.account(self.schedule.topology, tl) if tl else None
         return PipelineResult(stats[self.last.device].loss, tl, stats, sim)
+
+    def set_flags(self, **kw) -> None:
+        for x in self.devices:
+            x.set_flags(**kw)
 
     def params(self) -> Dict[str, DeviceExecutor]:
         return {n: x for x in self.devices for n in x.param_names()}

@@ -27,7 +27,7 @@ from ._lib import (KINDS, DocumentError, PipeblockError, ScheduleError, check, l
                    pb_timed_pass, pb_topology)
 
 __all__ = ["GridPass", "TimedPass", "Topology", "RunTimeProfile", "BlockBuild", "GridSchedule", "SimResult",
-           "build_entry", "assemble", "exact_peak", "simulate", "account", "parse", "emit", "schedule_from_passes",
+           "build_entry", "assemble", "exact_peak", "simulate", "replay", "account", "parse", "emit", "schedule_from_passes",
            "fnv1a64", "ScheduleError", "DocumentError", "PipeblockError", "GrowthReport", "growth_rate",
            "growth_rate_unrolled", "vhalf_condition", "lower_bound", "min_memory_for_od_bubble", "SearchSpec",
            "SearchParams", "SearchResult", "FrontierPoint", "search", "frontier", "render_svg", "render_ascii",
@@ -213,6 +213,19 @@ def simulate(schedule: GridSchedule, profile: RunTimeProfile = RunTimeProfile())
     arrs = [(C.c_double * d)() for _ in range(4)]
     prof = pb_profile(profile.f, profile.b, profile.w, profile.comm)
     check(lib().pb_simulate(schedule.handle, C.byref(prof), out, n, C.byref(st), *arrs))
+    timed = [TimedPass(p.device, p.stage, KINDS[p.kind], p.microbatch, p.start, p.duration) for p in out[:n]]
+    return SimResult(timed, st.makespan, list(arrs[0]), list(arrs[1]), list(arrs[2]), st.bubble_rate, list(arrs[3]))
+
+
+def replay(schedule: GridSchedule, durations: Sequence[float], comm: float = 0.0) -> SimResult:
+    """simulate() with one duration per pass (schedule.passes order): replays measured pass times."""
+    d, n = schedule.topology.devices, len(schedule.passes)
+    assert len(durations) == n
+    dur = (C.c_double * max(n, 1))(*durations)
+    out = (pb_timed_pass * max(n, 1))()
+    st = pb_sim_stats()
+    arrs = [(C.c_double * d)() for _ in range(4)]
+    check(lib().pb_replay(schedule.handle, dur, C.c_size_t(n), C.c_double(comm), out, C.byref(st), *arrs))
     timed = [TimedPass(p.device, p.stage, KINDS[p.kind], p.microbatch, p.start, p.duration) for p in out[:n]]
     return SimResult(timed, st.makespan, list(arrs[0]), list(arrs[1]), list(arrs[2]), st.bubble_rate, list(arrs[3]))
 

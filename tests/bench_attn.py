@@ -18,6 +18,15 @@ def main():
         dout = torch.randn_like(out)
         t_bwd = timeit(lambda: K.attn_bwd(qkv, out, dout, lse2, batch, seq, heads))
         t_bwd_tc = timeit(lambda: K.attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads))
+        # library reference point (cuDNN / flash SDPA through torch), fwd and fwd+bwd
+        q = torch.randn(batch, heads, seq, 128, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+        k, v = torch.randn_like(q, requires_grad=True), torch.randn_like(q, requires_grad=True)
+        sd = torch.nn.functional.scaled_dot_product_attention
+        t_sdpa = timeit(lambda: sd(q, k, v, is_causal=True))
+        o = sd(q, k, v, is_causal=True)
+        go = torch.randn_like(o)
+        t_sdpa_fb = timeit(lambda: torch.autograd.grad(sd(q, k, v, is_causal=True), (q, k, v), go))
+        print(json.dumps({"sdpa_fwd_tflops": fl / t_sdpa / 1e9, "sdpa_bwd_tflops_est": 2.5 * fl / max(1e-9, t_sdpa_fb - t_sdpa) / 1e9}))
         print(json.dumps({"batch": batch, "seq": seq, "heads": heads, "fwd_mma_sync_us": t_old * 1e3,
                           "fwd_tcgen05_us": t_new * 1e3, "fwd_mma_sync_tflops": fl / t_old / 1e9,
                           "fwd_tcgen05_tflops": fl / t_new / 1e9, "bwd_mma_sync_us": t_bwd * 1e3,

@@ -97,3 +97,40 @@ def test_rejects_bad_shapes():
     from paper_2405_15362_b200._lib import ScheduleError
     with pytest.raises(ScheduleError):
         K.gemm(A, W, C)
+
+
+# pass shapes whose tile count leaves a ragged last wave on 74 CTA pairs -> stream-K split tiles
+SK_SHAPES = [(2048, 2048, 8192), (2048, 2048, 2048), (2048, 6144, 2048), (2048, 8192, 2048), (4096, 2048, 512)]
+
+
+@pytest.mark.parametrize("M,N,Kd", SK_SHAPES)
+def test_stream_k_epilogues(M, N, Kd):
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N + Kd)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16() * 0.05
+    ref = A.float() @ W.float().t()
+    u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    gg = torch.empty_like(u)
+    K.gemm(A, W, u, epi=1, C2=gg)
+    R = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    out = torch.empty_like(u)
+    K.gemm(A, W, out, epi=2, aux=R)
+    Wt = W.t().contiguous()
+    dg = torch.empty_like(u)
+    K.gemm(A, Wt, dg, b_mn=True, epi=3, aux=u)
+    C32 = torch.zeros(M, N, device="cuda")
+    K.gemm(A, W, C32, epi=4, accumulate=1)
+    K.gemm(A, W, C32, epi=4, accumulate=1)
+    torch.cuda.synchronize()
+    assert rel(u, ref) < 4e-3
+    assert rel(gg, gelu(u.float())) < 4e-3
+    assert rel(out, ref + R.float()) < 4e-3
+    x = u.float().requires_grad_(True)
+    (gl,) = torch.autograd.grad(gelu(x), x, torch.ones_like(x))
+    assert rel(dg, ref * gl) < 5e-3
+    assert rel(C32, 2 * ref) < 1e-4
+    # deterministic: same inputs, same bits
+    u2 = torch.empty_like(u)
+    K.gemm(A, W, u2, epi=1, C2=gg)
+    torch.cuda.synchronize()
+    assert torch.equal(u, u2)

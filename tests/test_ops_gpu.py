@@ -153,3 +153,22 @@ def test_adamw():
     assert rel(w, p.detach()) < 1e-6
     assert torch.equal(wb, w.bfloat16())
     assert gr.abs().max().item() == 0.0
+
+
+def test_attention_forward_tcgen05_rescales():
+    """Scores that grow along the key axis force the lazy O rescale on most tiles."""
+    batch, seq, heads = 1, 2048, 2
+    g = torch.Generator(device="cuda").manual_seed(77)
+    qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g)
+    q = qkv[:, : heads * 128].view(seq, heads, 128)
+    q[:] = q.abs() * 0.5 + 0.5
+    k = qkv[:, heads * 128: 2 * heads * 128].view(seq, heads, 128)
+    ramp = torch.linspace(0.0, 3.0, seq, device="cuda").view(seq, 1, 1)
+    k[:] = k.abs() * 0.1 + ramp
+    qkv = qkv.bfloat16()
+    out, lse2 = K.attn_fwd_tc(qkv, batch, seq, heads)
+    torch.cuda.synchronize()
+    ref, lse = ref_attention(qkv, batch, seq, heads)
+    assert rel(out, ref) < 1e-2
+    got_lse = (lse2 * math.log(2)).view(heads, batch, seq).permute(1, 0, 2)
+    assert ((got_lse - lse).abs() / lse.abs().clamp_min(1)).max().item() < 1e-2

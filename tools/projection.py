@@ -1,0 +1,187 @@
+"""Multi-GPU projection from ONE B200 (this round's GPU pool gives one GPU per call).
+
+For each schedule, all p pipeline devices of the REAL schedule are instantiated in
+one process on cuda:0 (PipelineExecutor, in-process transport) and one training
+step runs with PB_FLAG_ISOLATE: passes execute one at a time over the whole group
+(a GPU token taken after each pass's cross-device waits), each synchronised, so every pass's CUDA-event duration is
+its stand-alone time on a B200 at the real chunk size (embedding / LM head / loss
+on the right stages, real message copies, real activation pool).  The measured
+per-pass durations are then replayed in each device's grid order with pb_replay
+(simulate.hpp:44-56 with one duration per pass) plus a per-crossing latency of
+msg_bytes / NVLink bandwidth (an assumption, stated in the output: no NVLink here).
+
+--via-chunks (models too large to instantiate whole on one GPU: 6B, 14B): a probe
+pipeline with the SAME chunk shapes runs instead — the same schedule family at p=2
+(V: 4 stages = first / middle / middle / last chunk) or p=3 (straight: first /
+middle / last stage), each chunk with the target's layers per chunk — and the
+target schedule is replayed with the probe's mean isolated pass time per
+(chunk class, kind).  Activation memory is then the plan's slot count times the
+probe's measured slot bytes for that chunk class.
+
+Output: one JSON object (stdout, and --out file) with, per schedule, the projected
+p-GPU step time, tokens/s, bubble rate (simulate.hpp:81-82 on the replay), the
+pipeline roofline fraction (max per-device busy / makespan), measured activation
+pool bytes per device vs the exact_peak prediction and vs 1F1B.
+
+    python tools/projection.py --model 1.5b --p 8 --microbatches 32 --out profiles/r1_projection_1p5b_p8.json
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import CONFIGS  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="1.5b", choices=sorted(CONFIGS))
+    ap.add_argument("--p", type=int, nargs="+", default=[8])
+    ap.add_argument("--microbatches", type=int, default=32)
+    ap.add_argument("--micro-batch", type=int, default=1)
+    ap.add_argument("--schedules", nargs="+", default=["1f1b", "zb-h1", "v-min", "v-half", "v-zb"])
+    ap.add_argument("--nvlink-gbs", type=float, default=720.0, help="assumed achieved P2P GB/s per direction")
+    ap.add_argument("--latency-us", type=float, default=8.0, help="assumed per-transfer latency")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--via-chunks", action="store_true", help="probe-pipeline projection (see module doc)")
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2405_15362_b200 import pipeblock as pb
+    from paper_2405_15362_b200.executor import ModelConfig, PipelineExecutor, synthetic_batch
+
+    mcfg = CONFIGS[args.model]
+    cfg = ModelConfig(**mcfg, micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    T = cfg.tokens_per_microbatch
+    m = args.microbatches
+    tokens, labels = synthetic_batch(cfg, m)
+    tok, lab = torch.from_numpy(tokens).cuda(), torch.from_numpy(labels).cuda()
+    msg_bytes = T * cfg.hidden * 2
+    comm_ms = (msg_bytes / (args.nvlink_gbs * 1e9) + args.latency_us * 1e-6) * 1e3
+    out = {"model": f"gpt-{args.model}", "config": mcfg, "microbatches": m, "micro_batch": args.micro_batch,
+           "tokens_per_step": m * T, "gpu": torch.cuda.get_device_name(0),
+           "method": "all p pipeline devices on one B200, PB_FLAG_ISOLATE per-pass CUDA-event times, "
+                     "replayed in grid order (pb_replay) with comm = msg_bytes/nvlink_gbs + latency",
+           "assumptions": {"nvlink_gbs": args.nvlink_gbs, "latency_us": args.latency_us, "msg_bytes": msg_bytes,
+                           "comm_ms": comm_ms}, "runs": []}
+    for p in args.p:
+        for name in args.schedules:
+            t0 = time.time()
+            if args.via_chunks:
+                out["runs"].append(project_via_chunks(args, mcfg, name, p, m, comm_ms))
+                print(json.dumps({k: out["runs"][-1][k] for k in ("schedule", "p", "projected_tokens_per_s",
+                                                                  "bubble_rate", "max_pool_gib")}), file=sys.stderr)
+                continue
+            sched = pb.assemble(pb.build_entry(name, p), m)
+            ex = PipelineExecutor(cfg, sched, [0] * p)
+            ex.set_flags(timeline=True, isolate=True)
+            ex.step(tok, lab, on_host=False)                  # warm-up
+            res = ex.step(tok, lab, on_host=False)
+            dur = {(q.device, q.stage, q.kind, q.microbatch): q.duration for q in res.timeline}
+            durations = [dur[(q.device, q.stage, q.kind, q.microbatch)] for q in sched.passes]
+            rep = pb.replay(sched, durations, comm_ms)
+            rep0 = pb.replay(sched, durations, 0.0)
+            per_kind = {}
+            for q in sched.passes:
+                per_kind.setdefault(q.kind, []).append(dur[(q.device, q.stage, q.kind, q.microbatch)])
+            pred = pb.exact_peak(sched)
+            pool = [res.per_device[d].pool_bytes for d in sorted(res.per_device)]
+            slots = [res.per_device[d].pool_slots for d in sorted(res.per_device)]
+            run = {"schedule": name, "p": p, "loss": res.loss,
+                   "projected_ms_per_step": rep.makespan, "projected_tokens_per_s": m * T / (rep.makespan / 1e3),
+                   "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
+                   "pipeline_roofline_frac": max(rep.busy) / rep.makespan,
+                   "ideal_ms": max(rep.busy), "busy_ms_per_device": rep.busy,
+                   "mean_pass_ms": {k: sum(v) / len(v) for k, v in per_kind.items()},
+                   "predicted_peak_units": pred, "measured_slots": slots, "pool_bytes_per_device": pool,
+                   "max_pool_gib": max(pool) / 2**30, "wall_s": time.time() - t0}
+            out["runs"].append(run)
+            print(json.dumps({k: run[k] for k in ("schedule", "p", "projected_tokens_per_s", "bubble_rate",
+                                                  "pipeline_roofline_frac", "max_pool_gib")}), file=sys.stderr)
+            del ex
+            torch.cuda.synchronize()
+    if args.via_chunks:
+        out["method"] = ("probe pipeline with the target's chunk shapes on one B200 (PB_FLAG_ISOLATE pass times, "
+                         "mean per chunk class and kind), target schedule replayed with pb_replay")
+    # activation memory vs 1F1B at the same p (measured pool bytes, max over devices)
+    for r in out["runs"]:
+        base = next((b for b in out["runs"] if b["schedule"] == "1f1b" and b["p"] == r["p"]), None)
+        if base:
+            r["pool_vs_1f1b"] = max(r["pool_bytes_per_device"]) / max(base["pool_bytes_per_device"])
+            r["tokens_per_s_vs_1f1b"] = r["projected_tokens_per_s"] / base["projected_tokens_per_s"]
+    text = json.dumps(out, indent=1)
+    print(text)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(text)
+
+
+def chunk_class(stage: int, num_stages: int) -> str:
+    return "first" if stage == 1 else ("last" if stage == num_stages else "middle")
+
+
+def project_via_chunks(args, mcfg, name, p, m, comm_ms):
+    import dataclasses
+
+    import torch
+
+    from paper_2405_15362_b200 import pipeblock as pb
+    from paper_2405_15362_b200.executor import ModelConfig, PipelineExecutor, synthetic_batch
+
+    target = pb.assemble(pb.build_entry(name, p), m)
+    S = target.topology.num_stages
+    if mcfg["layers"] % S:
+        raise SystemExit(f"{mcfg['layers']} layers do not split into {S} stages")
+    per_chunk = mcfg["layers"] // S
+    v_shape = S == 2 * p
+    probe_p = 2 if v_shape else 3
+    probe_S = 2 * probe_p if v_shape else probe_p
+    probe_m = min(m, 4 * probe_p)
+    cfg = ModelConfig(**dict(mcfg, layers=per_chunk * probe_S), micro_batch=args.micro_batch, optimizer=True,
+                      timeline=True)
+    probe = pb.assemble(pb.build_entry(name, probe_p), probe_m)
+    tokens, labels = synthetic_batch(cfg, probe_m)
+    tok, lab = torch.from_numpy(tokens).cuda(), torch.from_numpy(labels).cuda()
+    ex = PipelineExecutor(cfg, probe, [0] * probe_p)
+    ex.set_flags(timeline=True, isolate=True)
+    ex.step(tok, lab, on_host=False)
+    res = ex.step(tok, lab, on_host=False)
+    acc = {}
+    for q in res.timeline:
+        acc.setdefault((chunk_class(q.stage, probe_S), q.kind), []).append(q.duration)
+    mean = {k: sum(v) / len(v) for k, v in acc.items()}
+    # activation slot bytes per chunk class: the probe's slot size (largest chunk class on a device)
+    slot_bytes = {d: res.per_device[d].slot_bytes for d in res.per_device}
+    del ex
+    torch.cuda.synchronize()
+    durations = [mean[(chunk_class(q.stage, S), q.kind)] for q in target.passes]
+    rep = pb.replay(target, durations, comm_ms)
+    rep0 = pb.replay(target, durations, 0.0)
+    pred = pb.exact_peak(target)
+    # a device's slot holds its largest stage (last-stage slots add logits); middle-class bytes otherwise
+    mid_bytes = min(slot_bytes.values())
+    head_bytes = max(slot_bytes.values())
+    pool = []
+    for d in range(1, p + 1):
+        holds_last = target.topology.device_of(S) == d
+        pool.append(int(pred[d - 1]) * (head_bytes if holds_last else mid_bytes))
+    T = cfg.tokens_per_microbatch
+    return {"schedule": name, "p": p, "probe": f"{name} p={probe_p} m={probe_m}, {cfg.layers} layers "
+                                                f"({per_chunk} per chunk)",
+            "projected_ms_per_step": rep.makespan, "projected_tokens_per_s": m * T / (rep.makespan / 1e3),
+            "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
+            "pipeline_roofline_frac": max(rep.busy) / rep.makespan, "ideal_ms": max(rep.busy),
+            "busy_ms_per_device": rep.busy, "mean_pass_ms": {f"{c}.{k}": v for (c, k), v in sorted(mean.items())},
+            "predicted_peak_units": pred, "pool_bytes_per_device": pool, "max_pool_gib": max(pool) / 2**30,
+            "probe_slot_bytes": sorted(set(slot_bytes.values()))}
+
+
+if __name__ == "__main__":
+    main()
