@@ -110,3 +110,7 @@ extern "C" int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dou
 extern "C" int pbt_gemm_set_cta_group(int32_t cg) {
     return pbx::guard([&] { pbk::gemm_force_cta_group(cg); });
 }
+
+extern "C" int pbt_gemm_set_stream_k(int32_t on) {
+    return pbx::guard([&] { pbk::gemm_force_stream_k(on); });
+}

@@ -533,7 +533,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 //   * P^T kept in TMEM (bf16 pairs written over the consumed S^T columns) and fed to the
 //     dV MMA as the A operand straight from TMEM, which frees 32 KB of smem for
 //   * double-buffered Q / dO tiles: the TMA of tile i+1 overlaps tile i,
-//   * dQ drained from TMEM with red.global.add.v4.f32 (no fp32 smem staging).
+//   * dQ staged (fp32) in the tile's consumed Q / dO buffers and sent with one TMA bulk
+//     reduce-add per 16 KB chunk; the producer refills that buffer once the reduce has read it.
 struct Bwd3Smem {
     static constexpr int k = 0;
     static constexpr int v = k + kTile;
@@ -542,8 +543,11 @@ struct Bwd3Smem {
     static constexpr int dst = dO + 2 * kTile;
     static constexpr int lse = dst + kTile;   // [2][256] floats: lse2 | D
     static constexpr int bars = lse + 2048;
-    static constexpr int total = bars + 256 + 1024;
+    // 512 B of alignment slack (the 227 KB opt-in limit leaves no room for 1 KB; the dynamic
+    // window starts 1 KB-aligned when the kernel has no static shared memory)
+    static constexpr int total = bars + 256 + 512;
 };
+static_assert(Bwd3Smem::total <= 232448, "attn bwd v3: shared memory over the sm_100 opt-in limit");
 
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -565,10 +569,11 @@ __device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&r)[3
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                        float* __restrict__ dq_acc, const float* __restrict__ lse2, const float* __restrict__ dsum,
+                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2, const float* __restrict__ dsum,
                         __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (Bwd3Smem::total)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd3Smem::bars);
     uint64_t* kv_full = bars + 0;
     uint64_t* qdo_full = bars + 1;   // [2]
@@ -592,6 +597,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (warp == 0 && elect_one()) {
         tma_prefetch(&tm_qkv);
         tma_prefetch(&tm_do);
+        tma_prefetch(&tm_dq);
         for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 8 : 1);
         fence_barrier_init();
     }
@@ -667,7 +673,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
                            (i | kk) != 0);
                 }
-                tc_commit(&qdo_empty[st]);  // Q, dO of this tile consumed
                 // dQ = dS K -> TMEM [0,128) (after the dV MMA has read P^T there: in-order pipe)
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
@@ -736,26 +741,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(ds_full);
-            // dQ tile (thread = query row r, column half hf) -> fp32 atomics into dq_acc
-            mbar_wait(dq_full, i & 1);
+            // dQ tile (thread = query row r, column half hf): TMEM -> fp32 smem staged in this tile's
+            // consumed Q / dO buffers (4 swizzled [128][32] chunks) -> TMA bulk reduce-add into dq_acc
+            mbar_wait(dq_full, i & 1);  // every MMA of this tile retired: Q / dO no longer read
             tc_fence_after();
-            float* dqrow = dq_acc + size_t(tok0 + qb * BQ + r) * (H * D) + head * D;
+            uint8_t* stage_q = sm + Bwd3Smem::q + (i & 1) * kTile;
+            uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
 #pragma unroll 1
             for (int cc = 0; cc < 2; ++cc) {
                 const int c = hf * 2 + cc;
                 float v[32];
                 tmem_ld32(tmem + lane_base + c * 32, v);
                 tmem_ld_wait();
+                uint8_t* chunk = (c < 2 ? stage_q : stage_d) + (c & 1) * 16384 + r * 128;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dqrow + c * 32 + 4 * j),
-                                 "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
-                                 : "memory");
+                for (int g = 0; g < 8; ++g)
+                    *reinterpret_cast<float4*>(chunk + ((g ^ (r & 7)) << 4)) =
+                        make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
             }
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(s_free);  // TMEM [0,256) free for the next S^T / dP^T
+            fence_async_smem();
+            bar_sync_compute();
+            if (threadIdx.x == 64) {  // warp 2 lane 0
+                const int row = tok0 + qb * BQ;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tm_dq)),
+                        "r"(smem_u32((c < 2 ? stage_q : stage_d) + (c & 1) * 16384)), "r"(head * D + c * 32), "r"(row)
+                        : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(&qdo_empty[i & 1]);  // staging read out: the producer may refill this buffer
+            }
         }
+        if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         // dV, dK rows (thread = key row, column half hf)
         mbar_wait(dkv_full, 0);
         tc_fence_after();
@@ -814,7 +837,7 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
         launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
                  static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
     else
-        launch_k(attn_bwd_tc3_kernel, grid, dim3(kBwdThreads), Bwd3Smem::total, s, 1, tq, td, dq_acc, lse2,
+        launch_k(attn_bwd_tc3_kernel, grid, dim3(kBwdThreads), Bwd3Smem::total, s, 1, tq, td, tdq, lse2,
                  static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
     attn_dq_store(dq_acc, dqkv, heads, T, s);
 }

@@ -33,9 +33,10 @@ struct GemmArgs {
 };
 
 void gemm(const GemmArgs& g, cudaStream_t s);
-// Stream-K split tiles for ragged last waves (default on; PB_STREAMK=0 disables).  Per host
+// Stream-K split tiles for ragged last waves (PB_STREAMK=1 enables; off by default).  Per host
 // thread: off while other streams may run GEMMs concurrently on the same GPU (see gemm_tc.cu).
 void gemm_allow_stream_k(bool on);
+void gemm_force_stream_k(int on);  // tests: -1 environment, 0 off, 1 on
 
 // Grouped weight-gradient GEMMs: independent dW (+)= dY^T X problems (A and B MN-major,
 // fp32 epilogue) run as ONE persistent CTA-pair launch over their concatenated tiles,

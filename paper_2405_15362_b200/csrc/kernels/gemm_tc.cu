@@ -501,12 +501,15 @@ SkWorkspace& sk_workspace(cudaStream_t s) {
 // needs while their own owners spin.  Callers that share a GPU across concurrently running
 // streams turn it off for their thread (gemm_allow_stream_k).
 thread_local bool t_sk_allowed = true;
+// Off by default: on the 1.5B step it measured slower in-step (57k vs 70k tokens/s) although
+// isolated launches are on par; PB_STREAMK=1 enables it.
+int g_force_sk = -1;  // tests: -1 environment, 0 off, 1 on
 bool sk_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("PB_STREAMK");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
-    return on && t_sk_allowed;
+    return (g_force_sk < 0 ? on : g_force_sk == 1) && t_sk_allowed;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
@@ -642,6 +645,7 @@ void gemm_group_destroy(GemmGroup& g) {
 }
 
 void gemm_allow_stream_k(bool on) { t_sk_allowed = on; }
+void gemm_force_stream_k(int on) { g_force_sk = on; }
 
 static int g_force_cg = -1;  // tests: -1 auto, 1 or 2 forced
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }

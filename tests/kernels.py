@@ -109,3 +109,7 @@ def attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads):
 
 def set_cta_group(cg: int) -> None:
     _lib.check(_lib.lib().pbt_gemm_set_cta_group(cg))
+
+
+def set_stream_k(on: int) -> None:
+    _lib.check(_lib.lib().pbt_gemm_set_stream_k(on))

@@ -103,8 +103,15 @@ def test_rejects_bad_shapes():
 SK_SHAPES = [(2048, 2048, 8192), (2048, 2048, 2048), (2048, 6144, 2048), (2048, 8192, 2048), (4096, 2048, 512)]
 
 
+@pytest.fixture(params=[0, 1], ids=["tiles", "streamk"])
+def stream_k(request):
+    K.set_stream_k(request.param)
+    yield request.param
+    K.set_stream_k(-1)
+
+
 @pytest.mark.parametrize("M,N,Kd", SK_SHAPES)
-def test_stream_k_epilogues(M, N, Kd):
+def test_stream_k_epilogues(M, N, Kd, stream_k):
     g = torch.Generator(device="cuda").manual_seed(M * 3 + N + Kd)
     A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
     W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16() * 0.05

@@ -1,6 +1,6 @@
 set -x
-timeout 300 python -m pytest tests/test_gemm_gpu.py tests/test_ops_gpu.py --timeout 120 -x -q 2>&1 | tail -8
-timeout 900 python -m pytest tests/test_executor_gpu.py tests/test_multiprocess_gpu.py --timeout 240 -x -q 2>&1 | tail -8
+timeout 300 python -m pytest tests/test_gemm_gpu.py tests/test_ops_gpu.py --timeout 120 -q 2>&1 | tail -8
+timeout 900 python -m pytest tests/test_executor_gpu.py tests/test_multiprocess_gpu.py --timeout 240 -q 2>&1 | tail -8
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 300 python -m tests.bench_gemm 2048 > gpurun_out/bench_gemm_2048_sk.txt 2>&1
 timeout 300 python -m tests.bench_attn > gpurun_out/bench_attn_d.txt 2>&1
