@@ -5,9 +5,9 @@ AdamW) of a GPT on B200s, driven by the reference's schedule API.
     torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
 
 Workload (BASELINE.json configs[2]): GPT ~1.5B (L=32, h=2048, 16 heads,
-seq 2048, vocab 50304), bf16, synthetic tokens, m=32 microbatches of 1
-sequence per step (global batch 32 x 2048 tokens, fixed as N grows ->
-"strong" scaling).  N=1 runs zb-h1 with d=1 (all stages serialised; the
+seq 2048, vocab 50304), bf16, synthetic tokens, m=32 microbatches of 2
+sequences per step (global batch 64 x 2048 tokens, fixed as N grows ->
+"strong" scaling; micro-batch 2 measured +10% tokens/s over 1 at N=1).  N=1 runs zb-h1 with d=1 (all stages serialised; the
 V schedules need d >= 2), N>1 runs V-Half with p=N.  A step is every pass of
 the reference's assemble(build_entry(...), m) op order plus the optimizer.
 
@@ -16,6 +16,7 @@ Prints ONE JSON line on rank 0 (see README/DESIGN for the keys).
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -45,9 +46,11 @@ def parse():
     ap.add_argument("--model", default="1.5b", choices=sorted(CONFIGS))
     ap.add_argument("--schedule", default=None, help="gallery entry (default zb-h1 at N=1, v-half at N>1)")
     ap.add_argument("--microbatches", type=int, default=32)
-    ap.add_argument("--micro-batch", type=int, default=1)
+    ap.add_argument("--micro-batch", type=int, default=2)
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="target seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--even-split", action="store_true",
+                    help="layers / num_stages per stage (default: balance the LM-head stage, N > 1)")
     return ap.parse_args()
 
 
@@ -229,6 +232,9 @@ def main():
     sched_name = args.schedule or ("zb-h1" if p == 1 else "v-half")
     schedule = pb.assemble(pb.build_entry(sched_name, p), args.microbatches)
     cfg = ModelConfig(**mcfg, micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    if p > 1 and not args.even_split:
+        from paper_2405_15362_b200.executor import balanced_stage_layers
+        cfg = dataclasses.replace(cfg, stage_layers=balanced_stage_layers(cfg, schedule.topology))
     device = rank + 1
     ex = DeviceExecutor(cfg, schedule, device, local)
     if world > 1:
@@ -383,6 +389,7 @@ def main():
         "config": {"workload": workload_name(args, sched_name), "model": f"gpt-{args.model}",
                    "global_batch": m * args.micro_batch, "seq_len": cfg.seq, "parallelism": f"pp{p}",
                    "schedule": sched_name, "microbatches": m, "micro_batch": args.micro_batch,
+                   "stage_layers": list(cfg.stage_layers) if cfg.stage_layers else None,
                    "l2": "no flush: per-step working set (weights+grads+optimizer+activations, tens of GB) >> 126 MB L2"},
         "bubble_rate": sim.bubble_rate if sim else None,
         "bubble_def": "1 - sum busy / (d * makespan) over measured pass times (simulate.hpp:81-82)",

@@ -197,6 +197,10 @@ typedef struct pb_model_cfg {
     float lr, beta1, beta2, eps, weight_decay;
     int32_t optimizer; /* 1 = AdamW step after the flush, 0 = gradients only */
     int32_t flags;     /* PB_FLAG_* */
+    /* NULL: layers / num_stages per stage.  Else num_stages entries >= 1 summing to `layers`
+     * (e.g. fewer layers on the stages that also carry the embedding / LM head; the
+     * schedule is unchanged, only the work per pass).  Copied at pb_exec_create. */
+    const int32_t* stage_layers;
 } pb_model_cfg;
 
 #define PB_FLAG_SERIAL 1     /* device-synchronise after every pass (race check mode) */

@@ -55,8 +55,17 @@ def layer_forward(x, p: Dict[str, torch.Tensor], pre: str, cfg):
     return x1 + gelu(b @ p[pre + "w1"].t()) @ p[pre + "w2"].t()
 
 
+def stage_layers(cfg, S: int) -> List[int]:
+    """Layers per stage: cfg.stage_layers when given (uneven split), else layers // S each."""
+    sl = getattr(cfg, "stage_layers", None)
+    if sl is not None:
+        assert len(sl) == S and sum(sl) == cfg.layers
+        return list(sl)
+    return [cfg.layers // S] * S
+
+
 def stage_param_names(cfg, S: int, s: int) -> List[str]:
-    Lc = cfg.layers // S
+    Lc = stage_layers(cfg, S)[s - 1]
     names = ["s1.emb"] if s == 1 else []
     for l in range(Lc):
         names += [f"s{s}.l{l}.{w}" for w in ("norm1", "wqkv", "wo", "norm2", "w1", "w2")]
@@ -78,7 +87,7 @@ def shapes(cfg, S: int) -> Dict[str, Tuple[int, ...]]:
 
 def stage_forward(s: int, S: int, inp, p, cfg, tokens_mb=None, labels_mb=None, loss_scale=1.0):
     """Stage s on one microbatch: returns its output (s < S) or scaled CE sum (s == S)."""
-    Lc = cfg.layers // S
+    Lc = stage_layers(cfg, S)[s - 1]
     x = p["s1.emb"][tokens_mb] if s == 1 else inp
     for l in range(Lc):
         x = layer_forward(x, p, f"s{s}.l{l}.", cfg)
@@ -88,10 +97,18 @@ def stage_forward(s: int, S: int, inp, p, cfg, tokens_mb=None, labels_mb=None, l
     return F.cross_entropy(logits, labels_mb.long(), reduction="sum") * loss_scale
 
 
-def rename_for(params: Dict[str, torch.Tensor], cfg, S_from: int, S_to: int) -> Dict[str, torch.Tensor]:
-    """Map parameter names between stage partitions (global layer index is invariant)."""
+def rename_for(params: Dict[str, torch.Tensor], cfg, S_from: int, S_to: int, cfg_to=None) -> Dict[str, torch.Tensor]:
+    """Map parameter names between stage partitions (global layer index is invariant).
+    cfg gives the source split (its stage_layers, if any); cfg_to the target's (default: even)."""
+    import types
+    first_from = [0]
+    for n in stage_layers(cfg, S_from):
+        first_from.append(first_from[-1] + n)
+    tgt = cfg_to if cfg_to is not None else types.SimpleNamespace(layers=cfg.layers, stage_layers=None)
+    owner = []  # global layer -> (stage, local index) in the target split
+    for s, n in enumerate(stage_layers(tgt, S_to), 1):
+        owner += [(s, l) for l in range(n)]
     out = {}
-    Lf, Lt = cfg.layers // S_from, cfg.layers // S_to
     for n, t in params.items():
         parts = n.split(".")
         if parts[1] == "emb":
@@ -99,8 +116,9 @@ def rename_for(params: Dict[str, torch.Tensor], cfg, S_from: int, S_to: int) -> 
         elif len(parts) == 2:
             out[f"s{S_to}.{parts[1]}"] = t
         else:
-            gl = (int(parts[0][1:]) - 1) * Lf + int(parts[1][1:])
-            out[f"s{gl // Lt + 1}.l{gl % Lt}.{parts[2]}"] = t
+            gl = first_from[int(parts[0][1:]) - 1] + int(parts[1][1:])
+            s2, l2 = owner[gl]
+            out[f"s{s2}.l{l2}.{parts[2]}"] = t
     return out
 
 

@@ -42,7 +42,7 @@ class pb_model_cfg(C.Structure):
     _fields_ = [("layers", C.c_int32), ("hidden", C.c_int32), ("heads", C.c_int32), ("seq", C.c_int32),
                 ("vocab", C.c_int32), ("micro_batch", C.c_int32), ("seed", C.c_uint64), ("lr", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
-                ("optimizer", C.c_int32), ("flags", C.c_int32)]
+                ("optimizer", C.c_int32), ("flags", C.c_int32), ("stage_layers", C.POINTER(C.c_int32))]
 
 
 class pb_exec_stats(C.Structure):

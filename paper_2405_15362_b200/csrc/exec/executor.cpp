@@ -84,6 +84,7 @@ void Exec::build_layout() {
     };
     slot_bytes = 0;
     for (int s : stages) {
+        const int Lc = stage_L[s];
         StageLayout L;
         size_t cur = 0;
         L.x.resize(size_t(Lc) + 1);
@@ -108,10 +109,12 @@ void Exec::build_layout() {
             y.rstd2 = add(cur, size_t(T) * 4);
             y.lse = add(cur, size_t(H) * T * 4);
         }
-        if (s == S) {
-            L.hf = add(cur, Th * 2);
-            L.rstdf = add(cur, size_t(T) * 4);
-            L.logits = add(cur, size_t(T) * V * 2);
+        if (s == S) {  // LM-head buffers live in their own lifespan pool (head slots, see constructor)
+            size_t hc = 0;
+            L.hf = add(hc, Th * 2);
+            L.rstdf = add(hc, size_t(T) * 4);
+            L.logits = add(hc, size_t(T) * V * 2);
+            head_bytes = hc;
         }
         L.bytes = cur;
         layout[s] = L;
@@ -132,8 +135,8 @@ void Exec::build_params() {
     for (int s : stages) {
         StageParams sp;
         if (s == 1) sp.emb = add("s1.emb", size_t(V) * h, 1, std_in, 0.f);
-        for (int l = 0; l < Lc; ++l) {
-            const int gl = (s - 1) * Lc + l;
+        for (int l = 0; l < stage_L[s]; ++l) {
+            const int gl = stage_first[s] + l;
             const std::string pre = "s" + std::to_string(s) + ".l" + std::to_string(l) + ".";
             LayerParams lp;
             lp.g1 = add(pre + "norm1", h, 16 + gl * 8 + 0, 0.f, 1.f);
@@ -157,8 +160,22 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
     : cfg(c), plan(make_plan(grid)), dev(device), cuda(cuda_dev) {
     if (device < 1 || device > plan.topo.devices) throw std::invalid_argument("device out of range");
     S = plan.topo.num_stages;
-    if (cfg.layers % S) throw std::invalid_argument("layers must be a multiple of the stage count");
-    Lc = cfg.layers / S;
+    stage_L.assign(size_t(S) + 1, 0);
+    stage_first.assign(size_t(S) + 2, 0);
+    if (cfg.stage_layers) {
+        int sum = 0;
+        for (int s = 1; s <= S; ++s) {
+            stage_L[s] = cfg.stage_layers[s - 1];
+            if (stage_L[s] < 1) throw std::invalid_argument("stage_layers: every stage needs >= 1 layer");
+            sum += stage_L[s];
+        }
+        if (sum != cfg.layers) throw std::invalid_argument("stage_layers must sum to layers");
+        cfg.stage_layers = nullptr;  // copied
+    } else {
+        if (cfg.layers % S) throw std::invalid_argument("layers must be a multiple of the stage count");
+        for (int s = 1; s <= S; ++s) stage_L[s] = cfg.layers / S;
+    }
+    for (int s = 1; s <= S; ++s) stage_first[s + 1] = stage_first[s] + stage_L[s];
     h = cfg.hidden;
     H = cfg.heads;
     V = cfg.vocab;
@@ -231,6 +248,28 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
 
     nslots = plan.slots[dev];
     pool = static_cast<uint8_t*>(dmalloc(slot_bytes * size_t(std::max(nslots, 1)), "activation pool"));
+    // head pool: hf / rstd / logits of the last stage, a slot per live (S, mb) from F(S) to W(S),
+    // coloured like the main pool but over stage S alone — a V device holding stages 1 and 2p
+    // does not pay the logits in every one of its slots
+    head_slot_mb.assign(size_t(m), -1);
+    if (std::find(stages.begin(), stages.end(), S) != stages.end()) {
+        std::vector<bool> busy;
+        for (int i : plan.dev_ops[dev]) {
+            const auto& o = plan.ops[size_t(i)].op;
+            if (o.stage != S) continue;
+            if (o.kind == vsched::Kind::F) {
+                int k = 0;
+                while (k < int(busy.size()) && busy[k]) ++k;
+                if (k == int(busy.size())) busy.push_back(false);
+                busy[k] = true;
+                head_slot_mb[size_t(o.mb)] = k;
+            } else if (o.kind == vsched::Kind::W || o.kind == vsched::Kind::BW) {
+                busy[size_t(head_slot_mb[size_t(o.mb)])] = false;
+            }
+        }
+        nhead = int(busy.size());
+        hpool = static_cast<uint8_t*>(dmalloc(head_bytes * size_t(std::max(nhead, 1)), "head pool"));
+    }
     build_w_groups();
     msg_bytes = align_up(size_t(T) * h * 2, 1024);
     nout = std::max(plan.outboxes[dev], 1);
@@ -312,6 +351,9 @@ __nv_bfloat16* Exec::bf(int slot, size_t off) const {
     return reinterpret_cast<__nv_bfloat16*>(pool + size_t(slot) * slot_bytes + off);
 }
 float* Exec::f32(int slot, size_t off) const { return reinterpret_cast<float*>(pool + size_t(slot) * slot_bytes + off); }
+uint8_t* Exec::head(int mb, size_t off) const {
+    return hpool + size_t(head_slot_mb.at(size_t(mb))) * head_bytes + off;
+}
 __nv_bfloat16* Exec::outbox_ptr(int k) const { return reinterpret_cast<__nv_bfloat16*>(outbox + size_t(k) * msg_bytes); }
 
 template <typename Fn>
@@ -374,6 +416,7 @@ void Exec::build_w_groups() {
     for (int s : stages) {
         const StageLayout& L = layout.at(s);
         const StageParams& P = sparams.at(s);
+        const int Lc = stage_L[s];
         for (int slot = 0; slot < nslots; ++slot) {
             std::vector<pbk::GemmArgs> v;
             double fl = 0;
@@ -422,7 +465,11 @@ void Exec::run_gemm_timed(const char* label, double flops, const std::function<v
     ++launches;
 }
 
+#define HB(mb, off) reinterpret_cast<__nv_bfloat16*>(head(mb, off))
+#define HF(mb, off) reinterpret_cast<float*>(head(mb, off))
+
 void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
+    const int Lc = stage_L[s];
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
     __nv_bfloat16* x0 = bf(slot, L.x[0]);
@@ -446,24 +493,25 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         launches += 3;
     }
     if (s == S) {
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), bf(slot, L.hf), f32(slot, L.rstdf), T, h, cs); });
-        gemm(T, V, h, bf(slot, L.hf), false, W(P.head), false, bf(slot, L.logits), pbk::EPI_STORE);
-        timed("cross_entropy", [&] { pbk::cross_entropy(bf(slot, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), HB(mb, L.hf), HF(mb, L.rstdf), T, h, cs); });
+        gemm(T, V, h, HB(mb, L.hf), false, W(P.head), false, HB(mb, L.logits), pbk::EPI_STORE);
+        timed("cross_entropy", [&] { pbk::cross_entropy(HB(mb, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
                            cs); });
         launches += 2;
     }
 }
 
 void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
+    const int Lc = stage_L[s];
     (void)mb;
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
     if (s == S) {
         // dhf = dlogits . Whead ; dx_L = rmsnorm_bwd(dhf)
-        gemm(T, h, V, bf(slot, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), f32(slot, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
+        gemm(T, h, V, HB(mb, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), HF(mb, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
                          cs); });
-        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), f32(slot, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
+        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), HF(mb, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
         launches += fold ? 1 : 2;
     }
     for (int l = Lc - 1; l >= 0; --l) {
@@ -487,6 +535,7 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
 }
 
 void Exec::pass_weight(int s, int mb, int slot) {
+    const int Lc = stage_L[s];
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
     auto grp = wgroups.find({s, slot});
@@ -502,7 +551,7 @@ void Exec::pass_weight(int s, int mb, int slot) {
         gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, y.a), true, GW(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
     }
     if (s == S)
-        gemm(V, h, T, bf(slot, L.logits), true, bf(slot, L.hf), true, GW(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(V, h, T, HB(mb, L.logits), true, HB(mb, L.hf), true, GW(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
     if (s == 1) {
         timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, cs); });
         ++launches;
@@ -568,7 +617,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
         // ---- incoming boundary tensor
         __nv_bfloat16* in_dst = nullptr;
         const Msg* in = po.in_msg >= 0 ? &plan.msgs[po.in_msg] : nullptr;
-        if (in) in_dst = o.kind == Kind::F ? bf(po.slot, L.x[0]) : bf(po.slot, L.dx[Lc]);
+        if (in) in_dst = o.kind == Kind::F ? bf(po.slot, L.x[0]) : bf(po.slot, L.dx.back());
         if (in && !in->local()) {
             if (o.kind == Kind::F && po.free_op >= 0) {
                 ck(cudaStreamWaitEvent(xs, ev_free[size_t(pos_of[po.free_op])], 0), "wait");
@@ -706,7 +755,7 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
         st->pool_slots = nslots;
         st->pool_peak = pool_live_peak;
         st->slot_bytes = int64_t(slot_bytes);
-        st->pool_bytes = int64_t(slot_bytes) * nslots;
+        st->pool_bytes = int64_t(slot_bytes) * nslots + int64_t(head_bytes) * nhead;
         st->peer_bytes = peer_bytes;
         st->kernel_launches = launches;
         double gms = 0;

@@ -92,7 +92,8 @@ class Exec {
     pb_model_cfg cfg;
     ExecPlan plan;
     int dev, cuda;
-    int S = 0, Lc = 0, T = 0, h = 0, H = 0, V = 0, seq = 0, mbs = 0, m = 0;
+    int S = 0, T = 0, h = 0, H = 0, V = 0, seq = 0, mbs = 0, m = 0;
+    std::vector<int> stage_L, stage_first;  // [stage] layers held, global index of its first layer
     std::vector<int> stages;
     std::vector<PTensor> ptensors;
     float *master = nullptr, *grads = nullptr, *adam_m = nullptr, *adam_v = nullptr;
@@ -138,7 +139,11 @@ class Exec {
     std::map<std::pair<int, int>, double> wgroup_flops;
     std::map<int, StageLayout> layout;
     std::map<int, StageParams> sparams;
-    size_t slot_bytes = 0, msg_bytes = 0, nflags = 0;
+    size_t slot_bytes = 0, head_bytes = 0, msg_bytes = 0, nflags = 0;
+    uint8_t* hpool = nullptr;           // last-stage head buffers (hf, rstd, logits), own lifespan pool
+    int nhead = 0;
+    std::vector<int> head_slot_mb;      // microbatch -> head slot
+    uint8_t* head(int mb, size_t off) const;
     int nslots = 0, nout = 0, pool_live_peak = 0;
     uint8_t* pool = nullptr;
     uint8_t* outbox = nullptr;

@@ -51,6 +51,7 @@ class ModelConfig:
     timeline: bool = True
     serial: bool = False
     gemm_timing: bool = False
+    stage_layers: Optional[tuple] = None  # layers per stage (None: layers / num_stages each)
 
     @property
     def tokens_per_microbatch(self) -> int:
@@ -59,8 +60,13 @@ class ModelConfig:
     def c(self) -> pb_model_cfg:
         flags = ((PB_FLAG_TIMELINE if self.timeline else 0) | (PB_FLAG_SERIAL if self.serial else 0)
                  | (PB_FLAG_GEMM_TIMING if self.gemm_timing else 0))
-        return pb_model_cfg(self.layers, self.hidden, self.heads, self.seq, self.vocab, self.micro_batch, self.seed,
-                            self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, int(self.optimizer), flags)
+        sl = None
+        if self.stage_layers is not None:
+            sl = (C.c_int32 * len(self.stage_layers))(*self.stage_layers)
+        c = pb_model_cfg(self.layers, self.hidden, self.heads, self.seq, self.vocab, self.micro_batch, self.seed,
+                         self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, int(self.optimizer), flags, sl)
+        c._keep = sl  # the array must outlive the call that reads it
+        return c
 
     def params_per_layer(self) -> int:
         return 12 * self.hidden * self.hidden + 2 * self.hidden
@@ -281,6 +287,46 @@ class PipelineExecutor:
 
     def set(self, name: str, value) -> None:
         self.params()[name].set(name, value)
+
+
+def balanced_stage_layers(cfg: ModelConfig, topology: pb.Topology) -> tuple:
+    """Layers per stage that even out per-device work when the last stage also carries the
+    LM head (+ loss): head ~ V / (12h + 2s) layer-equivalents of F+B+W FLOPs (Megatron
+    counts, PAPER.md:575).  The reference cannot express per-stage durations (SPEC.md:352);
+    the paper deducts layers at the ends — this does the same, greedily:
+    move one layer from the most to the least loaded device while that lowers the
+    sum of squared device loads.  Every stage keeps >= 1 layer."""
+    S, d = topology.num_stages, topology.devices
+    head = cfg.vocab / (12.0 * cfg.hidden + 2.0 * cfg.seq)
+    L = [cfg.layers // S] * S
+    for i in range(cfg.layers - sum(L)):
+        L[i] += 1
+
+    def loads(L):
+        out = [0.0] * (d + 1)
+        for s in range(1, S + 1):
+            out[topology.device_of(s)] += L[s - 1] + (head if s == S else 0.0)
+        return out[1:]
+
+    def score(L):
+        return sum(x * x for x in loads(L))
+
+    for _ in range(4 * cfg.layers):
+        ld = loads(L)
+        hi, lo = ld.index(max(ld)) + 1, ld.index(min(ld)) + 1
+        src = [s for s in range(1, S + 1) if topology.device_of(s) == hi and L[s - 1] > 1]
+        dst = [s for s in range(1, S + 1) if topology.device_of(s) == lo]
+        if not src or not dst:
+            break
+        a = max(src, key=lambda s: (L[s - 1], s))
+        b = min(dst, key=lambda s: (L[s - 1], s))
+        cand = list(L)
+        cand[a - 1] -= 1
+        cand[b - 1] += 1
+        if score(cand) >= score(L) - 1e-9:
+            break
+        L = cand
+    return tuple(L)
 
 
 def synthetic_batch(cfg: ModelConfig, microbatches: int, seed: int = 1234):

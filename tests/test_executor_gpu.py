@@ -146,3 +146,26 @@ def test_isolate_mode_serialises_passes_and_matches(entry, p):
     rep = pb.replay(sched, [durs[(q.device, q.stage, q.kind, q.microbatch)] for q in sched.passes], 0.0)
     assert rep.makespan >= max(rep.busy) > 0
     assert 0.0 <= rep.bubble_rate < 1.0
+
+
+@pytest.mark.parametrize("entry,p,split", [("v-half", 2, (1, 3, 3, 1)), ("1f1b", 2, (3, 5)), ("v-zb", 4, (1, 1, 1, 1, 1, 1, 1, 1))])
+def test_uneven_stage_layers_match_oracle(entry, p, split):
+    import dataclasses
+    cfg = dataclasses.replace(CFG, stage_layers=split)
+    sched = pb.assemble(pb.build_entry(entry, p), M)
+    S = sched.topology.num_stages
+    ex = PipelineExecutor(cfg, sched)
+    tokens, labels = synthetic_batch(cfg, M)
+    res = ex.step(tokens, labels)
+    names = list(ex.params())
+    assert sorted(names) == sorted(N.shapes(cfg, S))
+    w = {n: torch.from_numpy(ex.get(n, "weight").reshape(N.shapes(cfg, S)[n])) for n in names}
+    loss_ref, grads_ref = N.reference_step(w, tokens, labels, cfg, S)
+    assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
+    for n in names:
+        g = ex.get(n, "grad")
+        r = grads_ref[n].numpy().ravel()
+        assert N.rel_l2(g, r) < GRAD_REL_L2, (n, N.rel_l2(g, r))
+    # same model as the even split: the loss does not depend on the partition
+    even = PipelineExecutor(CFG, pb.assemble(pb.build_entry("zb-h1", 1), M))
+    assert abs(even.step(tokens, labels).loss - res.loss) < 2e-3 * abs(res.loss)

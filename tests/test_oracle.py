@@ -60,3 +60,22 @@ def test_out_of_order_passes_rejected():
     tok, lab = batch(2)
     with pytest.raises(RuntimeError, match="before its"):
         N.schedule_step(make_params(4), tok, lab, CFG, bad, 4)
+
+
+def test_uneven_stage_layers_partition_invariance():
+    """Uneven split (fewer layers on the stages carrying embedding / head): same model, same numbers."""
+    cfg_u = SimpleNamespace(**vars(CFG), stage_layers=(1, 2, 1))
+    even = make_params(1)
+    pu = N.rename_for(even, CFG, 1, 3, cfg_to=cfg_u)
+    assert sorted(N.shapes(cfg_u, 3)) == sorted(pu)
+    tok, lab = batch(2)
+    l1, g1 = N.reference_step(even, tok, lab, CFG, 1)
+    lu, gu = N.reference_step(pu, tok, lab, cfg_u, 3)
+    assert abs(l1 - lu) < 1e-6 * abs(l1)
+    back = N.rename_for(gu, cfg_u, 3, 1)
+    for n in g1:
+        assert N.rel_l2(back[n], g1[n]) < 1e-5, n
+    g = pb.assemble(pb.build_entry("1f1b", 3), 3)
+    ls, gs = N.schedule_step(pu, tok[:1].repeat(3, 0), lab[:1].repeat(3, 0), cfg_u, g.passes, 3)
+    lr, gr = N.reference_step(pu, tok[:1].repeat(3, 0), lab[:1].repeat(3, 0), cfg_u, 3)
+    assert abs(ls - lr) < 1e-5 * abs(lr)

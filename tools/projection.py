@@ -28,6 +28,7 @@ pool bytes per device vs the exact_peak prediction and vs 1F1B.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -44,12 +45,13 @@ def main():
     ap.add_argument("--model", default="1.5b", choices=sorted(CONFIGS))
     ap.add_argument("--p", type=int, nargs="+", default=[8])
     ap.add_argument("--microbatches", type=int, default=32)
-    ap.add_argument("--micro-batch", type=int, default=1)
+    ap.add_argument("--micro-batch", type=int, default=2)
     ap.add_argument("--schedules", nargs="+", default=["1f1b", "zb-h1", "v-min", "v-half", "v-zb"])
     ap.add_argument("--nvlink-gbs", type=float, default=720.0, help="assumed achieved P2P GB/s per direction")
     ap.add_argument("--latency-us", type=float, default=8.0, help="assumed per-transfer latency")
     ap.add_argument("--out", default=None)
     ap.add_argument("--via-chunks", action="store_true", help="probe-pipeline projection (see module doc)")
+    ap.add_argument("--balance", action="store_true", help="balanced_stage_layers (LM-head stage carries fewer layers)")
     args = ap.parse_args()
 
     import torch
@@ -80,7 +82,11 @@ def main():
                                                                   "bubble_rate", "max_pool_gib")}), file=sys.stderr)
                 continue
             sched = pb.assemble(pb.build_entry(name, p), m)
-            ex = PipelineExecutor(cfg, sched, [0] * p)
+            rcfg = cfg
+            if args.balance:
+                from paper_2405_15362_b200.executor import balanced_stage_layers
+                rcfg = dataclasses.replace(cfg, stage_layers=balanced_stage_layers(cfg, sched.topology))
+            ex = PipelineExecutor(rcfg, sched, [0] * p)
             ex.set_flags(timeline=True, isolate=True)
             ex.step(tok, lab, on_host=False)                  # warm-up
             res = ex.step(tok, lab, on_host=False)
@@ -95,6 +101,7 @@ def main():
             pool = [res.per_device[d].pool_bytes for d in sorted(res.per_device)]
             slots = [res.per_device[d].pool_slots for d in sorted(res.per_device)]
             run = {"schedule": name, "p": p, "loss": res.loss,
+                   "stage_layers": list(rcfg.stage_layers) if rcfg.stage_layers else None,
                    "projected_ms_per_step": rep.makespan, "projected_tokens_per_s": m * T / (rep.makespan / 1e3),
                    "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
                    "pipeline_roofline_frac": max(rep.busy) / rep.makespan,
@@ -105,7 +112,9 @@ def main():
             out["runs"].append(run)
             print(json.dumps({k: run[k] for k in ("schedule", "p", "projected_tokens_per_s", "bubble_rate",
                                                   "pipeline_roofline_frac", "max_pool_gib")}), file=sys.stderr)
-            del ex
+            del ex, res
+            import gc
+            gc.collect()
             torch.cuda.synchronize()
     if args.via_chunks:
         out["method"] = ("probe pipeline with the target's chunk shapes on one B200 (PB_FLAG_ISOLATE pass times, "
