@@ -1,9 +1,10 @@
-"""One launch of each hot kernel at GPT-1.5B / seq 2048 / mbs 1 pass shapes (for ncu captures)."""
+"""One launch of each hot kernel at GPT-1.5B / seq 2048 / micro-batch 2 pass shapes (T=4096; for ncu captures)."""
 import torch
 
 from tests import kernels as K
 
-T, h, H = 2048, 2048, 16
+B_, S_, h, H = 2, 2048, 2048, 16
+T = B_ * S_
 torch.manual_seed(0)
 A = torch.randn(T, h, device="cuda").bfloat16()
 W1 = torch.randn(4 * h, h, device="cuda").bfloat16()
@@ -16,8 +17,8 @@ K.gemm(dY, W2t, U, b_mn=True, epi=3, aux=U)                     # B: dgl * gelu'
 dW = torch.zeros(h, 4 * h, device="cuda")
 K.gemm(dY, G, dW, a_mn=True, b_mn=True, epi=4, accumulate=1)   # W: dW2 += dY^T gelu(u)
 qkv = torch.randn(T, 3 * h, device="cuda").bfloat16()
-out, lse2 = K.attn_fwd_tc(qkv, 1, T, H)
+out, lse2 = K.attn_fwd_tc(qkv, B_, S_, H)
 dout = torch.randn_like(out)
-K.attn_bwd_tc(qkv, out, dout, lse2, 1, T, H)
+K.attn_bwd_tc(qkv, out, dout, lse2, B_, S_, H)
 torch.cuda.synchronize()
 print("ok")
