@@ -190,15 +190,21 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&s_free[st]);
-            float mx = -INFINITY;
+            // one warp per SM sub-partition runs this: keep the reductions as 8 independent
+            // chains (a single 128-long chain would be latency-bound), scale folded into the exp
+            float mx8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
             const bool diag = (j == nkv - 1);
 #pragma unroll
             for (int c = 0; c < 128; ++c) {
-                float v = s[c] * sl2;
+                float v = s[c];
                 if (diag && c > r) v = -INFINITY;
                 s[c] = v;
-                mx = fmaxf(mx, v);
+                mx8[c & 7] = fmaxf(mx8[c & 7], v);
             }
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
             const float m_new = fmaxf(m_used, mx);
             bool rescale = (j > 0) && (m_new > m_used + 8.f);
             const bool any_rescale = __any_sync(0xffffffff, rescale);
@@ -228,20 +234,20 @@ __global__ void __launch_bounds__(192, 1)
                 }
             }
             if (j == 0) m_used = m_new;
-            float rs = 0.f;
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int c8 = 0; c8 < 16; ++c8) {
                 float p[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    p[e] = exp2f(s[c8 * 8 + e] - m_used);
-                    rs += p[e];
+                    p[e] = fast_exp2(fmaf(s[c8 * 8 + e], sl2, -m_used));
+                    rs8[e] += p[e];
                 }
                 uint4 w = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
                                      pack_bf16(p[6], p[7]));
                 *reinterpret_cast<uint4*>(sp + sw128(r, c8 * 8)) = w;
             }
-            l += rs;
+            l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     const int ql = c * 32 + e;
-                    float v = exp2f(sv[e] * sl2 - Lb[ql]);
+                    float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
                     if (diag && key > qb * BQ + ql) v = 0.f;
                     p[e] = v;
                     ds[e] = v * (dp[e] - Lb[128 + ql]);
@@ -719,7 +725,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int u = 0; u < 2; ++u) {
                     const int e = 2 * e2 + u;
                     const int ql = hf * 64 + e;
-                    float v = exp2f(sv[e] * sl2 - Lb[ql]);
+                    float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
                     if (diag && key > qb * BQ + ql) v = 0.f;
                     pv[u] = v;
                     dsv[u] = v * (dp[e] - Lb[128 + ql]);

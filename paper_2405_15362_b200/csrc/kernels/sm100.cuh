@@ -223,6 +223,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a
            | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// 2^x on the SFU without exp2f's range-fixup instructions (x <= 0 after max subtraction, so
+// flushing denormal results to zero is harmless for bf16 probabilities)
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {

@@ -169,3 +169,9 @@ def test_uneven_stage_layers_match_oracle(entry, p, split):
     # same model as the even split: the loss does not depend on the partition
     even = PipelineExecutor(CFG, pb.assemble(pb.build_entry("zb-h1", 1), M))
     assert abs(even.step(tokens, labels).loss - res.loss) < 2e-3 * abs(res.loss)
+
+
+def test_unfolded_gamma_path_matches_oracle(monkeypatch):
+    """PB_NO_FOLD=1: per-microbatch gamma reductions instead of the folded projection weights."""
+    monkeypatch.setenv("PB_NO_FOLD", "1")
+    test_step_matches_oracle("v-half", 2)
