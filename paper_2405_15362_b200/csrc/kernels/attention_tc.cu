@@ -817,6 +817,243 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
+
+// ------------------------------------------------------------------ forward v2 (two Q tiles per CTA)
+// One CTA per (256 queries = tiles A and B, head, sequence); 320 threads:
+//   warp 0     TMA: Q_A, Q_B once, then a 2-stage ring of K/V tiles shared by both Q tiles
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer, ping-ponging the two tiles:
+//                S_A(j) S_B(j) | PV_A(j) S_A(j+1) | PV_B(j) S_B(j+1) | ...
+//   warps 2-5  softmax of tile A, warps 6-9 softmax of tile B (thread = query row = TMEM lane)
+// TMEM: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).  P (bf16) is written back over
+// the consumed S columns and read by the PV MMA as its A operand straight from TMEM, so smem only
+// holds Q_A, Q_B and the K/V ring.  While one tile's softmax runs, the tensor pipe works on the
+// other tile.  The MMA pipe executes in issue order, so when S_X(j) is complete PV_X(j-1) is too:
+// the lazy O rescale needs no extra wait.
+struct Fwd2Smem {
+    static constexpr int qa = 0;
+    static constexpr int qb = kTile;
+    static constexpr int k0 = 2 * kTile;             // [2]
+    static constexpr int v0 = k0 + kStages * kTile;  // [2]
+    static constexpr int bars = v0 + kStages * kTile;
+    static constexpr int total = bars + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
+                        float* __restrict__ lse2, int seq, int H, int T, float scale) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd2Smem::bars);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;   // [2]
+    uint64_t* kv_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;    // [2] per tile
+    uint64_t* p_full = bars + 7;    // [2] per tile (4 softmax warps)
+    uint64_t* o_full = bars + 9;    // [2] per tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+
+    const uint32_t warp = warp_id();
+    const int npair = seq / (2 * BQ);
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int c = npair - 1 - int(blockIdx.x) / (H * (T / seq));  // heaviest pair of tiles first (LPT)
+    const int head = hb % H, b = hb / H;
+    const int row0 = b * seq + c * 2 * BQ;  // first query row of tile A
+    const int nA = 2 * c + 1, nB = 2 * c + 2;  // causal key tiles of A and B
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&o_full[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const int cq = head * D, ck = H * D + head * D, cv = 2 * H * D + head * D;
+            mbar_expect_tx(q_full, 2 * kTile);
+            tma_load_2d(sm + Fwd2Smem::qa, &tm, q_full, cq, row0);
+            tma_load_2d(sm + Fwd2Smem::qa + 16384, &tm, q_full, cq + 64, row0);
+            tma_load_2d(sm + Fwd2Smem::qb, &tm, q_full, cq, row0 + BQ);
+            tma_load_2d(sm + Fwd2Smem::qb + 16384, &tm, q_full, cq + 64, row0 + BQ);
+            for (int j = 0; j < nB; ++j) {
+                const int st = j & 1;
+                if (j >= kStages) mbar_wait(&kv_empty[st], ((j - kStages) >> 1) & 1);
+                mbar_expect_tx(&kv_full[st], 2 * kTile);
+                const int kr = b * seq + j * BK;
+                uint8_t* ks = sm + Fwd2Smem::k0 + st * kTile;
+                uint8_t* vs = sm + Fwd2Smem::v0 + st * kTile;
+                tma_load_2d(ks, &tm, &kv_full[st], ck, kr);
+                tma_load_2d(ks + 16384, &tm, &kv_full[st], ck + 64, kr);
+                tma_load_2d(vs, &tm, &kv_full[st], cv, kr);
+                tma_load_2d(vs + 16384, &tm, &kv_full[st], cv + 64, kr);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t idesc_o = idesc_bf16(128, 128, false, true);
+        mbar_wait(q_full, 0);
+        auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T -> TMEM [t*128, +128)
+            mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t sq = smem_u32(sm + (t ? Fwd2Smem::qb : Fwd2Smem::qa));
+                const uint32_t sk = smem_u32(sm + Fwd2Smem::k0 + (j & 1) * kTile);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + t * 128, sdesc(sq + o, 16, 1024), sdesc(sk + o, 16, 1024), idesc_s, kk != 0);
+                }
+                tc_commit(&s_full[t]);
+            }
+            __syncwarp();
+        };
+        auto issue_pv = [&](int t, int j, bool release_kv) {  // O_t += P_t(j) V_j, P from TMEM
+            mbar_wait(&p_full[t], j & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t sv = smem_u32(sm + Fwd2Smem::v0 + (j & 1) * kTile);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc(sv + kk * 2048, 16384, 1024),
+                              idesc_o, (j | kk) != 0);
+                if (release_kv) tc_commit(&kv_empty[j & 1]);
+            }
+            __syncwarp();
+        };
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j < nB; ++j) {
+            if (j < nA) {
+                issue_pv(0, j, false);
+                if (j + 1 < nA) issue_s(0, j + 1);
+            }
+            issue_pv(1, j, true);  // tile B reads every K/V tile last
+            if (j + 1 < nB) issue_s(1, j + 1);
+        }
+        if (elect_one()) {
+            tc_commit(&o_full[0]);
+            tc_commit(&o_full[1]);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ softmax (tile t)
+        const int t = int(warp - 2) >> 2;
+        const uint32_t q4 = warp & 3;
+        const int r = int(q4 * 32 + lane_id());
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const uint32_t ts = tmem + lane_base + t * 128;      // S_t / P_t
+        const uint32_t to = tmem + lane_base + 256 + t * 128;  // O_t
+        const int nkv = t ? nB : nA;
+        const float sl2 = scale * kLog2e;
+        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            mbar_wait(&s_full[t], j & 1);  // S_t(j) done, and with it PV_t(j-1): O_t stable
+            tc_fence_after();
+            // two passes over S_t (TMEM reads are cheap, registers are not: 10 warps leave 168 per
+            // thread): row max over all 128 columns, then exp / pack per 64-column half
+            float mx8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+            const bool diag = (j == nkv - 1);
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                float v[32];
+                tmem_ld32(ts + cc * 32, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const float x = (diag && cc * 32 + e > r) ? -INFINITY : v[e];
+                    mx8[e & 7] = fmaxf(mx8[e & 7], x);
+                }
+            }
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+            const float m_new = fmaxf(m_used, mx);
+            const bool rescale = (j > 0) && (m_new > m_used + 8.f);
+            if (__any_sync(0xffffffff, rescale)) {
+                const float f = rescale ? exp2f(m_used - m_new) : 1.f;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    float o[32];
+                    tmem_ld32(to + cc * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(to + cc * 32, o);
+                }
+                if (rescale) {
+                    l *= f;
+                    m_used = m_new;
+                }
+            }
+            if (j == 0) m_used = m_new;
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                float sv[64];
+                tmem_ld32(ts + h2 * 64, *reinterpret_cast<float(*)[32]>(&sv[0]));
+                tmem_ld32(ts + h2 * 64 + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
+                tmem_ld_wait();
+                uint32_t pk[32];
+#pragma unroll
+                for (int e2 = 0; e2 < 32; ++e2) {
+                    const int c0 = h2 * 64 + 2 * e2;
+                    const float x0 = (diag && c0 > r) ? -INFINITY : sv[2 * e2];
+                    const float x1 = (diag && c0 + 1 > r) ? -INFINITY : sv[2 * e2 + 1];
+                    const float p0 = fast_exp2(fmaf(x0, sl2, -m_used));
+                    const float p1 = fast_exp2(fmaf(x1, sl2, -m_used));
+                    rs8[(2 * e2) & 7] += p0;
+                    rs8[(2 * e2 + 1) & 7] += p1;
+                    pk[e2] = pack_bf16(p0, p1);
+                }
+                // P_t bf16 pairs over S_t columns [h2*32, +32): S columns already consumed
+                tmem_st32u(ts + h2 * 32, pk);
+            }
+            l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&p_full[t]);
+        }
+        mbar_wait(&o_full[t], 0);
+        tc_fence_after();
+        const float inv = 1.f / l;
+        const int qrow = row0 + t * BQ + r;
+        __nv_bfloat16* orow = out + size_t(qrow) * (H * D) + head * D;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            float o[32];
+            tmem_ld32(to + cc * 32, o);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                                    pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+        }
+        lse2[size_t(head) * T + qrow] = m_used + log2f(l);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<512>(tmem);
+    }
+}
+
 }  // namespace
 
 void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
@@ -853,14 +1090,28 @@ void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int 
     if (seq % 128) throw std::invalid_argument("attention: seq must be a multiple of 128");
     static bool once = [] {
         cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::total);
+        cudaFuncSetAttribute(attn_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::total);
         return true;
     }();
     (void)once;
     const int T = batch * seq;
     const CUtensorMap tm = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
-    dim3 grid(seq / BQ * heads * batch);
-    launch_k(attn_fwd_tc_kernel, grid, dim3(192), FwdSmem::total, s, 1, tm, out, lse2, seq, heads, T,
-             0.08838834764831845f);
+    // PB_ATTN_FWD=2: the two-Q-tile ping-pong kernel (P in TMEM).  Correct (tested) but measured
+    // slower than the single-tile kernel (467 vs 556 TFLOP/s at 2 x 2048 x 16 heads): its
+    // softmax -> PV -> S chain per tile is longer than the double-buffered S/P overlap of v1.
+    static const bool v2 = [] {
+        const char* e = std::getenv("PB_ATTN_FWD");
+        return e && e[0] == '2';
+    }();
+    if (!v2 || seq % (2 * BQ)) {
+        dim3 grid(seq / BQ * heads * batch);
+        launch_k(attn_fwd_tc_kernel, grid, dim3(192), FwdSmem::total, s, 1, tm, out, lse2, seq, heads, T,
+                 0.08838834764831845f);
+    } else {
+        dim3 grid(seq / (2 * BQ) * heads * batch);
+        launch_k(attn_fwd_tc2_kernel, grid, dim3(320), Fwd2Smem::total, s, 1, tm, out, lse2, seq, heads, T,
+                 0.08838834764831845f);
+    }
 }
 
 }  // namespace pbk
