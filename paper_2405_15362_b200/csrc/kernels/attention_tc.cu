@@ -8,8 +8,9 @@
 //   warps 2-5  softmax: thread = query row = TMEM lane; reads its S row with
 //              tcgen05.ld, online softmax in registers (no shuffles), writes P
 //              (bf16, 128B-swizzled K-major) to smem for the PV MMA.
-// S_{j+1} is computed while the softmax of S_j runs (two S buffers), and P is
-// double-buffered in smem so the softmax of tile j overlaps PV_{j-1}.  The
+// S_{j+1} is computed while the softmax of S_j runs (two S buffers).  P goes back to TMEM
+// (bf16 pairs, two buffers) and feeds the PV MMA as its A operand, so the softmax of tile j
+// overlaps PV_{j-1} and smem holds only Q and a 3-stage K/V ring.  The
 // running max is rescaled lazily: O (in TMEM) is only rescaled when a row's
 // max grows by more than 2^8, which keeps the result exact (O and the row sum
 // share the same stale max) and avoids a TMEM round trip per tile.
@@ -30,14 +31,15 @@ constexpr int kTile = BQ * D * 2;  // 32 KB: two 128B-swizzled atoms of [128 row
 constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
+constexpr int kFwdStages = 3;  // K/V ring depth of the forward kernel
 struct FwdSmem {
     static constexpr int q = 0;
-    static constexpr int k0 = kTile;
-    static constexpr int v0 = k0 + kStages * kTile;
-    static constexpr int p = v0 + kStages * kTile;  // [2] P buffers
-    static constexpr int bars = p + 2 * kTile;
+    static constexpr int k0 = kTile;                       // [3]
+    static constexpr int v0 = k0 + kFwdStages * kTile;     // [3]
+    static constexpr int bars = v0 + kFwdStages * kTile;
     static constexpr int total = bars + 256 + 1024;
 };
+static_assert(FwdSmem::total <= 232448, "attn fwd: shared memory over the sm_100 opt-in limit");
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
     const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
@@ -58,6 +60,25 @@ __device__ __forceinline__ uint32_t sw128(int row, int col) {
     return uint32_t((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2);
 }
 
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
 __global__ void __launch_bounds__(192, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ lse2, int seq, int H, int T, float scale) {
@@ -65,14 +86,14 @@ __global__ void __launch_bounds__(192, 1)
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::bars);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* s_free = bars + 7;    // [2]
-    uint64_t* p_full = bars + 9;    // [2]
-    uint64_t* p_empty = bars + 11;  // [2]
-    uint64_t* o_full = bars + 13;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* kv_full = bars + 1;   // [3]
+    uint64_t* kv_empty = bars + 4;  // [3]
+    uint64_t* s_full = bars + 7;    // [2]
+    uint64_t* s_free = bars + 9;    // [2]
+    uint64_t* p_full = bars + 11;   // [2]
+    uint64_t* p_empty = bars + 13;  // [2]
+    uint64_t* o_full = bars + 15;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
     const uint32_t warp = warp_id();
     const int nqb = seq / BQ;
@@ -86,9 +107,11 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 0 && elect_one()) {
         tma_prefetch(&tm);
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kFwdStages; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&s_free[i], 4);
         }
@@ -103,7 +126,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;  // cols [0,128) S0, [128,256) S1, [256,384) O
+    const uint32_t tmem = *tmem_slot;  // cols [0,128) S0, [128,256) S1, [256,384) O, [384,448) P0, [448,512) P1
     pdl_wait();
     pdl_launch();
 
@@ -114,8 +137,8 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_2d(sm + FwdSmem::q, &tm, q_full, cq, row0);
             tma_load_2d(sm + FwdSmem::q + 16384, &tm, q_full, cq + 64, row0);
             for (int j = 0; j < nkv; ++j) {
-                const int st = j & 1;
-                if (j >= kStages) mbar_wait(&kv_empty[st], ((j - kStages) >> 1) & 1);
+                const int st = j % kFwdStages;
+                if (j >= kFwdStages) mbar_wait(&kv_empty[st], ((j - kFwdStages) / kFwdStages) & 1);
                 mbar_expect_tx(&kv_full[st], 2 * kTile);
                 const int kr = b * seq + j * BK;
                 uint8_t* ks = sm + FwdSmem::k0 + st * kTile;
@@ -130,33 +153,31 @@ __global__ void __launch_bounds__(192, 1)
         constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
         constexpr uint32_t idesc_o = idesc_bf16(128, 128, false, true);
         const uint32_t sq = smem_u32(sm + FwdSmem::q);
-        const uint32_t sp = smem_u32(sm + FwdSmem::p);
         mbar_wait(q_full, 0);
-        auto issue_pv = [&](int j) {  // O += P_j V_j
+        auto issue_pv = [&](int j) {  // O += P_j V_j, P from TMEM
             const int pb = j & 1;
+            const int kv = j % kFwdStages;
             mbar_wait(&p_full[pb], (j >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t sv = smem_u32(sm + FwdSmem::v0 + (j & 1) * kTile);
-                const uint32_t spj = sp + pb * kTile;
+                const uint32_t sv = smem_u32(sm + FwdSmem::v0 + kv * kTile);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = sdesc(spj + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-                    const uint64_t bd = sdesc(sv + kk * 2048, 16384, 1024);
-                    tc_mma(tmem + 256, ad, bd, idesc_o, (j | kk) != 0);
-                }
-                tc_commit(&kv_empty[j & 1]);
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 256, tmem + 384 + pb * 64 + kk * 8, sdesc(sv + kk * 2048, 16384, 1024), idesc_o,
+                              (j | kk) != 0);
+                tc_commit(&kv_empty[kv]);
                 tc_commit(&p_empty[pb]);
             }
             __syncwarp();
         };
         for (int j = 0; j < nkv; ++j) {
             const int st = j & 1;
-            mbar_wait(&kv_full[st], (j >> 1) & 1);
+            const int kv = j % kFwdStages;
+            mbar_wait(&kv_full[kv], (j / kFwdStages) & 1);
             if (j >= 2) mbar_wait(&s_free[st], ((j - 2) >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t sk = smem_u32(sm + FwdSmem::k0 + st * kTile);
+                const uint32_t sk = smem_u32(sm + FwdSmem::k0 + kv * kTile);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t ad = sdesc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
@@ -179,7 +200,6 @@ __global__ void __launch_bounds__(192, 1)
         const float sl2 = scale * kLog2e;
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < nkv; ++j) {
-            uint8_t* sp = sm + FwdSmem::p + (j & 1) * kTile;
             const int st = j & 1;
             mbar_wait(&s_full[st], (j >> 1) & 1);
             tc_fence_after();
@@ -236,19 +256,21 @@ __global__ void __launch_bounds__(192, 1)
             if (j == 0) m_used = m_new;
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c8 = 0; c8 < 16; ++c8) {
-                float p[8];
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t pk[32];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    p[e] = fast_exp2(fmaf(s[c8 * 8 + e], sl2, -m_used));
-                    rs8[e] += p[e];
+                for (int e2 = 0; e2 < 32; ++e2) {
+                    const int c = h2 * 64 + 2 * e2;
+                    const float p0 = fast_exp2(fmaf(s[c], sl2, -m_used));
+                    const float p1 = fast_exp2(fmaf(s[c + 1], sl2, -m_used));
+                    rs8[(2 * e2) & 7] += p0;
+                    rs8[(2 * e2 + 1) & 7] += p1;
+                    pk[e2] = pack_bf16(p0, p1);
                 }
-                uint4 w = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
-                                     pack_bf16(p[6], p[7]));
-                *reinterpret_cast<uint4*>(sp + sw128(r, c8 * 8)) = w;
+                tmem_st32u(tmem + lane_base + 384 + (j & 1) * 64 + h2 * 32, pk);
             }
             l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-            fence_async_smem();
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&p_full[j & 1]);
@@ -555,23 +577,6 @@ struct Bwd3Smem {
 };
 static_assert(Bwd3Smem::total <= 232448, "attn bwd v3: shared memory over the sm_100 opt-in limit");
 
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
