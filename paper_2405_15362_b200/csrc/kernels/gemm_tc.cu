@@ -336,8 +336,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } while (e != p.sk_epoch);
                 }
             }
+            // residual / pre-activation operand of the next 32 columns is loaded one chunk ahead
+            // (each element is read and written by the same thread, so C may alias aux)
+            constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_DGELU;
+            uint4 aux_next[4];
+            if constexpr (kAux) {
+                const uint4* s4 = reinterpret_cast<const uint4*>(p.aux + size_t(row) * p.ldaux + n0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) aux_next[j] = s4[j];
+            }
 #pragma unroll 1
             for (int c = 0; c < BN; c += 32) {
+                uint4 aux_cur[4];
+                if constexpr (kAux) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) aux_cur[j] = aux_next[j];
+                    if (c + 32 < BN) {
+                        const uint4* s4 = reinterpret_cast<const uint4*>(p.aux + size_t(row) * p.ldaux + n0 + c + 32);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) aux_next[j] = s4[j];
+                    }
+                }
                 float v[32];
                 tmem_ld32(tbase + c, v);
                 tmem_ld_wait();
@@ -367,11 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                     }
                 } else {
-                    if constexpr (EPI == EPI_RESID || EPI == EPI_DGELU) {
-                        const uint4* s4 = reinterpret_cast<const uint4*>(p.aux + size_t(row) * p.ldaux + col);
+                    if constexpr (kAux) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
-                            uint4 a = s4[j];
+                            uint4 a = aux_cur[j];
                             uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
