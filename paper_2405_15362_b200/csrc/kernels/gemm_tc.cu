@@ -80,7 +80,7 @@ template <int BN, int CG>
 __device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int t,
                                                 int& cursor) {
     if (p.group == nullptr) {
-        const int num_m = p.M / (BM * CG);
+        const int num_m = (p.M + BM * CG - 1) / (BM * CG);  // the last M / N tile may be half empty
         return TileRef{ta, tb, p.C, t % num_m, t / num_m, p.K / BK, p.ldc};
     }
     while (t >= p.group[cursor].tile0 + p.group[cursor].ntiles) ++cursor;  // tiles visited in increasing order
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = warp_id();
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
-    const int num_tiles = p.group ? p.total_tiles : (p.M / (BM * CG)) * (p.N / BN);
+    const int num_tiles = p.group ? p.total_tiles : ((p.M + BM * CG - 1) / (BM * CG)) * ((p.N + BN - 1) / BN);
     const int cid = int(blockIdx.x) / CG, ncl = int(gridDim.x) / CG;
 
     if (warp == 0 && elect_one()) {
@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (each element is read and written by the same thread, so C may alias aux)
             constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_DGELU;
             uint4 aux_next[4];
+            // (aux epilogues run only on full tiles: layer GEMMs have M = tokens, N = h or 4h)
             if constexpr (kAux) {
                 const uint4* s4 = reinterpret_cast<const uint4*>(p.aux + size_t(row) * p.ldaux + n0);
 #pragma unroll
@@ -370,6 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 const int col = n0 + c;
+                // partial last tile (M or N = 128 mod 256): nothing to store outside the matrix
+                if (!(p.group || (row < p.M && col < p.N))) continue;
                 if constexpr (EPI == EPI_F32) {
                     float* dst = reinterpret_cast<float*>(Cout) + size_t(row) * ldc + col;
                     float4* d4 = reinterpret_cast<float4*>(dst);
@@ -544,7 +547,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
                nullptr, nullptr, 0, 0};
-    const int tiles = (g.M / (BM * CG)) * (g.N / BN);
+    const int tiles = ((g.M + BM * CG - 1) / (BM * CG)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
     int grid = (tiles < slots ? tiles : slots) * CG;
     // stream-K when whole tiles would leave a ragged last wave (and a k split is possible)
@@ -672,7 +675,10 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M % BM || g.N % 128 || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
         throw std::invalid_argument("gemm: M%128, N%128, K%64 must be 0 (M=" + std::to_string(g.M) +
                                     " N=" + std::to_string(g.N) + " K=" + std::to_string(g.K) + ")");
-    const bool pair_ok = g.M % 256 == 0 && g.N % 256 == 0;
+    // CTA pairs also take M or N = 128 (mod 256) (e.g. the LM head, V = 50304): TMA zero-fills
+    // the empty half of the last tile and the epilogue skips its rows / columns
+    const bool full = g.M % 256 == 0 && g.N % 256 == 0;
+    const bool pair_ok = full || (g.M >= 256 && g.N >= 256 && g.epi != EPI_RESID && g.epi != EPI_DGELU);
     const int cg = g_force_cg > 0 ? (pair_ok ? g_force_cg : 1) : (pair_ok ? 2 : 1);
     if (cg == 2)
         dispatch<256, 2>(g, s);

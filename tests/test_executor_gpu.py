@@ -175,3 +175,19 @@ def test_unfolded_gamma_path_matches_oracle(monkeypatch):
     """PB_NO_FOLD=1: per-microbatch gamma reductions instead of the folded projection weights."""
     monkeypatch.setenv("PB_NO_FOLD", "1")
     test_step_matches_oracle("v-half", 2)
+
+
+def test_vocab_half_tile_matches_oracle():
+    """vocab = 128 (mod 256): the LM-head GEMMs run on CTA pairs with a half-empty last tile."""
+    import dataclasses
+    cfg = dataclasses.replace(CFG, vocab=1152)
+    sched = pb.assemble(pb.build_entry("v-half", 2), M)
+    ex = PipelineExecutor(cfg, sched)
+    tokens, labels = synthetic_batch(cfg, M)
+    res = ex.step(tokens, labels)
+    S = sched.topology.num_stages
+    w = {n: torch.from_numpy(ex.get(n, "weight").reshape(N.shapes(cfg, S)[n])) for n in ex.params()}
+    loss_ref, grads_ref = N.reference_step(w, tokens, labels, cfg, S)
+    assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
+    for n in ex.params():
+        assert N.rel_l2(ex.get(n, "grad"), grads_ref[n].numpy().ravel()) < GRAD_REL_L2, n

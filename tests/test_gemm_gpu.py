@@ -141,3 +141,22 @@ def test_stream_k_epilogues(M, N, Kd, stream_k):
     K.gemm(A, W, u2, epi=1, C2=gg)
     torch.cuda.synchronize()
     assert torch.equal(u, u2)
+
+
+@pytest.mark.parametrize("M,N,Kd", [(4096, 50304, 256), (640, 896, 128)])
+def test_half_empty_last_tile(M, N, Kd):
+    """M or N = 128 (mod 256) on CTA pairs (the LM head: V = 50304): zero-filled loads, skipped stores."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16()
+    guard = torch.full((M + 256, N + 256), 7.0, device="cuda", dtype=torch.bfloat16)
+    C = guard[:M, :N]
+    K.gemm(A, W, C)
+    Wt = torch.randn(Kd, M, device="cuda", generator=g).bfloat16()
+    X = torch.randn(Kd, N, device="cuda", generator=g).bfloat16()
+    D = torch.zeros(M, N, device="cuda")
+    K.gemm(Wt, X, D, a_mn=True, b_mn=True, epi=4, accumulate=1)
+    torch.cuda.synchronize()
+    assert rel(C, A.float() @ W.float().t()) < 4e-3
+    assert (guard[M:, :] == 7.0).all() and (guard[:, N:] == 7.0).all()  # nothing written outside
+    assert rel(D, Wt.float().t() @ X.float()) < 1e-4 * max(1.0, Kd / 64)
