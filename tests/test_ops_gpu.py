@@ -81,9 +81,10 @@ def test_attention_backward_tcgen05(batch, seq, heads):
         assert rel(dqkv[:, sl], gx[:, sl]) < 2e-2, (name, rel(dqkv[:, sl], gx[:, sl]))
 
 
-def test_rmsnorm_forward_backward():
+@pytest.mark.parametrize("h", [1024, 2048, 4096])
+def test_rmsnorm_forward_backward(h):
     g = torch.Generator(device="cuda").manual_seed(5)
-    T, h = 300, 1024
+    T = 300  # not a multiple of the 8 rows per CTA
     x = torch.randn(T, h, device="cuda", generator=g).bfloat16()
     gam = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).bfloat16()
     y, rstd = K.rmsnorm_fwd(x, gam)
@@ -172,3 +173,19 @@ def test_attention_forward_tcgen05_rescales():
     assert rel(out, ref) < 1e-2
     got_lse = (lse2 * math.log(2)).view(heads, batch, seq).permute(1, 0, 2)
     assert ((got_lse - lse).abs() / lse.abs().clamp_min(1)).max().item() < 1e-2
+
+
+@pytest.mark.parametrize("h", [1024, 2048])
+def test_rmsnorm_unit_gamma(h):
+    """g = NULL (gamma folded into the next projection) equals g = 1."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    T = 77
+    x = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    ones = torch.ones(h, device="cuda", dtype=torch.bfloat16)
+    y1, r1 = K.rmsnorm_fwd(x, ones)
+    y0, r0 = K.rmsnorm_fwd(x, None)
+    dy = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    d1 = K.rmsnorm_bwd(dy, x, ones, r1)
+    d0 = K.rmsnorm_bwd(dy, x, None, r0)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1) and torch.equal(r0, r1) and torch.equal(d0, d1)
