@@ -79,3 +79,20 @@ def test_uneven_stage_layers_partition_invariance():
     ls, gs = N.schedule_step(pu, tok[:1].repeat(3, 0), lab[:1].repeat(3, 0), cfg_u, g.passes, 3)
     lr, gr = N.reference_step(pu, tok[:1].repeat(3, 0), lab[:1].repeat(3, 0), cfg_u, 3)
     assert abs(ls - lr) < 1e-5 * abs(lr)
+
+
+def test_balanced_stage_layers():
+    """The LM-head stage sheds layers until per-device work (layers + head ~ V/(12h+2s)) evens out."""
+    from paper_2405_15362_b200.executor import ModelConfig, balanced_stage_layers
+    cfg = ModelConfig(layers=32, hidden=2048, heads=16, seq=2048, vocab=50304)
+    v8 = pb.assemble(pb.build_entry("v-half", 8), 16).topology
+    L = balanced_stage_layers(cfg, v8)
+    assert sum(L) == 32 and min(L) >= 1 and len(L) == 16
+    head = cfg.vocab / (12 * cfg.hidden + 2 * cfg.seq)
+    load = [0.0] * 8
+    for s in range(1, 17):
+        load[v8.device_of(s) - 1] += L[s - 1] + (head if s == 16 else 0)
+    assert max(load) <= 5.0 + 1e-9            # even split: device 1 carries 4 + 1.75
+    assert balanced_stage_layers(cfg, pb.assemble(pb.build_entry("1f1b", 8), 8).topology)[-1] < 4
+    big = ModelConfig(layers=32, hidden=6144, heads=48, seq=6144, vocab=50304)  # head < 1 layer: unchanged
+    assert balanced_stage_layers(big, v8) == (2,) * 16
