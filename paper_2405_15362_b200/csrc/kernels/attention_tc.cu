@@ -14,6 +14,7 @@
 // running max is rescaled lazily: O (in TMEM) is only rescaled when a row's
 // max grows by more than 2^8, which keeps the result exact (O and the row sum
 // share the same stale max) and avoids a TMEM round trip per tile.
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -578,6 +579,13 @@ struct Bwd3Smem {
 static_assert(Bwd3Smem::total <= 232448, "attn bwd v3: shared memory over the sm_100 opt-in limit");
 
 
+// PB_ATTN_TRACE=1: clock64 stamps of block 0's phases (tests/trace_attn_bwd.py); null otherwise
+__device__ unsigned long long* g_attn_trace = nullptr;
+#define ATRACE(i, ev)                                                                        \
+    do {                                                                                     \
+        if (g_attn_trace && blockIdx.x == 0 && (i) < 32) g_attn_trace[(i) * 16 + (ev)] = clock64(); \
+    } while (0)
+
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                         const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2, const float* __restrict__ dsum,
@@ -594,7 +602,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* dq_full = bars + 7;
     uint64_t* s_free = bars + 8;     // 8 compute warps
     uint64_t* dkv_full = bars + 9;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* dq_staged = bars + 10;  // 8 compute warps: this tile's dQ sits in the staging buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
     float* sL = reinterpret_cast<float*>(sm + Bwd3Smem::lse);
 
     const uint32_t warp = warp_id();
@@ -609,7 +618,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_prefetch(&tm_qkv);
         tma_prefetch(&tm_do);
         tma_prefetch(&tm_dq);
-        for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 8 : 1);
+        for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 6 || i == 8 || i == 10) ? 8 : 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -621,7 +630,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     pdl_launch();
 
     if (warp == 0) {
-        if (elect_one()) {
+        if (lane_id() == 1) {
+            // dQ reducer: one TMA bulk reduce-add per 16 KB chunk of the staged tile; waiting for the
+            // staging reads here (not in a compute warp) keeps that latency off the tile loop
+            for (int i = 0; i < nq; ++i) {
+                mbar_wait(dq_staged, i & 1);
+                const int row = tok0 + (kb + i) * BQ;
+                uint8_t* stage_q = sm + Bwd3Smem::q + (i & 1) * kTile;
+                uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tm_dq)),
+                        "r"(smem_u32((c < 2 ? stage_q : stage_d) + (c & 1) * 16384)), "r"(head * D + c * 32), "r"(row)
+                        : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(&qdo_empty[i & 1]);  // staging read out: the producer may refill this buffer
+                ATRACE(i, 7);
+            }
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        if (lane_id() == 0) {
             const int ck = H * D + head * D, cv = 2 * H * D + head * D, cq = head * D;
             const int kr = tok0 + kb * BK;
             mbar_expect_tx(kv_full, 2 * kTile);
@@ -653,9 +684,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int st = i & 1;
             const uint32_t sq = smem_u32(sm + Bwd3Smem::q + st * kTile);
             const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + st * kTile);
+            if (lane_id() == 0) ATRACE(i, 8);
             mbar_wait(&qdo_full[st], (i >> 1) & 1);
+            if (lane_id() == 0) ATRACE(i, 9);
             if (i > 0) mbar_wait(s_free, (i - 1) & 1);
             tc_fence_after();
+            if (lane_id() == 0) ATRACE(i, 10);
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
@@ -672,6 +706,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             __syncwarp();
             mbar_wait(ds_full, i & 1);
             tc_fence_after();
+            if (lane_id() == 0) ATRACE(i, 12);
             if (elect_one()) {
                 // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step)
 #pragma unroll
@@ -705,12 +740,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int key = kb * BK + r;
         for (int i = 0; i < nq; ++i) {
             const int qb = kb + i;
+            if (threadIdx.x == 64) ATRACE(i, 0);
             float* Lb = sL + (i & 1) * 256;
             Lb[hf * 128 + r] = hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r]
                                        : dsum[size_t(head) * T + tok0 + qb * BQ + r];
             bar_sync_compute();  // lse / D of this tile staged
+            if (threadIdx.x == 64) ATRACE(i, 1);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(i, 2);
             const bool diag = (qb == kb);
             float sv[64], dp[64];
             tmem_ld32(tmem + lane_base + hf * 64, *reinterpret_cast<float(*)[32]>(&sv[0]));
@@ -718,6 +756,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tmem_ld32(tmem + lane_base + 128 + hf * 64, *reinterpret_cast<float(*)[32]>(&dp[0]));
             tmem_ld32(tmem + lane_base + 128 + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&dp[32]));
             tmem_ld_wait();
+            if (threadIdx.x == 64) ATRACE(i, 3);
             // every S^T column read before P^T is written over columns [0,64)
             tc_fence_before();
             bar_sync_compute();
@@ -751,11 +790,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
+            if (threadIdx.x == 64) ATRACE(i, 4);
             if (lane_id() == 0) mbar_arrive(ds_full);
             // dQ tile (thread = query row r, column half hf): TMEM -> fp32 smem staged in this tile's
             // consumed Q / dO buffers (4 swizzled [128][32] chunks) -> TMA bulk reduce-add into dq_acc
             mbar_wait(dq_full, i & 1);  // every MMA of this tile retired: Q / dO no longer read
             tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(i, 5);
             uint8_t* stage_q = sm + Bwd3Smem::q + (i & 1) * kTile;
             uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
 #pragma unroll 1
@@ -772,24 +813,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
+            if (threadIdx.x == 64) ATRACE(i, 6);
             if (lane_id() == 0) mbar_arrive(s_free);  // TMEM [0,256) free for the next S^T / dP^T
-            fence_async_smem();
-            bar_sync_compute();
-            if (threadIdx.x == 64) {  // warp 2 lane 0
-                const int row = tok0 + qb * BQ;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    asm volatile(
-                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tm_dq)),
-                        "r"(smem_u32((c < 2 ? stage_q : stage_d) + (c & 1) * 16384)), "r"(head * D + c * 32), "r"(row)
-                        : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                mbar_arrive(&qdo_empty[i & 1]);  // staging read out: the producer may refill this buffer
-            }
+            fence_async_smem();  // staging writes visible to the TMA reduce
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(dq_staged);
         }
-        if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         // dV, dK rows (thread = key row, column half hf)
         mbar_wait(dkv_full, 0);
         tc_fence_after();
@@ -1084,9 +1113,30 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     if (v2)
         launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
                  static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
-    else
+    else {
+        static unsigned long long* trace = [] {
+            unsigned long long* t = nullptr;
+            if (std::getenv("PB_ATTN_TRACE")) {
+                cudaMalloc(&t, 32 * 16 * 8);
+                cudaMemset(t, 0, 32 * 16 * 8);
+                cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
+            }
+            return t;
+        }();
         launch_k(attn_bwd_tc3_kernel, grid, dim3(kBwdThreads), Bwd3Smem::total, s, 1, tq, td, tdq, lse2,
                  static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
+        if (trace) {
+            unsigned long long h[32 * 16];
+            cudaStreamSynchronize(s);
+            cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+            for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
+                std::fprintf(stderr, "attn_bwd trace it %2d: t0=%lld", i, (long long)(h[i * 16] - h[0]));
+                for (int e = 1; e < 16; ++e)
+                    if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
+                std::fprintf(stderr, "\n");
+            }
+        }
+    }
     attn_dq_store(dq_acc, dqkv, heads, T, s);
 }
 
