@@ -708,10 +708,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_after();
             if (lane_id() == 0) ATRACE(i, 12);
             if (elect_one()) {
-                // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step)
+                // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step; queries 0-63 in
+                // columns [0,32), 64-127 in [96,128))
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 256, tmem + kk * 8, sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
+                    tc_mma_ts(tmem + 256, tmem + (kk < 4 ? kk * 8 : 96 + (kk - 4) * 8),
+                              sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
                 // dK += dS^T Q
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
@@ -750,42 +752,43 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_after();
             if (threadIdx.x == 64) ATRACE(i, 2);
             const bool diag = (qb == kb);
-            float sv[64], dp[64];
-            tmem_ld32(tmem + lane_base + hf * 64, *reinterpret_cast<float(*)[32]>(&sv[0]));
-            tmem_ld32(tmem + lane_base + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
-            tmem_ld32(tmem + lane_base + 128 + hf * 64, *reinterpret_cast<float(*)[32]>(&dp[0]));
-            tmem_ld32(tmem + lane_base + 128 + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&dp[32]));
-            tmem_ld_wait();
-            if (threadIdx.x == 64) ATRACE(i, 3);
-            // every S^T column read before P^T is written over columns [0,64)
-            tc_fence_before();
-            bar_sync_compute();
-            tc_fence_after();
+            // per 32-column chunk of this half: S^T / dP^T -> P^T (bf16 pairs) and dS^T; each half writes
+            // its P^T over its OWN consumed S^T columns (half 0 -> [0,32), half 1 -> [96,128)), so no
+            // barrier between the halves and only one chunk of S / dP live in registers
             uint32_t pk[32];
 #pragma unroll
-            for (int e2 = 0; e2 < 32; ++e2) {
-                float pv[2], dsv[2];
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c0 = hf * 64 + cc * 32;  // first query (column) of this chunk
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + c0, sv);
+                tmem_ld32(tmem + lane_base + 128 + c0, dp);
+                tmem_ld_wait();
+                if (threadIdx.x == 64 && cc == 0) ATRACE(i, 3);
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int e = 2 * e2 + u;
-                    const int ql = hf * 64 + e;
-                    float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
-                    if (diag && key > qb * BQ + ql) v = 0.f;
-                    pv[u] = v;
-                    dsv[u] = v * (dp[e] - Lb[128 + ql]);
+                for (int e2 = 0; e2 < 16; ++e2) {
+                    float pv[2], dsv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int e = 2 * e2 + u;
+                        const int ql = c0 + e;
+                        float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
+                        if (diag && key > qb * BQ + ql) v = 0.f;
+                        pv[u] = v;
+                        dsv[u] = v * (dp[e] - Lb[128 + ql]);
+                    }
+                    pk[cc * 16 + e2] = pack_bf16(pv[0], pv[1]);
+                    dp[2 * e2] = dsv[0];
+                    dp[2 * e2 + 1] = dsv[1];
                 }
-                pk[e2] = pack_bf16(pv[0], pv[1]);
-                dp[2 * e2] = dsv[0];
-                dp[2 * e2 + 1] = dsv[1];
-            }
-            tmem_st32u(tmem + lane_base + hf * 32, pk);
 #pragma unroll
-            for (int e8 = 0; e8 < 8; ++e8) {
-                const int col = hf * 64 + e8 * 8;
-                *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
-                    make_uint4(pack_bf16(dp[e8 * 8], dp[e8 * 8 + 1]), pack_bf16(dp[e8 * 8 + 2], dp[e8 * 8 + 3]),
-                               pack_bf16(dp[e8 * 8 + 4], dp[e8 * 8 + 5]), pack_bf16(dp[e8 * 8 + 6], dp[e8 * 8 + 7]));
+                for (int e8 = 0; e8 < 4; ++e8) {
+                    const int col = c0 + e8 * 8;
+                    *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
+                        make_uint4(pack_bf16(dp[e8 * 8], dp[e8 * 8 + 1]), pack_bf16(dp[e8 * 8 + 2], dp[e8 * 8 + 3]),
+                                   pack_bf16(dp[e8 * 8 + 4], dp[e8 * 8 + 5]), pack_bf16(dp[e8 * 8 + 6], dp[e8 * 8 + 7]));
+                }
             }
+            tmem_st32u(tmem + lane_base + (hf ? 96 : 0), pk);
             tmem_st_wait();
             fence_async_smem();
             tc_fence_before();
