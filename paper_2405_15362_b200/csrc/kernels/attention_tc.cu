@@ -687,6 +687,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             if (lane_id() == 0) ATRACE(i, 8);
             mbar_wait(&qdo_full[st], (i >> 1) & 1);
             if (lane_id() == 0) ATRACE(i, 9);
+            tc_fence_after();
+            // dP^T first: [128,256) was read out before the previous tile's ds_full, so this MMA
+            // overlaps the previous tile's dQ drain; S^T waits for [0,128) (dQ) to be free
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
+                }
+            }
+            __syncwarp();
             if (i > 0) mbar_wait(s_free, (i - 1) & 1);
             tc_fence_after();
             if (lane_id() == 0) ATRACE(i, 10);
@@ -695,11 +706,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
                     tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
-                }
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
                 }
                 tc_commit(s_full);
             }
