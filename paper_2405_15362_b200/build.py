@@ -43,7 +43,8 @@ def _flags(src):
     common = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I" + CSRC, "-I" + os.path.join(ROOT, "include"),
               "-I" + JSON_DIR, "-DNDEBUG"] + ARCH
     if src.endswith(".cu"):
-        return common + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas=-v" if os.environ.get("PB_PTXAS_V") else "-w"]
+        extra = ["-DPB_ATTN_TRACE_BUILD"] if os.environ.get("PB_ATTN_TRACE_BUILD") else []
+        return common + extra + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas=-v" if os.environ.get("PB_PTXAS_V") else "-w"]
     return common
 
 

@@ -61,6 +61,20 @@ __device__ __forceinline__ uint32_t sw128(int row, int col) {
     return uint32_t((col >> 6) * 16384 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2);
 }
 
+// Phase stamps (clock64) of block 0, compiled in only with -DPB_ATTN_TRACE_BUILD (build.py:
+// PB_ATTN_TRACE_BUILD=1); read by PB_ATTN_TRACE / PB_ATTN_TRACE_FWD (tests/trace_attn_*.py)
+__device__ unsigned long long* g_attn_trace = nullptr;
+#ifdef PB_ATTN_TRACE_BUILD
+#define ATRACE(i, ev)                                                                        \
+    do {                                                                                     \
+        if (g_attn_trace && blockIdx.x == 0 && (i) < 32) g_attn_trace[(i) * 16 + (ev)] = clock64(); \
+    } while (0)
+#else
+#define ATRACE(i, ev) \
+    do {              \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
     asm volatile(
@@ -158,8 +172,10 @@ __global__ void __launch_bounds__(192, 1)
         auto issue_pv = [&](int j) {  // O += P_j V_j, P from TMEM
             const int pb = j & 1;
             const int kv = j % kFwdStages;
+            if (lane_id() == 0) ATRACE(j, 11);
             mbar_wait(&p_full[pb], (j >> 1) & 1);
             tc_fence_after();
+            if (lane_id() == 0) ATRACE(j, 12);
             if (elect_one()) {
                 const uint32_t sv = smem_u32(sm + FwdSmem::v0 + kv * kTile);
 #pragma unroll
@@ -174,9 +190,12 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < nkv; ++j) {
             const int st = j & 1;
             const int kv = j % kFwdStages;
+            if (lane_id() == 0) ATRACE(j, 8);
             mbar_wait(&kv_full[kv], (j / kFwdStages) & 1);
+            if (lane_id() == 0) ATRACE(j, 9);
             if (j >= 2) mbar_wait(&s_free[st], ((j - 2) >> 1) & 1);
             tc_fence_after();
+            if (lane_id() == 0) ATRACE(j, 10);
             if (elect_one()) {
                 const uint32_t sk = smem_u32(sm + FwdSmem::k0 + kv * kTile);
 #pragma unroll
@@ -202,8 +221,10 @@ __global__ void __launch_bounds__(192, 1)
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < nkv; ++j) {
             const int st = j & 1;
+            if (threadIdx.x == 64) ATRACE(j, 0);
             mbar_wait(&s_full[st], (j >> 1) & 1);
             tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(j, 1);
             float s[128];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + st * 128 + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
@@ -211,19 +232,21 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&s_free[st]);
+            if (threadIdx.x == 64) ATRACE(j, 2);
             // one warp per SM sub-partition runs this: keep the reductions as 8 independent
             // chains (a single 128-long chain would be latency-bound), scale folded into the exp
             float mx8[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
-            const bool diag = (j == nkv - 1);
+            // causal mask only on the diagonal tile: a separate (warp-uniform) branch, so the other
+            // tiles do not pay a compare + select per element
+            if (__builtin_expect(j == nkv - 1, 0)) {
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                float v = s[c];
-                if (diag && c > r) v = -INFINITY;
-                s[c] = v;
-                mx8[c & 7] = fmaxf(mx8[c & 7], v);
+                for (int c = 0; c < 128; ++c)
+                    if (c > r) s[c] = -INFINITY;
             }
+#pragma unroll
+            for (int c = 0; c < 128; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
             const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
             const float m_new = fmaxf(m_used, mx);
@@ -255,6 +278,7 @@ __global__ void __launch_bounds__(192, 1)
                 }
             }
             if (j == 0) m_used = m_new;
+            if (threadIdx.x == 64) ATRACE(j, 4);
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
@@ -274,6 +298,7 @@ __global__ void __launch_bounds__(192, 1)
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
+            if (threadIdx.x == 64) ATRACE(j, 5);
             if (lane_id() == 0) mbar_arrive(&p_full[j & 1]);
         }
         // epilogue: O / l -> bf16
@@ -579,12 +604,6 @@ struct Bwd3Smem {
 static_assert(Bwd3Smem::total <= 232448, "attn bwd v3: shared memory over the sm_100 opt-in limit");
 
 
-// PB_ATTN_TRACE=1: clock64 stamps of block 0's phases (tests/trace_attn_bwd.py); null otherwise
-__device__ unsigned long long* g_attn_trace = nullptr;
-#define ATRACE(i, ev)                                                                        \
-    do {                                                                                     \
-        if (g_attn_trace && blockIdx.x == 0 && (i) < 32) g_attn_trace[(i) * 16 + (ev)] = clock64(); \
-    } while (0)
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -770,6 +789,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 tmem_ld32(tmem + lane_base + 128 + c0, dp);
                 tmem_ld_wait();
                 if (threadIdx.x == 64 && cc == 0) ATRACE(i, 3);
+                if (__builtin_expect(diag, 0)) {  // causal mask on the diagonal tile only
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (key > qb * BQ + c0 + e) sv[e] = -INFINITY;
+                }
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2) {
                     float pv[2], dsv[2];
@@ -777,8 +801,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     for (int u = 0; u < 2; ++u) {
                         const int e = 2 * e2 + u;
                         const int ql = c0 + e;
-                        float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
-                        if (diag && key > qb * BQ + ql) v = 0.f;
+                        const float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
                         pv[u] = v;
                         dsv[u] = v * (dp[e] - Lb[128 + ql]);
                     }
@@ -1169,8 +1192,28 @@ void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int 
     }();
     if (!v2 || seq % (2 * BQ)) {
         dim3 grid(seq / BQ * heads * batch);
+        static unsigned long long* trace = [] {
+            unsigned long long* t = nullptr;
+            if (std::getenv("PB_ATTN_TRACE_FWD")) {
+                cudaMalloc(&t, 32 * 16 * 8);
+                cudaMemset(t, 0, 32 * 16 * 8);
+                cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
+            }
+            return t;
+        }();
         launch_k(attn_fwd_tc_kernel, grid, dim3(192), FwdSmem::total, s, 1, tm, out, lse2, seq, heads, T,
                  0.08838834764831845f);
+        if (trace) {
+            unsigned long long h[32 * 16];
+            cudaStreamSynchronize(s);
+            cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+            for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
+                std::fprintf(stderr, "attn_fwd trace it %2d: t0=%lld", i, (long long)(h[i * 16] - h[0]));
+                for (int e = 1; e < 16; ++e)
+                    if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
+                std::fprintf(stderr, "\n");
+            }
+        }
     } else {
         dim3 grid(seq / (2 * BQ) * heads * batch);
         launch_k(attn_fwd_tc2_kernel, grid, dim3(320), Fwd2Smem::total, s, 1, tm, out, lse2, seq, heads, T,
