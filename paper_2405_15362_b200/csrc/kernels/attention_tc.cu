@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(192, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ lse2, int seq, int H, int T, float scale) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FwdSmem::bars);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;   // [3]
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T,
                        float scale) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::bars);
     uint64_t* kv_full = bars + 0;
     uint64_t* qdo_full = bars + 1;
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2, const float* __restrict__ dsum,
                         __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (Bwd3Smem::total)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd3Smem::bars);
     uint64_t* kv_full = bars + 0;
@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(320, 1)
     attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
                         float* __restrict__ lse2, int seq, int H, int T, float scale) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd2Smem::bars);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;   // [2]
