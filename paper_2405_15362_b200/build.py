@@ -44,6 +44,7 @@ def _flags(src):
               "-I" + JSON_DIR, "-DNDEBUG"] + ARCH
     if src.endswith(".cu"):
         extra = ["-DPB_ATTN_TRACE_BUILD"] if os.environ.get("PB_ATTN_TRACE_BUILD") else []
+        extra += os.environ.get("PB_NVCC_EXTRA", "").split()  # experiments only (-D switches)
         return common + extra + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas=-v" if os.environ.get("PB_PTXAS_V") else "-w"]
     return common
 

@@ -348,6 +348,7 @@ struct BwdSmem {
     static constexpr int total = bars + 256 + 1024;
 };
 constexpr int kBwdThreads = 320;
+constexpr int kBwd4Threads = 384;
 
 __device__ __forceinline__ void bar_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
@@ -883,6 +884,345 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ backward v4
+// Same decomposition and TMEM map as v3, re-ordered so that the dQ drain, its reduce and the
+// lse / D loads leave the tensor pipe's critical path:
+//   * dQ(i) = dS K goes into the consumed dP^T columns [128,256) and is issued FIRST after dS^T
+//     lands; the compute warps read it out (registers), release the columns, then stage it (fp32)
+//     in the consumed dO(i) buffer (d columns 0-63) and the consumed dS^T buffer (64-127) for the
+//     TMA bulk reduce-add, while the tensor pipe runs dV(i), dK(i) and S^T(i+1);
+//   * Q and dO have separate full / empty barriers: Q(i) is refilled as soon as dK(i) retires, dO(i)
+//     once the reduce has read the staging; the dS^T buffer is handed back to the compute warps
+//     (ds_buf) once the reduce has read its half, before they store dS^T(i+1);
+//   * dP^T(i+1) follows once dQ(i) has left TMEM, S^T(i+1) right after dV(i) read P^T (in-order pipe);
+//   * lse / D of query tile i+1 are loaded into registers while tile i is processed.
+// MMA issue order per tile: dQ(i) dV(i) dK(i) S^T(i+1) | dP^T(i+1).
+// 384 threads: warp 0 K/V + Q loads, warp 1 MMA, warps 2-9 compute, warp 10 dQ reducer, warp 11 dO
+// loads (each blocking wait on its own warp: a divergent lane's wait_group stalls its whole warp).
+// Measured dead ends: staging dQ in both Q(i) and dO(i) (as v3) stalls S^T(i+1) on the Q reload
+// behind the reduce; splitting the elementwise phase to run P^T under the MMAs, and draining dQ
+// with red.global.add from registers (L2 atomics issue-bound, ~2.7k cycles per tile), were slower.
+__global__ void __launch_bounds__(kBwd4Threads, 1)
+    attn_bwd_tc4_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
+                        const float* __restrict__ dsum,
+                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
+    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (Bwd3Smem::total)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd3Smem::bars);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* q_full = bars + 1;     // [2]
+    uint64_t* do_full = bars + 3;    // [2]
+    uint64_t* q_empty = bars + 5;    // [2] MMA commit after dK(i): Q(i) no longer read
+    uint64_t* do_empty = bars + 7;   // [2] reducer: dQ(i) staging in dO(i) read out
+    uint64_t* s_full = bars + 9;     // MMA: S^T(i) in [0,128)
+    uint64_t* qdo_used = bars + 10;  // MMA commit after dK(i): dO(i), dS^T(i) no longer read
+    uint64_t* dp_full = bars + 11;   // MMA: dP^T(i) in [128,256)
+    uint64_t* ds_full = bars + 12;   // 8 compute warps: dS^T(i) in smem, P^T(i) in TMEM, S^T / dP^T consumed
+    uint64_t* dq_full = bars + 13;   // MMA: dQ(i) in [128,256)
+    uint64_t* dq_free = bars + 14;   // 8 compute warps: dQ(i) read out of TMEM
+    uint64_t* dkv_full = bars + 15;
+    uint64_t* dq_staged = bars + 16;  // 8 compute warps: dQ(i) staged (fp32) in dO(i) / dS^T buffers
+    uint64_t* ds_buf = bars + 17;     // reducer: the dS^T-buffer half of the staging read out
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+    float* sL = reinterpret_cast<float*>(sm + Bwd3Smem::lse);
+
+    const uint32_t warp = warp_id();
+    const int nqb = seq / BQ;
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int kb = int(blockIdx.x) / (H * (T / seq));
+    const int head = hb % H, b = hb / H;
+    const int tok0 = b * seq;
+    const int nq = nqb - kb;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm_qkv);
+        tma_prefetch(&tm_do);
+        tma_prefetch(&tm_dq);
+        for (int i = 0; i < 18; ++i) mbar_init(&bars[i], (i == 12 || i == 14 || i == 16) ? 8 : 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;  // [0,128) S^T -> P^T ; [128,256) dP^T -> dQ ; dV ; dK
+    pdl_wait();
+    pdl_launch();
+
+    if (warp >= 10) {
+        if (warp == 10 && lane_id() == 0) {
+            // dQ reducer: one TMA bulk reduce-add per 16 KB chunk; the dS^T-buffer half first, so the
+            // compute warps get that buffer back early
+            for (int i = 0; i < nq; ++i) {
+                mbar_wait(dq_staged, i & 1);
+                const int row = tok0 + (kb + i) * BQ;
+                uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
+                uint8_t* stage_s = sm + Bwd3Smem::dst;
+#pragma unroll
+                for (int c = 3; c >= 0; --c) {
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tm_dq)),
+                        "r"(smem_u32((c < 2 ? stage_d : stage_s) + (c & 1) * 16384)), "r"(head * D + c * 32), "r"(row)
+                        : "memory");
+                    if (c == 2) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                mbar_arrive(ds_buf);
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(&do_empty[i & 1]);
+            }
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        if (warp == 11 && lane_id() == 0) {
+            for (int i = 0; i < nq; ++i) {
+                const int st = i & 1;
+                if (i >= 2) mbar_wait(&do_empty[st], ((i - 2) >> 1) & 1);
+                uint8_t* ds = sm + Bwd3Smem::dO + st * kTile;
+                const int qr = tok0 + (kb + i) * BQ;
+                mbar_expect_tx(&do_full[st], kTile);
+                tma_load_2d(ds, &tm_do, &do_full[st], head * D, qr);
+                tma_load_2d(ds + 16384, &tm_do, &do_full[st], head * D + 64, qr);
+            }
+        }
+    } else if (warp == 0) {
+        const int cq = head * D;
+        if (lane_id() == 0) {
+            const int ck = H * D + head * D, cv = 2 * H * D + head * D;
+            const int kr = tok0 + kb * BK;
+            mbar_expect_tx(kv_full, 2 * kTile);
+            tma_load_2d(sm + Bwd3Smem::k, &tm_qkv, kv_full, ck, kr);
+            tma_load_2d(sm + Bwd3Smem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
+            tma_load_2d(sm + Bwd3Smem::v, &tm_qkv, kv_full, cv, kr);
+            tma_load_2d(sm + Bwd3Smem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i & 1;
+                if (i >= 2) mbar_wait(&q_empty[st], ((i - 2) >> 1) & 1);
+                uint8_t* qs = sm + Bwd3Smem::q + st * kTile;
+                const int qr = tok0 + (kb + i) * BQ;
+                mbar_expect_tx(&q_full[st], kTile);
+                tma_load_2d(qs, &tm_qkv, &q_full[st], cq, qr);
+                tma_load_2d(qs + 16384, &tm_qkv, &q_full[st], cq + 64, qr);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
+        constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
+        const uint32_t sk = smem_u32(sm + Bwd3Smem::k), sv = smem_u32(sm + Bwd3Smem::v);
+        const uint32_t sdst = smem_u32(sm + Bwd3Smem::dst);
+        auto issue_s = [&](int i) {  // S^T(i) = K Q(i)^T -> [0,128)
+            const uint32_t sq = smem_u32(sm + Bwd3Smem::q + (i & 1) * kTile);
+            mbar_wait(&q_full[i & 1], (i >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
+                }
+                tc_commit(s_full);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int i) {  // dP^T(i) = V dO(i)^T -> [128,256)
+            const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + (i & 1) * kTile);
+            mbar_wait(&do_full[i & 1], (i >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
+                }
+                tc_commit(dp_full);
+            }
+            __syncwarp();
+        };
+        mbar_wait(kv_full, 0);
+        issue_s(0);
+        issue_dp(0);
+        for (int i = 0; i < nq; ++i) {
+            const int st = i & 1;
+            const uint32_t sq = smem_u32(sm + Bwd3Smem::q + st * kTile);
+            const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + st * kTile);
+            mbar_wait(ds_full, i & 1);
+            tc_fence_after();
+            if (lane_id() == 0) ATRACE(i, 8);
+            if (elect_one()) {
+                // dQ = dS K -> [128,256) (dP^T(i) consumed before ds_full)
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma(tmem + 128, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
+                           id_mnmn, kk != 0);
+                tc_commit(dq_full);
+                // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step; queries 0-63 in
+                // columns [0,32), 64-127 in [96,128))
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 256, tmem + (kk < 4 ? kk * 8 : 96 + (kk - 4) * 8),
+                              sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
+                // dK += dS^T Q
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
+                           (i | kk) != 0);
+                }
+                tc_commit(qdo_used);  // dO(i), dS^T(i) no longer read
+                tc_commit(&q_empty[st]);
+            }
+            __syncwarp();
+            if (i + 1 < nq) {
+                // S^T(i+1) overwrites [0,128) after dV(i) has read P^T there (the MMA pipe runs in issue order)
+                issue_s(i + 1);
+                if (lane_id() == 0) ATRACE(i, 10);
+                mbar_wait(dq_free, i & 1);
+                tc_fence_after();
+                if (lane_id() == 0) ATRACE(i, 9);
+                issue_dp(i + 1);
+            }
+        }
+        if (elect_one()) tc_commit(dkv_full);
+        __syncwarp();
+    } else {
+        const uint32_t q4 = warp & 3;
+        const int hf = int(warp - 2) >> 2;  // query half (columns of S^T) handled by this warp
+        const int r = int(q4 * 32 + lane_id());
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const float sl2 = scale * kLog2e;
+        uint8_t* sdst = sm + Bwd3Smem::dst;
+        const int key = kb * BK + r;
+        auto lse_of = [&](int qb) {  // this thread's staged value: lse2 (half 0) or D (half 1) of query row r
+            return hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r] : dsum[size_t(head) * T + tok0 + qb * BQ + r];
+        };
+        sL[hf * 128 + r] = lse_of(kb);
+        bar_sync_compute();
+        for (int i = 0; i < nq; ++i) {
+            const int qb = kb + i;
+            const float* Lb = sL + (i & 1) * 256;
+            const float lnext = i + 1 < nq ? lse_of(qb + 1) : 0.f;  // in flight during this tile
+            if (threadIdx.x == 64) ATRACE(i, 0);
+            mbar_wait(s_full, i & 1);
+            mbar_wait(dp_full, i & 1);
+            tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(i, 1);
+            const bool diag = (qb == kb);
+            // per 32-column chunk of this half: S^T / dP^T -> P^T (bf16 pairs) and dS^T; each half writes
+            // its P^T over its OWN consumed S^T columns (half 0 -> [0,32), half 1 -> [96,128))
+            uint32_t pk[32];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c0 = hf * 64 + cc * 32;
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + c0, sv);
+                tmem_ld32(tmem + lane_base + 128 + c0, dp);
+                tmem_ld_wait();
+                if (__builtin_expect(diag, 0)) {  // causal mask on the diagonal tile only
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (key > qb * BQ + c0 + e) sv[e] = -INFINITY;
+                }
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) {
+                    float pv[2], dsv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int e = 2 * e2 + u;
+                        const float v = fast_exp2(fmaf(sv[e], sl2, -Lb[c0 + e]));
+                        pv[u] = v;
+                        dsv[u] = v * (dp[e] - Lb[128 + c0 + e]);
+                    }
+                    pk[cc * 16 + e2] = pack_bf16(pv[0], pv[1]);
+                    dp[2 * e2] = dsv[0];
+                    dp[2 * e2 + 1] = dsv[1];
+                }
+                if (cc == 0 && i > 0) mbar_wait(ds_buf, (i - 1) & 1);  // dQ(i-1) staging there read out
+#pragma unroll
+                for (int e8 = 0; e8 < 4; ++e8) {
+                    const int col = c0 + e8 * 8;
+                    *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
+                        make_uint4(pack_bf16(dp[e8 * 8], dp[e8 * 8 + 1]), pack_bf16(dp[e8 * 8 + 2], dp[e8 * 8 + 3]),
+                                   pack_bf16(dp[e8 * 8 + 4], dp[e8 * 8 + 5]), pack_bf16(dp[e8 * 8 + 6], dp[e8 * 8 + 7]));
+                }
+            }
+            tmem_st32u(tmem + lane_base + (hf ? 96 : 0), pk);
+            tmem_st_wait();
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(ds_full);
+            if (threadIdx.x == 64) ATRACE(i, 2);
+            // ---- dQ(i) (thread = query row r, d columns of half hf): TMEM -> registers -> release the
+            // columns -> fp32 smem staged in the tile's consumed Q / dO buffers -> TMA bulk reduce-add
+            mbar_wait(dq_full, i & 1);
+            tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(i, 3);
+            {
+                float v[64];
+                tmem_ld32(tmem + lane_base + 128 + hf * 64, *reinterpret_cast<float(*)[32]>(&v[0]));
+                tmem_ld32(tmem + lane_base + 128 + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane_id() == 0) mbar_arrive(dq_free);  // [128,256) free for dP^T(i+1)
+                if (threadIdx.x == 64) ATRACE(i, 5);
+                mbar_wait(qdo_used, i & 1);               // dK(i) retired: dO(i) / dS^T may be overwritten
+                uint8_t* stage = hf == 0 ? sm + Bwd3Smem::dO + (i & 1) * kTile : sm + Bwd3Smem::dst;
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    uint8_t* chunk = stage + cc * 16384 + r * 128;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        *reinterpret_cast<float4*>(chunk + ((g ^ (r & 7)) << 4)) =
+                            make_float4(v[cc * 32 + 4 * g], v[cc * 32 + 4 * g + 1], v[cc * 32 + 4 * g + 2],
+                                        v[cc * 32 + 4 * g + 3]);
+                }
+            }
+            fence_async_smem();  // staging writes visible to the TMA reduce
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(dq_staged);
+            if (threadIdx.x == 64) ATRACE(i, 4);
+            if (i + 1 < nq) {
+                sL[((i + 1) & 1) * 256 + hf * 128 + r] = lnext;  // buffer last read by tile i-1
+                bar_sync_compute();
+            }
+        }
+        // dV, dK rows (thread = key row, column half hf)
+        mbar_wait(dkv_full, 0);
+        tc_fence_after();
+        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = hf * 2 + cc;
+            float v[32], k[32];
+            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
+            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
+            tmem_ld_wait();
+            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
+            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                dv[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
+                                   pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
+                dk[e] = make_uint4(pack_bf16(k[8 * e] * scale, k[8 * e + 1] * scale),
+                                   pack_bf16(k[8 * e + 2] * scale, k[8 * e + 3] * scale),
+                                   pack_bf16(k[8 * e + 4] * scale, k[8 * e + 5] * scale),
+                                   pack_bf16(k[8 * e + 6] * scale, k[8 * e + 7] * scale));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<512>(tmem);
+    }
+}
+
 
 // ------------------------------------------------------------------ forward v2 (two Q tiles per CTA)
 // One CTA per (256 queries = tiles A and B, head, sequence); 320 threads:
@@ -1138,11 +1478,40 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
                                        uint64_t(heads) * D, 32, 128);
     dim3 grid(seq / BK * heads * batch);
-    static const bool v2 = [] {
+    // PB_ATTN_BWD=2 / =3: the earlier kernels (v2: smem P^T; v3: serial elementwise phase)
+    static const int ver = [] {
         const char* e = std::getenv("PB_ATTN_BWD");
-        return e && e[0] == '2';
+        return e && (e[0] == '2' || e[0] == '3') ? e[0] - '0' : 4;
     }();
-    if (v2)
+    if (ver == 4) {
+        static bool attr4 = [] {
+            cudaFuncSetAttribute(attn_bwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd3Smem::total);
+            return true;
+        }();
+        (void)attr4;
+        static unsigned long long* trace4 = [] {
+            unsigned long long* t = nullptr;
+            if (std::getenv("PB_ATTN_TRACE")) {
+                cudaMalloc(&t, 32 * 16 * 8);
+                cudaMemset(t, 0, 32 * 16 * 8);
+                cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
+            }
+            return t;
+        }();
+        launch_k(attn_bwd_tc4_kernel, grid, dim3(kBwd4Threads), Bwd3Smem::total, s, 1, tq, td, tdq, lse2,
+                 static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
+        if (trace4) {
+            unsigned long long h[32 * 16];
+            cudaStreamSynchronize(s);
+            cudaMemcpy(h, trace4, sizeof(h), cudaMemcpyDeviceToHost);
+            for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
+                std::fprintf(stderr, "attn_bwd4 trace it %2d: t0=%lld", i, (long long)(h[i * 16] - h[0]));
+                for (int e = 1; e < 16; ++e)
+                    if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
+                std::fprintf(stderr, "\n");
+            }
+        }
+    } else if (ver == 2)
         launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
                  static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
     else {

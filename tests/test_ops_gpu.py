@@ -189,3 +189,35 @@ def test_rmsnorm_unit_gamma(h):
     d0 = K.rmsnorm_bwd(dy, x, None, r0)
     torch.cuda.synchronize()
     assert torch.equal(y0, y1) and torch.equal(r0, r1) and torch.equal(d0, d1)
+
+
+_V3_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+from tests import kernels as K
+g = torch.Generator(device="cuda").manual_seed(11)
+qkv = torch.randn(2 * 1024, 3 * 4 * 128, device="cuda", generator=g).bfloat16()
+dout = torch.randn(2 * 1024, 4 * 128, device="cuda", generator=g).bfloat16()
+out, lse2 = K.attn_fwd_tc(qkv, 2, 1024, 4)
+torch.save(K.attn_bwd_tc(qkv, out, dout, lse2, 2, 1024, 4).cpu(), {path!r})
+"""
+
+
+def test_attention_backward_v4_matches_v3(tmp_path):
+    """The default backward (v4: re-ordered MMAs, dQ released early) against the previous kernel
+    (PB_ATTN_BWD=3) on the same inputs: only the fp32 dQ reduction order differs."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for ver in ("3", "4"):
+        path = str(tmp_path / f"dqkv{ver}.pt")
+        env = dict(os.environ, PB_ATTN_BWD=ver)
+        subprocess.run([sys.executable, "-c", _V3_SCRIPT.format(root=root, path=path)], env=env, check=True,
+                       timeout=300)
+        outs[ver] = torch.load(path)
+    H = 4 * 128
+    assert torch.equal(outs["3"][:, H:], outs["4"][:, H:])  # dK, dV: same MMAs, same order
+    assert rel(outs["4"][:, :H], outs["3"][:, :H]) < 1e-2  # dQ: fp32 reduce order
