@@ -84,6 +84,14 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+
 __device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -896,7 +904,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 //     (ds_buf) once the reduce has read its half, before they store dS^T(i+1);
 //   * dP^T(i+1) follows once dQ(i) has left TMEM, S^T(i+1) right after dV(i) read P^T (in-order pipe);
 //   * lse / D of query tile i+1 are loaded into registers while tile i is processed.
-// MMA issue order per tile: dQ(i) dV(i) dK(i) S^T(i+1) | dP^T(i+1).
+// MMA issue order per tile: dK(i) dQ(i) dV(i) S^T(i+1) | dP^T(i+1); P^T and dS^T are A operands
+// straight from TMEM (bf16 pairs over their consumed fp32 columns), which keeps dK off shared memory.
 // 384 threads: warp 0 K/V + Q loads, warp 1 MMA, warps 2-9 compute, warp 10 dQ reducer, warp 11 dO
 // loads (each blocking wait on its own warp: a divergent lane's wait_group stalls its whole warp).
 // Measured dead ends: staging dQ in both Q(i) and dO(i) (as v3) stalls S^T(i+1) on the Q reload
@@ -1053,27 +1062,25 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             tc_fence_after();
             if (lane_id() == 0) ATRACE(i, 8);
             if (elect_one()) {
-                // dQ = dS K -> [128,256) (dP^T(i) consumed before ds_full)
+                // dK += dS^T Q : A = dS^T (bf16 pairs over the consumed dP^T columns) from TMEM
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 384, tmem + 128 + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
+                              sdesc(sq + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
+                // dQ = dS K -> [128,256), after dK has read dS^T there (in-order pipe)
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
                     tc_mma(tmem + 128, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
                            id_mnmn, kk != 0);
                 tc_commit(dq_full);
                 // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step; queries 0-63 in
-                // columns [0,32), 64-127 in [96,128))
+                // columns [0,32), 64-127 in [64,96))
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 256, tmem + (kk < 4 ? kk * 8 : 96 + (kk - 4) * 8),
+                    tc_mma_ts(tmem + 256, tmem + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
                               sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
-                // dK += dS^T Q
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
-                           (i | kk) != 0);
-                }
                 tc_commit(qdo_used);  // dO(i), dS^T(i) no longer read
-                tc_commit(&q_empty[st]);
+                tc_commit(&q_empty[st]);  // (Q(i) was last read by dK(i))
             }
             __syncwarp();
             if (i + 1 < nq) {
@@ -1111,9 +1118,9 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             tc_fence_after();
             if (threadIdx.x == 64) ATRACE(i, 1);
             const bool diag = (qb == kb);
-            // per 32-column chunk of this half: S^T / dP^T -> P^T (bf16 pairs) and dS^T; each half writes
-            // its P^T over its OWN consumed S^T columns (half 0 -> [0,32), half 1 -> [96,128))
-            uint32_t pk[32];
+            // per 32-column chunk of this half: S^T / dP^T -> P^T and dS^T (bf16 pairs) written back over
+            // the chunk's own consumed columns (P^T: half 0 -> [0,32), half 1 -> [64,96); dS^T at +128),
+            // and dS^T to smem (the dQ MMA reads it MN-major)
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
                 const int c0 = hf * 64 + cc * 32;
@@ -1126,6 +1133,7 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
                     for (int e = 0; e < 32; ++e)
                         if (key > qb * BQ + c0 + e) sv[e] = -INFINITY;
                 }
+                uint32_t pk[16], dk[16];
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2) {
                     float pv[2], dsv[2];
@@ -1136,20 +1144,19 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
                         pv[u] = v;
                         dsv[u] = v * (dp[e] - Lb[128 + c0 + e]);
                     }
-                    pk[cc * 16 + e2] = pack_bf16(pv[0], pv[1]);
-                    dp[2 * e2] = dsv[0];
-                    dp[2 * e2 + 1] = dsv[1];
+                    pk[e2] = pack_bf16(pv[0], pv[1]);
+                    dk[e2] = pack_bf16(dsv[0], dsv[1]);
                 }
+                tmem_st16u(tmem + lane_base + hf * 64 + cc * 16, pk);
+                tmem_st16u(tmem + lane_base + 128 + hf * 64 + cc * 16, dk);
                 if (cc == 0 && i > 0) mbar_wait(ds_buf, (i - 1) & 1);  // dQ(i-1) staging there read out
 #pragma unroll
                 for (int e8 = 0; e8 < 4; ++e8) {
                     const int col = c0 + e8 * 8;
                     *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
-                        make_uint4(pack_bf16(dp[e8 * 8], dp[e8 * 8 + 1]), pack_bf16(dp[e8 * 8 + 2], dp[e8 * 8 + 3]),
-                                   pack_bf16(dp[e8 * 8 + 4], dp[e8 * 8 + 5]), pack_bf16(dp[e8 * 8 + 6], dp[e8 * 8 + 7]));
+                        make_uint4(dk[4 * e8], dk[4 * e8 + 1], dk[4 * e8 + 2], dk[4 * e8 + 3]);
                 }
             }
-            tmem_st32u(tmem + lane_base + (hf ? 96 : 0), pk);
             tmem_st_wait();
             fence_async_smem();
             tc_fence_before();
