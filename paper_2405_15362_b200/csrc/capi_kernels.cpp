@@ -111,6 +111,13 @@ extern "C" int pbt_gemm_set_cta_group(int32_t cg) {
     return pbx::guard([&] { pbk::gemm_force_cta_group(cg); });
 }
 
+extern "C" int pbt_gemm_set_tile_n(int32_t bn) {
+    return pbx::guard([&] {
+        if (bn != 0 && bn != 256 && bn != 192 && bn != 160) throw std::invalid_argument("tile N must be 0, 256, 192 or 160");
+        pbk::gemm_force_bn(bn);
+    });
+}
+
 extern "C" int pbt_gemm_set_stream_k(int32_t on) {
     return pbx::guard([&] { pbk::gemm_force_stream_k(on); });
 }

@@ -41,7 +41,8 @@ struct Cfg {
     static constexpr int kBBytes = kBRows * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-    static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+    static constexpr int kAccStride = BN <= 128 ? 128 : 256;  // accumulator buffer pitch (TMEM columns)
+    static constexpr int kTmemCols = 2 * kAccStride;           // double-buffered accumulator (power of 2)
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int num_k = kb1 < 0 ? resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor).num_k : kb1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + acc * C_::kAccStride;
                 for (int kb = kb0; kb < num_k; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = m0 + row_in_tile;
-            const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
+            const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * C_::kAccStride;
             if (kb1 >= 0 && kb0 > 0) {
                 // stream-K contributor (this pair's first segment): park the partial tile, publish
                 float* slot = p.sk_ws + (size_t(cid) * CG + rank) * (BM * BN) + size_t(row_in_tile) * BN;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (kAux) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) aux_cur[j] = aux_next[j];
-                    if (c + 32 < BN) {
+                    if (c + 32 < BN && n0 + c + 32 < p.N) {  // (BN = 160 / 192: the last tile may be partial)
                         const uint4* s4 = reinterpret_cast<const uint4*>(p.aux + size_t(row) * p.ldaux + n0 + c + 32);
 #pragma unroll
                         for (int j = 0; j < 4; ++j) aux_next[j] = s4[j];
@@ -671,6 +672,35 @@ void gemm_force_stream_k(int on) { g_force_sk = on; }
 static int g_force_cg = -1;  // tests: -1 auto, 1 or 2 forced
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
 
+// F-pass pair GEMMs (both operands K-major) can pick the tile width that minimises
+// waves x width on the GPU's CTA pairs: e.g. at T = 4096 the QKV projection (N = 3h = 6144)
+// runs 512 tiles of 256 x 192 in 7 waves instead of 384 of 256 x 256 in 6 (5.2 used), and the
+// N = h = 2048 projections 208 tiles of 256 x 160 in 3 waves instead of 128 in 2 (1.73 used).
+// The last column tile may be partial (TMA zero-fills B rows >= N, the epilogue skips them).
+// Off by default (PB_GEMM_BN=1 enables it): measured at T = 4096 the narrower tiles lose more per
+// tile than the waves gain (QKV 1431 -> 1446 TFLOP/s, FC2 1399 -> 1334 on 256 x 160), consistent
+// with the extra A-panel traffic (13 instead of 8 column tiles re-read A from L2).
+static int g_force_bn = 0;  // tests: 0 = PB_GEMM_BN, else 256 / 192 / 160
+void gemm_force_bn(int bn) { g_force_bn = bn; }
+int gemm_f_bn(int M, int N) {
+    if (g_force_bn) return g_force_bn;
+    static const bool on = [] {
+        const char* e = std::getenv("PB_GEMM_BN");
+        return e && e[0] == '1';
+    }();
+    if (!on) return 256;
+    const int pairs = sm_count() / 2;
+    const int mt = M / 256;
+    auto cost = [&](int bn) {
+        const long long tiles = (long long)mt * ((N + bn - 1) / bn);
+        return double((tiles + pairs - 1) / pairs) * bn * (bn == 256 ? 1.0 : 1.03);  // narrower tiles: more A reuse traffic
+    };
+    int best = 256;
+    for (int bn : {192, 160})
+        if (cost(bn) < cost(best)) best = bn;
+    return best;
+}
+
 void gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M % BM || g.N % 128 || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
         throw std::invalid_argument("gemm: M%128, N%128, K%64 must be 0 (M=" + std::to_string(g.M) +
@@ -680,7 +710,21 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     const bool full = g.M % 256 == 0 && g.N % 256 == 0;
     const bool pair_ok = full || (g.M >= 256 && g.N >= 256 && g.epi != EPI_RESID && g.epi != EPI_DGELU);
     const int cg = g_force_cg > 0 ? (pair_ok ? g_force_cg : 1) : (pair_ok ? 2 : 1);
-    if (cg == 2)
+    const bool f_pass = !g.a_mn && !g.b_mn && (g.epi == EPI_STORE || g.epi == EPI_GELU || g.epi == EPI_RESID);
+    const int fbn = cg == 2 && f_pass && g.M % 256 == 0 ? gemm_f_bn(g.M, g.N) : 256;
+    if (cg == 2 && fbn == 192) {
+        switch (g.epi) {
+            case EPI_STORE: return launch<192, false, false, EPI_STORE, 2>(g, s);
+            case EPI_GELU: return launch<192, false, false, EPI_GELU, 2>(g, s);
+            default: return launch<192, false, false, EPI_RESID, 2>(g, s);
+        }
+    } else if (cg == 2 && fbn == 160) {
+        switch (g.epi) {
+            case EPI_STORE: return launch<160, false, false, EPI_STORE, 2>(g, s);
+            case EPI_GELU: return launch<160, false, false, EPI_GELU, 2>(g, s);
+            default: return launch<160, false, false, EPI_RESID, 2>(g, s);
+        }
+    } else if (cg == 2)
         dispatch<256, 2>(g, s);
     else if (gemm_bn(g) == 256)
         dispatch<256, 1>(g, s);

@@ -160,3 +160,38 @@ def test_half_empty_last_tile(M, N, Kd):
     assert rel(C, A.float() @ W.float().t()) < 4e-3
     assert (guard[M:, :] == 7.0).all() and (guard[:, N:] == 7.0).all()  # nothing written outside
     assert rel(D, Wt.float().t() @ X.float()) < 1e-4 * max(1.0, Kd / 64)
+
+
+@pytest.mark.parametrize("bn", [192, 160])
+@pytest.mark.parametrize("M,N,Kd", [(512, 2048, 256), (256, 6144, 128), (768, 1024, 320), (256, 384, 64)])
+@pytest.mark.parametrize("epi", ["store", "gelu", "resid"])
+def test_forward_narrow_tiles(cta_group, bn, M, N, Kd, epi):
+    """F-pass pair GEMMs on 256 x 192 / 256 x 160 tiles (gemm_f_bn): partial last column tile,
+    GELU and residual epilogues."""
+    if cta_group != 2:
+        pytest.skip("narrow tiles are a CTA-pair variant")
+    g = torch.Generator(device="cuda").manual_seed(3 * M + N + bn)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16()
+    C = torch.full((M, N + 64), 7.0, device="cuda", dtype=torch.bfloat16)  # padded: nothing past N is written
+    C2 = torch.full((M, N + 64), 7.0, device="cuda", dtype=torch.bfloat16)
+    aux = torch.randn(M, N + 64, device="cuda", generator=g).bfloat16()
+    K.set_tile_n(bn)
+    try:
+        if epi == "store":
+            K.gemm(A, W, C[:, :N])
+        elif epi == "gelu":
+            K.gemm(A, W, C[:, :N], epi=1, C2=C2[:, :N])
+        else:
+            K.gemm(A, W, C[:, :N], epi=2, aux=aux[:, :N])
+        torch.cuda.synchronize()
+    finally:
+        K.set_tile_n(0)
+    ref = A.float() @ W.float().t()
+    if epi == "resid":
+        ref = ref + aux[:, :N].float()
+    assert rel(C[:, :N], ref) < 4e-3
+    assert bool((C[:, N:] == 7.0).all())
+    if epi == "gelu":
+        assert rel(C2[:, :N], gelu(C[:, :N].float())) < 4e-3
+        assert bool((C2[:, N:] == 7.0).all())
