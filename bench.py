@@ -204,6 +204,21 @@ def workload_name(args, sched):
 
 
 # ---------------------------------------------------------------- our arm
+def transfer_summary(gathered):
+    """Stage-boundary activation / gradient pulls of the timeline step: bytes and copy-engine time per
+    device (CUDA events around each cudaMemcpyAsync on the copy stream), achieved GB/s.  The link is
+    NVLink P2P when the ranks sit on different GPUs; ranks sharing one GPU measure a local HBM copy."""
+    pb_, ms_ = sum(g[4] for g in gathered), sum(g[5] for g in gathered)
+    if pb_ == 0:
+        return None
+    uuids = {str(g[6]) for g in gathered}
+    return {"bytes_per_step": int(pb_), "copy_ms_per_step": ms_,
+            "achieved_gbps": pb_ / (ms_ * 1e-3) / 1e9 if ms_ > 0 else None,
+            "per_device_gbps": [g[4] / (g[5] * 1e-3) / 1e9 if g[5] > 0 else None for g in gathered],
+            "link": "nvlink-p2p" if len(uuids) == len(gathered) else "same-gpu (ranks share a device; not NVLink)",
+            "peak_gbps_per_direction": 900.0}
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -316,9 +331,11 @@ def main():
     loss = tst.loss
     if world > 1:
         gathered = [None] * world
-        dist.all_gather_object(gathered, ([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss))
+        dist.all_gather_object(gathered, ([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss,
+                                          tst.peer_bytes, tst.copy_ms, torch.cuda.get_device_properties(local).uuid))
     else:
-        gathered = [([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss)]
+        gathered = [([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss, tst.peer_bytes, tst.copy_ms,
+                     None)]
 
     # ---- GEMM roofline: one more step with CUDA events around every GEMM launch (compute stream)
     barrier()
@@ -408,6 +425,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "def": "pb_exec_step with pinned host tokens/labels, wall clock"},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "transfer": transfer_summary(gathered),
         "cpu_baseline": cpu,
         "reference_schedule": reference_schedule_time(sched_name, p, m),
     }

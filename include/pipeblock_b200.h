@@ -224,6 +224,8 @@ typedef struct pb_exec_stats {
     double gemm_ms;         /* PB_FLAG_GEMM_TIMING: summed GEMM launch durations (CUDA events, compute stream) */
     double gemm_flops;      /* algorithmic FLOPs of those GEMMs (2*M*N*K each) */
     int64_t gemm_launches;
+    double copy_ms;         /* summed durations of this device's stage-boundary pulls (CUDA events on the
+                               copy stream); peer_bytes / copy_ms = achieved transfer bandwidth */
 } pb_exec_stats;
 
 typedef struct pb_exec pb_exec;

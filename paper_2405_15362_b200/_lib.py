@@ -49,7 +49,7 @@ class pb_exec_stats(C.Structure):
     _fields_ = [("loss", C.c_double), ("step_ms", C.c_double), ("busy_ms", C.c_double), ("pool_slots", C.c_int64),
                 ("pool_peak", C.c_int64), ("slot_bytes", C.c_int64), ("pool_bytes", C.c_int64),
                 ("peer_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("gemm_ms", C.c_double),
-                ("gemm_flops", C.c_double), ("gemm_launches", C.c_int64)]
+                ("gemm_flops", C.c_double), ("gemm_launches", C.c_int64), ("copy_ms", C.c_double)]
 
 
 # every symbol include/pipeblock_b200.h declares (checked by tests/test_capi.py)

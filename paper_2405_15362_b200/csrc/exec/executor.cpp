@@ -292,11 +292,15 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
     ev_end.resize(ops.size());
     ev_pull.resize(ops.size());
     ev_free.resize(ops.size());
+    ev_copy0.resize(ops.size());
+    ev_copy1.resize(ops.size());
     for (size_t i = 0; i < ops.size(); ++i) {
         ck(cudaEventCreate(&ev_start[i]), "event");
         ck(cudaEventCreate(&ev_end[i]), "event");
         ck(cudaEventCreateWithFlags(&ev_pull[i], cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming), "event");
+        ck(cudaEventCreate(&ev_copy0[i]), "event");
+        ck(cudaEventCreate(&ev_copy1[i]), "event");
     }
     ck(cudaEventCreate(&ev_step0), "event");
     ck(cudaEventCreate(&ev_step1), "event");
@@ -309,7 +313,7 @@ Exec::~Exec() {
     cudaSetDevice(cuda);
     cudaDeviceSynchronize();
     for (auto& kv : wgroups) pbk::gemm_group_destroy(kv.second);
-    for (auto* v : {&ev_start, &ev_end, &ev_pull, &ev_free})
+    for (auto* v : {&ev_start, &ev_end, &ev_pull, &ev_free, &ev_copy0, &ev_copy1})
         for (auto e : *v) cudaEventDestroy(e);
     for (auto e : gev) cudaEventDestroy(e);
     for (auto e : kev) cudaEventDestroy(e);
@@ -583,6 +587,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     pbk::gemm_allow_stream_k(isolate || !shares_gpu);
     launches = 0;
     peer_bytes = 0;
+    copied.assign(plan.dev_ops[dev].size(), 0);
     gev_used = 0;
     kev_used = 0;
     gemm_flops_acc = 0;
@@ -631,9 +636,12 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
             } else {
                 wait_value(xs, ready_flag(flags, in->src_dev, in->outbox), g);
             }
+            ck(cudaEventRecord(ev_copy0[j], xs), "event");
             ck(cudaMemcpyAsync(in_dst, reinterpret_cast<uint8_t*>(src.outbox) + size_t(in->outbox) * msg_bytes,
                                size_t(T) * h * 2, cudaMemcpyDeviceToDevice, xs),
                "peer copy");
+            ck(cudaEventRecord(ev_copy1[j], xs), "event");
+            copied[j] = 1;
             if (group) {
                 ck(cudaEventRecord(group->ack_ev[t & 1][mi], xs), "event");
                 group->set(group->ack_step, mi, t);
@@ -757,6 +765,14 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
         st->slot_bytes = int64_t(slot_bytes);
         st->pool_bytes = int64_t(slot_bytes) * nslots + int64_t(head_bytes) * nhead;
         st->peer_bytes = peer_bytes;
+        double cms = 0;  // stage-boundary pulls: copy-engine time on the copy stream (CUDA events)
+        for (size_t j = 0; j < copied.size(); ++j)
+            if (copied[j]) {
+                float t = 0;
+                ck(cudaEventElapsedTime(&t, ev_copy0[j], ev_copy1[j]), "elapsed");
+                cms += t;
+            }
+        st->copy_ms = cms;
         st->kernel_launches = launches;
         double gms = 0;
         for (size_t i = 0; i + 1 < gev_used; i += 2) {

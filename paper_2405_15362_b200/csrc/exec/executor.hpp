@@ -152,7 +152,8 @@ class Exec {
     float *dsum = nullptr, *dq_acc = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
     int32_t *tokens = nullptr, *labels = nullptr;
     std::vector<void*> allocations;
-    std::vector<cudaEvent_t> ev_start, ev_end, ev_pull, ev_free;
+    std::vector<cudaEvent_t> ev_start, ev_end, ev_pull, ev_free, ev_copy0, ev_copy1;
+    std::vector<uint8_t> copied;  // this step: op j pulled its input from a peer
     cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
     std::vector<Peer> peers;
     std::vector<int> pos_of;

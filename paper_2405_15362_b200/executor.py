@@ -91,11 +91,12 @@ class StepStats:
     gemm_ms: float = 0.0
     gemm_flops: float = 0.0
     gemm_launches: int = 0
+    copy_ms: float = 0.0
 
     @staticmethod
     def of(s: pb_exec_stats) -> "StepStats":
         return StepStats(s.loss, s.step_ms, s.busy_ms, s.pool_slots, s.pool_peak, s.slot_bytes, s.pool_bytes,
-                         s.peer_bytes, s.kernel_launches, s.gemm_ms, s.gemm_flops, s.gemm_launches)
+                         s.peer_bytes, s.kernel_launches, s.gemm_ms, s.gemm_flops, s.gemm_launches, s.copy_ms)
 
 
 def _i32(x) -> C.POINTER(C.c_int32):

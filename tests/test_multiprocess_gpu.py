@@ -30,6 +30,9 @@ def test_bench_torchrun_shared_gpu(n, sched):
     assert line["n_gpus"] == n and line["value"] > 0
     assert 0 <= line["bubble_rate"] < 1
     assert line["activation_memory"]["measured_slots_max"] == max(line["activation_memory"]["predicted_slots_per_device"])
+    tr = line["transfer"]  # every stage crossing pulled once per step, timed on the copy stream
+    assert tr["bytes_per_step"] > 0 and tr["copy_ms_per_step"] > 0 and tr["achieved_gbps"] > 0
+    assert tr["link"].startswith("same-gpu")
 
 
 def test_ipc_step_matches_in_process():
