@@ -23,7 +23,7 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
  * where M and N allow it, -1 = automatic (default). Process-wide; for tests and benchmarks. */
 int pbt_gemm_set_cta_group(int32_t cg);
 int pbt_gemm_set_tile_n(int32_t bn);  /* F-pass CTA-pair tile width: 0 = per-shape choice, 256 / 192 / 160 */
-/* stream-K split tiles: -1 = environment (PB_STREAMK), 0 off, 1 on */
+/* stream-K split tiles: -1 = environment (PB_STREAMK), 0 off, 1 on, 2 hybrid (whole tiles for the full waves, split ragged last wave) */
 int pbt_gemm_set_stream_k(int32_t on);
 /* causal attention, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T] (base-2 LSE of scaled scores) */
 int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);

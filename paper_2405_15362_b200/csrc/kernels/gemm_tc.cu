@@ -68,6 +68,7 @@ struct KParams {
     uint32_t* sk_flag;
     uint32_t sk_epoch;
     int sk;
+    int sk_dp;  // hybrid: tiles [0, sk_dp) are whole (one per pair, the full waves); stream-K covers the rest
 };
 
 // Resolves tile t of the launch: its problem's descriptors, origin, K blocks, output.
@@ -95,7 +96,7 @@ __device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensor
 struct SegIter {
     long long u, u1;  // stream-K
     int nk;
-    int t, step, num_tiles;  // whole tiles
+    int t, step, num_tiles, dp;  // whole tiles
     bool sk;
     __device__ SegIter(const KParams& p, int num_tiles_, int cid, int ncl) {
         sk = p.sk != 0;
@@ -103,13 +104,14 @@ struct SegIter {
         t = cid;
         step = ncl;
         nk = p.K / BK;
-        const long long U = (long long)num_tiles * nk;
+        dp = sk ? p.sk_dp : 0;
+        const long long U = (long long)(num_tiles - dp) * nk;
         u = U * cid / ncl;
         u1 = U * (cid + 1) / ncl;
     }
     __device__ bool next(int& tile, int& kb0, int& kb1) {
-        if (!sk) {
-            if (t >= num_tiles) return false;
+        if (!sk || t < dp) {
+            if (t >= (sk ? dp : num_tiles)) return false;
             tile = t;
             kb0 = 0;
             kb1 = -1;  // whole tile (resolved per problem)
@@ -117,10 +119,11 @@ struct SegIter {
             return true;
         }
         if (u >= u1) return false;
-        tile = int(u / nk);
-        const long long end = u1 < (long long)(tile + 1) * nk ? u1 : (long long)(tile + 1) * nk;
-        kb0 = int(u - (long long)tile * nk);
-        kb1 = int(end - (long long)tile * nk);
+        tile = dp + int(u / nk);
+        const long long ts = (long long)(tile - dp) * nk;  // first unit of this tile
+        const long long end = u1 < ts + nk ? u1 : ts + nk;
+        kb0 = int(u - ts);
+        kb1 = int(end - ts);
         u = end;
         return true;
     }
@@ -285,7 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         SegIter it(p, num_tiles, cid, ncl);
         int t, kb0, kb1;
         const int nk = p.K / BK;
-        const long long U = (long long)num_tiles * nk;
+        const int sk_dp = p.sk ? p.sk_dp : 0;
+        const long long U = (long long)(num_tiles - sk_dp) * nk;
         while (it.next(t, kb0, kb1)) {
             const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
             const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN;
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // stream-K owner of a split tile: pairs cid+1 .. whose ranges start inside this tile contributed
             int c_last = cid;
             if (kb1 >= 0 && kb1 < nk) {
-                while (c_last + 1 < ncl && U * (c_last + 1) / ncl < (long long)(t + 1) * nk) ++c_last;
+                while (c_last + 1 < ncl && U * (c_last + 1) / ncl < (long long)(t - sk_dp + 1) * nk) ++c_last;
                 for (int c = cid + 1; c <= c_last; ++c) {
                     const uint32_t* f = p.sk_flag + size_t(c) * CG + rank;
                     uint32_t e;
@@ -525,13 +529,14 @@ SkWorkspace& sk_workspace(cudaStream_t s) {
 thread_local bool t_sk_allowed = true;
 // Off by default: on the 1.5B step it measured slower in-step (57k vs 70k tokens/s) although
 // isolated launches are on par; PB_STREAMK=1 enables it.
-int g_force_sk = -1;  // tests: -1 environment, 0 off, 1 on
-bool sk_enabled() {
-    static const bool on = [] {
+int g_force_sk = -1;  // tests: -1 environment, 0 off, 1 stream-K, 2 hybrid
+int sk_enabled() {
+    static const int on = [] {
         const char* e = std::getenv("PB_STREAMK");
-        return e && e[0] == '1';
+        return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
     }();
-    return (g_force_sk < 0 ? on : g_force_sk == 1) && t_sk_allowed;
+    if (!t_sk_allowed) return 0;
+    return g_force_sk < 0 ? on : g_force_sk;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
@@ -547,17 +552,21 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
-               nullptr, nullptr, 0, 0};
+               nullptr, nullptr, 0, 0, 0};
     const int tiles = ((g.M + BM * CG - 1) / (BM * CG)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
     int grid = (tiles < slots ? tiles : slots) * CG;
     // stream-K when whole tiles would leave a ragged last wave (and a k split is possible)
     // (>= 2 k-blocks of work per pair, so no pair's range is empty: an owner waits on every pair
     // whose range starts inside its tile)
-    if (sk_enabled() && tiles % slots != 0 && tiles < 8 * slots && g.K / BK >= 4 &&
-        (long long)tiles * (g.K / BK) >= 2LL * slots) {
+    // hybrid (PB_STREAMK=2): the full waves run whole tiles, only the ragged last wave is split
+    const int sk_mode = sk_enabled();
+    const int dp = sk_mode == 2 ? (tiles / slots) * slots : 0;
+    if (sk_mode && tiles % slots != 0 && tiles < 8 * slots && g.K / BK >= 4 &&
+        (long long)(tiles - dp) * (g.K / BK) >= 2LL * slots) {
         SkWorkspace& w = sk_workspace(s);
         kp.sk = 1;
+        kp.sk_dp = dp;
         kp.sk_ws = w.ws;
         kp.sk_flag = w.flags;
         kp.sk_epoch = ++w.epoch;
@@ -653,7 +662,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     }();
     (void)attr;
     KParams kp{0, 0, 0, nullptr, nullptr, nullptr, 0, 0, g.accumulate,
-               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, nullptr, 0, 0};
+               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, nullptr, 0, 0, 0};
     const int slots = sm_count() / 2;
     const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
     CUtensorMap dummy{};

@@ -100,10 +100,10 @@ def test_rejects_bad_shapes():
 
 
 # pass shapes whose tile count leaves a ragged last wave on 74 CTA pairs -> stream-K split tiles
-SK_SHAPES = [(2048, 2048, 8192), (2048, 2048, 2048), (2048, 6144, 2048), (2048, 8192, 2048), (4096, 2048, 512)]
+SK_SHAPES = [(2048, 2048, 8192), (2048, 2048, 2048), (2048, 6144, 2048), (2048, 8192, 2048), (4096, 2048, 512), (4096, 2048, 8192), (4096, 6144, 2048)]
 
 
-@pytest.fixture(params=[0, 1], ids=["tiles", "streamk"])
+@pytest.fixture(params=[0, 1, 2], ids=["tiles", "streamk", "hybrid"])
 def stream_k(request):
     K.set_stream_k(request.param)
     yield request.param
