@@ -332,7 +332,7 @@ def main():
     if world > 1:
         gathered = [None] * world
         dist.all_gather_object(gathered, ([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss,
-                                          tst.peer_bytes, tst.copy_ms, torch.cuda.get_device_properties(local).uuid))
+                                          tst.peer_bytes, tst.copy_ms, str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)))
     else:
         gathered = [([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss, tst.peer_bytes, tst.copy_ms,
                      None)]

@@ -191,3 +191,32 @@ def test_vocab_half_tile_matches_oracle():
     assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
     for n in ex.params():
         assert N.rel_l2(ex.get(n, "grad"), grads_ref[n].numpy().ravel()) < GRAD_REL_L2, n
+
+
+CFG16 = ModelConfig(layers=16, hidden=256, heads=2, seq=256, vocab=1024, micro_batch=1, optimizer=False)
+
+
+@pytest.mark.parametrize("entry,p,m,cfg", [
+    ("zb-h2", 2, 8, CFG), ("gpipe", 2, 8, CFG), ("eager-1f1b", 2, 8, CFG),   # other straight gallery entries
+    ("v-half", 2, 1, CFG), ("v-zb", 4, 3, CFG), ("v-min", 2, 5, CFG),       # m = 1 and m not a multiple of p
+    ("v-half", 8, 8, CFG16), ("v-zb", 8, 8, CFG16), ("1f1b", 8, 8, CFG16),  # p = 8: 16 V stages of one layer
+])
+def test_more_schedules_match_oracle(entry, p, m, cfg):
+    """Executor parity beyond the main sweep: the straight zb-h2 / gpipe / eager-1f1b entries,
+    microbatch counts below or not divisible by p, and p = 8 (all pipeline devices on one GPU)."""
+    sched = pb.assemble(pb.build_entry(entry, p), m)
+    S = sched.topology.num_stages
+    ex = PipelineExecutor(cfg, sched)
+    tokens, labels = synthetic_batch(cfg, m)
+    res = ex.step(tokens, labels)
+    names = list(ex.params())
+    w = {n: torch.from_numpy(ex.get(n, "weight").reshape(N.shapes(cfg, S)[n])) for n in names}
+    loss_ref, grads_ref = N.reference_step(w, tokens, labels, cfg, S)
+    assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
+    for n in names:
+        g, r = ex.get(n, "grad"), grads_ref[n].numpy().ravel()
+        assert N.rel_l2(g, r) < GRAD_REL_L2, (n, N.rel_l2(g, r))
+        assert N.cosine(g, r) > GRAD_COS, (n, N.cosine(g, r))
+    peaks = pb.exact_peak(sched)
+    for d, st in res.per_device.items():
+        assert st.pool_slots == int(peaks[d - 1]) and st.pool_peak == int(peaks[d - 1])
