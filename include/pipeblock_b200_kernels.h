@@ -22,7 +22,8 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
 /* Force the GEMM variant: 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2) per 256-row tile
  * where M and N allow it, -1 = automatic (default). Process-wide; for tests and benchmarks. */
 int pbt_gemm_set_cta_group(int32_t cg);
-int pbt_gemm_set_tile_n(int32_t bn);  /* F-pass CTA-pair tile width: 0 = per-shape choice, 256 / 192 / 160 */
+int pbt_gemm_set_tile_n(int32_t bn);
+int pbt_gemm_set_pair_rows(int32_t rows); /* CTA-pair tile rows: 256, 512 (two A sub-tiles per CTA, M % 512 == 0), -1 = PB_GEMM_BM2 */  /* F-pass CTA-pair tile width: 0 = per-shape choice, 256 / 192 / 160 */
 /* stream-K split tiles: -1 = environment (PB_STREAMK), 0 off, 1 on, 2 hybrid (whole tiles for the full waves, split ragged last wave) */
 int pbt_gemm_set_stream_k(int32_t on);
 /* causal attention, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T] (base-2 LSE of scaled scores) */

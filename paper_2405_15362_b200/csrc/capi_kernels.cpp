@@ -118,6 +118,13 @@ extern "C" int pbt_gemm_set_tile_n(int32_t bn) {
     });
 }
 
+extern "C" int pbt_gemm_set_pair_rows(int32_t rows) {
+    return pbx::guard([&] {
+        if (rows != -1 && rows != 256 && rows != 512) throw std::invalid_argument("pair rows must be -1, 256 or 512");
+        pbk::gemm_force_bm2(rows < 0 ? -1 : rows == 512 ? 1 : 0);
+    });
+}
+
 extern "C" int pbt_gemm_set_stream_k(int32_t on) {
     return pbx::guard([&] { pbk::gemm_force_stream_k(on); });
 }

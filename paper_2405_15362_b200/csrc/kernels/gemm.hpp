@@ -56,6 +56,7 @@ int gemm_bn(const GemmArgs& g);
 int num_sms();
 // tests: force the 1-CTA (1) or CTA-pair (2) variant where shapes allow; -1 = automatic
 void gemm_force_cta_group(int cg);
+void gemm_force_bm2(int on);  // tests: 512 x 256 CTA-pair tiles, -1 = PB_GEMM_BM2
 void gemm_force_bn(int bn);  // tests: F-pass pair tile width, 0 = per-shape choice (gemm_f_bn)
 int gemm_f_bn(int M, int N);
 // 2-D bf16 tensor map [outer][inner], row stride ld elements, box_inner x box_outer, 128B swizzle

@@ -34,15 +34,20 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-template <int BN, int CG>
+// BM2 = 2: each CTA holds TWO 128-row A sub-tiles (a CTA pair covers 512 x BN) sharing one B
+// stage, and the two accumulators fill all 512 TMEM columns (single-buffered): a quarter less
+// operand traffic per FLOP than BM2 = 1 (48 KB per 2 x 4.2 MFLOP instead of 32 KB per 4.2).
+template <int BN, int CG, int BM2 = 1>
 struct Cfg {
     static constexpr int kBRows = BN / CG;  // B rows (N) held by each CTA of the pair
-    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kABytes = BM * BK * 2 * BM2;
     static constexpr int kBBytes = kBRows * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
     static constexpr int kAccStride = BN <= 128 ? 128 : 256;  // accumulator buffer pitch (TMEM columns)
-    static constexpr int kTmemCols = 2 * kAccStride;           // double-buffered accumulator (power of 2)
+    static constexpr int kAccBufs = BM2 == 2 ? 1 : 2;          // double-buffered unless BM2 fills TMEM
+    static constexpr int kTmemCols = 2 * kAccStride;           // (power of 2)
+    static_assert(BM2 == 1 || (BN == 256 && CG == 2), "BM2 = 2 is a CTA-pair 512 x 256 tile");
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -78,11 +83,11 @@ struct TileRef {
     void* C;
     int m_blk, n_blk, num_k, ldc;
 };
-template <int BN, int CG>
+template <int BN, int CG, int BM2 = 1>
 __device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int t,
                                                 int& cursor) {
     if (p.group == nullptr) {
-        const int num_m = (p.M + BM * CG - 1) / (BM * CG);  // the last M / N tile may be half empty
+        const int num_m = (p.M + BM * CG * BM2 - 1) / (BM * CG * BM2);  // the last M / N tile may be half empty
         return TileRef{ta, tb, p.C, t % num_m, t / num_m, p.K / BK, p.ldc};
     }
     while (t >= p.group[cursor].tile0 + p.group[cursor].ntiles) ++cursor;  // tiles visited in increasing order
@@ -132,10 +137,11 @@ struct SegIter {
 // CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (cluster of 2) per
 // 256 x BN tile; each CTA stages its 128 rows of A and BN/2 rows of B, the
 // leader issues tcgen05.mma.cta_group::2 (M=256) and commits to both CTAs.
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, KParams p) {
-    using C_ = Cfg<BN, CG>;
+    using C_ = Cfg<BN, CG, BM2>;
+    constexpr int kPairRows = BM * CG;  // rows of one MMA (both CTAs of a pair)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C_::kStages * C_::kStageBytes);
@@ -147,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = warp_id();
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
-    const int num_tiles = p.group ? p.total_tiles : ((p.M + BM * CG - 1) / (BM * CG)) * ((p.N + BN - 1) / BN);
+    const int num_tiles =
+        p.group ? p.total_tiles : ((p.M + kPairRows * BM2 - 1) / (kPairRows * BM2)) * ((p.N + BN - 1) / BN);
     const int cid = int(blockIdx.x) / CG, ncl = int(gridDim.x) / CG;
 
     if (warp == 0 && elect_one()) {
@@ -183,11 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             SegIter it(p, num_tiles, cid, ncl);
             int t, kb0, kb1;
             while (it.next(t, kb0, kb1)) {
-                const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
+                const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor);
                 const CUtensorMap* pa = tr.ta;
                 const CUtensorMap* pb = tr.tb;
                 const int num_k = kb1 < 0 ? tr.num_k : kb1;
-                const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN + int(rank) * C_::kBRows;
+                const int m0 = tr.m_blk * kPairRows * BM2 + int(rank) * BM, n0 = tr.n_blk * BN + int(rank) * C_::kBRows;
                 for (int kb = kb0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * C_::kStageBytes;
@@ -195,11 +202,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int k0 = kb * BK;
                     if constexpr (CG == 1) {
                         mbar_expect_tx(&full[stage], C_::kStageBytes);
-                        if constexpr (A_MN) {
-                            tma_load_2d(sa, pa, &full[stage], m0, k0);
-                            tma_load_2d(sa + 8192, pa, &full[stage], m0 + 64, k0);
-                        } else {
-                            tma_load_2d(sa, pa, &full[stage], k0, m0);
+#pragma unroll
+                        for (int s2 = 0; s2 < BM2; ++s2) {
+                            if constexpr (A_MN) {
+                                tma_load_2d(sa + s2 * 16384, pa, &full[stage], m0 + s2 * kPairRows, k0);
+                                tma_load_2d(sa + s2 * 16384 + 8192, pa, &full[stage], m0 + s2 * kPairRows + 64, k0);
+                            } else {
+                                tma_load_2d(sa + s2 * 16384, pa, &full[stage], k0, m0 + s2 * kPairRows);
+                            }
                         }
                         if constexpr (B_MN) {
 #pragma unroll
@@ -214,11 +224,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // complete (the peer waited on `empty`, released after it was consumed)
                         const uint32_t bar = map_peer(smem_u32(&full[stage]), 0);
                         if (leader) mbar_expect_tx(&full[stage], CG * C_::kStageBytes);
-                        if constexpr (A_MN) {
-                            tma_load_2d_2sm(sa, pa, bar, m0, k0);
-                            tma_load_2d_2sm(sa + 8192, pa, bar, m0 + 64, k0);
-                        } else {
-                            tma_load_2d_2sm(sa, pa, bar, k0, m0);
+#pragma unroll
+                        for (int s2 = 0; s2 < BM2; ++s2) {
+                            if constexpr (A_MN) {
+                                tma_load_2d_2sm(sa + s2 * 16384, pa, bar, m0 + s2 * kPairRows, k0);
+                                tma_load_2d_2sm(sa + s2 * 16384 + 8192, pa, bar, m0 + s2 * kPairRows + 64, k0);
+                            } else {
+                                tma_load_2d_2sm(sa + s2 * 16384, pa, bar, k0, m0 + s2 * kPairRows);
+                            }
                         }
                         if constexpr (B_MN) {
 #pragma unroll
@@ -244,10 +257,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             SegIter it(p, num_tiles, cid, ncl);
             int t, kb0, kb1;
             while (it.next(t, kb0, kb1)) {
-                const int num_k = kb1 < 0 ? resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor).num_k : kb1;
+                const int num_k = kb1 < 0 ? resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor).num_k : kb1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * C_::kAccStride;
+                const uint32_t d_tmem = tmem_base + acc * C_::kAccStride;  // (BM2 = 2: sub-tile s2 at + s2 * 256)
                 for (int kb = kb0; kb < num_k; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -256,13 +269,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t sb = sa + C_::kABytes;
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k) {
-                            const uint64_t ad = A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
                             const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
                             const bool accum = kb != kb0 || k != 0;
-                            if constexpr (CG == 1)
-                                tc_mma(d_tmem, ad, bd, idesc, accum);
-                            else
-                                tc_mma2(d_tmem, ad, bd, idesc, accum);
+#pragma unroll
+                            for (int s2 = 0; s2 < BM2; ++s2) {
+                                const uint32_t sa2 = sa + s2 * 16384;
+                                const uint64_t ad = A_MN ? sdesc(sa2 + k * 2048, 8192, 1024) : sdesc(sa2 + k * 32, 16, 1024);
+                                if constexpr (CG == 1)
+                                    tc_mma(d_tmem + s2 * 256, ad, bd, idesc, accum);
+                                else
+                                    tc_mma2(d_tmem + s2 * 256, ad, bd, idesc, accum);
+                            }
                         }
                         if constexpr (CG == 1) {
                             tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
@@ -275,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (++stage == C_::kStages) stage = 0, phase ^= 1;
                 }
-                if (++acc == 2) acc = 0, acc_phase ^= 1;
+                if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
             }
         }
     } else {
@@ -291,21 +308,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sk_dp = p.sk ? p.sk_dp : 0;
         const long long U = (long long)(num_tiles - sk_dp) * nk;
         while (it.next(t, kb0, kb1)) {
-            const TileRef tr = resolve_tile<BN, CG>(p, &tma_a, &tma_b, t, cursor);
-            const int m0 = tr.m_blk * BM * CG + int(rank) * BM, n0 = tr.n_blk * BN;
+            const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor);
+            const int m0 = tr.m_blk * kPairRows * BM2 + int(rank) * BM, n0 = tr.n_blk * BN;
             void* const Cout = tr.C;
             const int ldc = tr.ldc;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = m0 + row_in_tile;
-            const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * C_::kAccStride;
+            const int row0 = m0 + row_in_tile;
+            const uint32_t tbase0 = tmem_base + ((q * 32) << 16) + acc * C_::kAccStride;
             if (kb1 >= 0 && kb0 > 0) {
                 // stream-K contributor (this pair's first segment): park the partial tile, publish
                 float* slot = p.sk_ws + (size_t(cid) * CG + rank) * (BM * BN) + size_t(row_in_tile) * BN;
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 32) {
                     float v[32];
-                    tmem_ld32(tbase + c, v);
+                    tmem_ld32(tbase0 + c, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
@@ -326,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flag + size_t(cid) * CG + rank),
                                  "r"(p.sk_epoch)
                                  : "memory");
-                if (++acc == 2) acc = 0, acc_phase ^= 1;
+                if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
                 continue;
             }
             // stream-K owner of a split tile: pairs cid+1 .. whose ranges start inside this tile contributed
@@ -344,6 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             // residual / pre-activation operand of the next 32 columns is loaded one chunk ahead
             // (each element is read and written by the same thread, so C may alias aux)
             constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_DGELU;
+#pragma unroll 1
+            for (int s2 = 0; s2 < BM2; ++s2) {  // BM2 = 2: the CTA's second 128-row sub-tile is 256 rows on
+            const int row = row0 + s2 * kPairRows;
+            const uint32_t tbase = tbase0 + s2 * 256;
             uint4 aux_next[4];
             // (aux epilogues run only on full tiles: layer GEMMs have M = tokens, N = h or 4h)
             if constexpr (kAux) {
@@ -432,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            }  // s2
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) {
@@ -440,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                     mbar_arrive_cluster(map_peer(smem_u32(&tempty[acc]), 0));
             }
-            if (++acc == 2) acc = 0, acc_phase ^= 1;
+            if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
         }
     }
     tc_fence_before();
@@ -539,10 +561,10 @@ int sk_enabled() {
     return g_force_sk < 0 ? on : g_force_sk;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2 = 1>
 void launch(const GemmArgs& g, cudaStream_t s) {
-    using C_ = Cfg<BN, CG>;
-    auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
+    using C_ = Cfg<BN, CG, BM2>;
+    auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, CG, BM2>;
     static bool attr = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
         if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
@@ -553,7 +575,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
                nullptr, nullptr, 0, 0, 0};
-    const int tiles = ((g.M + BM * CG - 1) / (BM * CG)) * ((g.N + BN - 1) / BN);
+    const int tiles = ((g.M + BM * CG * BM2 - 1) / (BM * CG * BM2)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
     int grid = (tiles < slots ? tiles : slots) * CG;
     // stream-K when whole tiles would leave a ragged last wave (and a k split is possible)
@@ -562,7 +584,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     // hybrid (PB_STREAMK=2): the full waves run whole tiles, only the ragged last wave is split
     const int sk_mode = sk_enabled();
     const int dp = sk_mode == 2 ? (tiles / slots) * slots : 0;
-    if (sk_mode && tiles % slots != 0 && tiles < 8 * slots && g.K / BK >= 4 &&
+    if (BM2 == 1 && sk_mode && tiles % slots != 0 && tiles < 8 * slots && g.K / BK >= 4 &&
         (long long)(tiles - dp) * (g.K / BK) >= 2LL * slots) {
         SkWorkspace& w = sk_workspace(s);
         kp.sk = 1;
@@ -575,30 +597,30 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, CG, ta, tb, kp);
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int BM2 = 1>
 void dispatch(const GemmArgs& g, cudaStream_t s) {
     if (!g.a_mn && !g.b_mn) {
         switch (g.epi) {
-            case EPI_STORE: return launch<BN, false, false, EPI_STORE, CG>(g, s);
-            case EPI_GELU: return launch<BN, false, false, EPI_GELU, CG>(g, s);
-            case EPI_RESID: return launch<BN, false, false, EPI_RESID, CG>(g, s);
-            case EPI_F32: return launch<BN, false, false, EPI_F32, CG>(g, s);
+            case EPI_STORE: return launch<BN, false, false, EPI_STORE, CG, BM2>(g, s);
+            case EPI_GELU: return launch<BN, false, false, EPI_GELU, CG, BM2>(g, s);
+            case EPI_RESID: return launch<BN, false, false, EPI_RESID, CG, BM2>(g, s);
+            case EPI_F32: return launch<BN, false, false, EPI_F32, CG, BM2>(g, s);
             default: break;
         }
     } else if (!g.a_mn && g.b_mn) {
         switch (g.epi) {
-            case EPI_STORE: return launch<BN, false, true, EPI_STORE, CG>(g, s);
-            case EPI_DGELU: return launch<BN, false, true, EPI_DGELU, CG>(g, s);
-            case EPI_RESID: return launch<BN, false, true, EPI_RESID, CG>(g, s);
-            case EPI_F32: return launch<BN, false, true, EPI_F32, CG>(g, s);
+            case EPI_STORE: return launch<BN, false, true, EPI_STORE, CG, BM2>(g, s);
+            case EPI_DGELU: return launch<BN, false, true, EPI_DGELU, CG, BM2>(g, s);
+            case EPI_RESID: return launch<BN, false, true, EPI_RESID, CG, BM2>(g, s);
+            case EPI_F32: return launch<BN, false, true, EPI_F32, CG, BM2>(g, s);
             default: break;
         }
     } else if (g.a_mn && g.b_mn) {
-        if (g.epi == EPI_F32) return launch<BN, true, true, EPI_F32, CG>(g, s);
-        if (g.epi == EPI_STORE) return launch<BN, true, true, EPI_STORE, CG>(g, s);
+        if (g.epi == EPI_F32) return launch<BN, true, true, EPI_F32, CG, BM2>(g, s);
+        if (g.epi == EPI_STORE) return launch<BN, true, true, EPI_STORE, CG, BM2>(g, s);
     } else {
-        if (g.epi == EPI_F32) return launch<BN, true, false, EPI_F32, CG>(g, s);
-        if (g.epi == EPI_STORE) return launch<BN, true, false, EPI_STORE, CG>(g, s);
+        if (g.epi == EPI_F32) return launch<BN, true, false, EPI_F32, CG, BM2>(g, s);
+        if (g.epi == EPI_STORE) return launch<BN, true, false, EPI_STORE, CG, BM2>(g, s);
     }
     throw std::invalid_argument("gemm: unsupported operand-major / epilogue combination");
 }
@@ -654,8 +676,8 @@ GemmGroup gemm_group_create(const GemmArgs* probs, int n) {
 
 void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     if (g.n == 0) return;
-    using C_ = Cfg<256, 2>;
-    auto kern = gemm_kernel<256, true, true, EPI_F32, 2>;
+    using C_ = Cfg<256, 2, 1>;
+    auto kern = gemm_kernel<256, true, true, EPI_F32, 2, 1>;
     static bool attr = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
         return true;
@@ -710,6 +732,22 @@ int gemm_f_bn(int M, int N) {
     return best;
 }
 
+// 512 x 256 CTA-pair tiles (BM2 = 2) for full-tile launches (PB_GEMM_BM2=1 or the test hook);
+// a pair's epilogue is then not overlapped with its next tile's main loop.  Off by default:
+// measured at T = 4096 it gains on long-K shapes (FC1 dX, K = 8192: 1399 -> 1454 TFLOP/s; FC2,
+// K = 8192: 1355 -> 1375) but loses more on K = 2048 (FC1 + GELU 1317 -> 1016), where the exposed
+// epilogue is a quarter of the tile; 82.5k vs 86.5k tokens/s in-step with it on everywhere.
+static int g_force_bm2 = -1;  // tests: -1 environment, 0 off, 1 on
+void gemm_force_bm2(int on) { g_force_bm2 = on; }
+static bool use_bm2(const GemmArgs& g) {
+    static const bool env = [] {
+        const char* e = std::getenv("PB_GEMM_BM2");
+        return e && e[0] == '1';
+    }();
+    const bool on = g_force_bm2 < 0 ? env : g_force_bm2 == 1;
+    return on && g.M % 512 == 0 && g.N % 256 == 0 && sk_enabled() == 0;
+}
+
 void gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M % BM || g.N % 128 || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
         throw std::invalid_argument("gemm: M%128, N%128, K%64 must be 0 (M=" + std::to_string(g.M) +
@@ -733,7 +771,9 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
             case EPI_GELU: return launch<160, false, false, EPI_GELU, 2>(g, s);
             default: return launch<160, false, false, EPI_RESID, 2>(g, s);
         }
-    } else if (cg == 2)
+    } else if (cg == 2 && use_bm2(g))
+        dispatch<256, 2, 2>(g, s);
+    else if (cg == 2)
         dispatch<256, 2>(g, s);
     else if (gemm_bn(g) == 256)
         dispatch<256, 1>(g, s);

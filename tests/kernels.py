@@ -107,6 +107,10 @@ def attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads):
     return dqkv
 
 
+def set_pair_rows(rows: int) -> None:
+    _lib.check(_lib.lib().pbt_gemm_set_pair_rows(rows))
+
+
 def set_tile_n(bn: int) -> None:
     _lib.check(_lib.lib().pbt_gemm_set_tile_n(bn))
 

@@ -195,3 +195,43 @@ def test_forward_narrow_tiles(cta_group, bn, M, N, Kd, epi):
     if epi == "gelu":
         assert rel(C2[:, :N], gelu(C[:, :N].float())) < 4e-3
         assert bool((C2[:, N:] == 7.0).all())
+
+
+@pytest.mark.parametrize("M,N,Kd", [(512, 256, 128), (1024, 768, 384), (2048, 2048, 1024), (512, 6144, 512)])
+def test_pair_512_row_tiles(cta_group, M, N, Kd):
+    """512 x 256 CTA-pair tiles (two 128-row A sub-tiles per CTA, accumulators in all 512 TMEM
+    columns): F (store / GELU / residual), B (store / dGELU) and W (fp32 accumulate) operand majors."""
+    if cta_group != 2:
+        pytest.skip("a CTA-pair variant")
+    g = torch.Generator(device="cuda").manual_seed(M + 2 * N + Kd)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16()
+    Wt = W.t().contiguous()
+    R = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    At = A.t().contiguous()
+    X = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    K.set_pair_rows(512)
+    try:
+        u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        gg = torch.empty_like(u)
+        K.gemm(A, W, u, epi=1, C2=gg)
+        res = torch.empty_like(u)
+        K.gemm(A, W, res, epi=2, aux=R)
+        st = torch.empty_like(u)
+        K.gemm(A, Wt, st, b_mn=True)
+        dg = torch.empty_like(u)
+        K.gemm(A, Wt, dg, b_mn=True, epi=3, aux=u)
+        C32 = torch.ones(Kd, N, device="cuda")
+        K.gemm(A, X, C32, a_mn=True, b_mn=True, epi=4, accumulate=1)  # C += A^T X, A stored [M][Kd] = [K][M']
+        torch.cuda.synchronize()
+    finally:
+        K.set_pair_rows(-1)
+    ref = A.float() @ W.float().t()
+    assert rel(u, ref) < 4e-3
+    assert rel(gg, gelu(u.float())) < 4e-3
+    assert rel(res, ref + R.float()) < 4e-3
+    assert rel(st, ref) < 4e-3
+    x = u.float().requires_grad_(True)
+    (gl,) = torch.autograd.grad(gelu(x), x, torch.ones_like(x))
+    assert rel(dg, ref * gl) < 5e-3
+    assert rel(C32, 1 + At.float() @ X.float()) < 1e-4
