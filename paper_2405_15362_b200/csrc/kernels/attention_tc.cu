@@ -1230,6 +1230,214 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
     }
 }
 
+// ------------------------------------------------------------------ forward v3 (two CTAs per SM)
+// Single-buffered per CTA so that TWO CTAs fit on an SM (96 KB smem: Q, K, V; 256 TMEM columns:
+// S / P at [0,128), O at [128,256)): while one CTA runs its softmax the other CTA's S / PV MMAs
+// keep the tensor pipe busy, and one CTA's prologue / epilogue hides under the other's main loop.
+// Per CTA and key tile j:  S(j) = Q K(j)^T -> softmax (thread = query row; P written back over S as
+// bf16 pairs) -> O += P(j) V(j) (A = P from TMEM).  The MMA pipe runs in issue order, so S(j+1)
+// overwrites P(j) only after PV(j) has read it, and when s_full(j) completes PV(j-1) has too (the
+// lazy O rescale needs no extra wait).  The softmax reads S twice (max pass, exp pass) instead of
+// holding 128 scores in registers, which keeps the kernel under 168 registers for 2 CTAs / SM.
+struct Fwd3Smem {
+    static constexpr int q = 0;
+    static constexpr int k = kTile;
+    static constexpr int v = 2 * kTile;
+    static constexpr int bars = 3 * kTile;
+    static constexpr int total = bars + 128 + 1024;
+};
+
+__global__ void __launch_bounds__(192, 2)
+    attn_fwd_tc3_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
+                        float* __restrict__ lse2, int seq, int H, int T, float scale) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd3Smem::bars);
+    uint64_t* q_full = bars + 0;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = bars + 2;  // MMA commit after S(j)
+    uint64_t* v_full = bars + 3;
+    uint64_t* v_empty = bars + 4;  // MMA commit after PV(j)
+    uint64_t* s_full = bars + 5;   // MMA commit after S(j)
+    uint64_t* p_full = bars + 6;   // 4 softmax warps: P(j) in TMEM
+    uint64_t* o_full = bars + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+    const uint32_t warp = warp_id();
+    const int nqb = seq / BQ;
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int qb = nqb - 1 - int(blockIdx.x) / (H * (T / seq));  // heaviest causal tile first (LPT)
+    const int head = hb % H, b = hb / H;
+    const int row0 = b * seq + qb * BQ;
+    const int nkv = qb + 1;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm);
+        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], i == 6 ? 4 : 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<256>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const int cq = head * D, ck = H * D + head * D, cv = 2 * H * D + head * D;
+            mbar_expect_tx(q_full, kTile);
+            tma_load_2d(sm + Fwd3Smem::q, &tm, q_full, cq, row0);
+            tma_load_2d(sm + Fwd3Smem::q + 16384, &tm, q_full, cq + 64, row0);
+            for (int j = 0; j < nkv; ++j) {
+                const int kr = b * seq + j * BK;
+                if (j > 0) mbar_wait(k_empty, (j - 1) & 1);
+                mbar_expect_tx(k_full, kTile);
+                tma_load_2d(sm + Fwd3Smem::k, &tm, k_full, ck, kr);
+                tma_load_2d(sm + Fwd3Smem::k + 16384, &tm, k_full, ck + 64, kr);
+                if (j > 0) mbar_wait(v_empty, (j - 1) & 1);
+                mbar_expect_tx(v_full, kTile);
+                tma_load_2d(sm + Fwd3Smem::v, &tm, v_full, cv, kr);
+                tma_load_2d(sm + Fwd3Smem::v + 16384, &tm, v_full, cv + 64, kr);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t idesc_o = idesc_bf16(128, 128, false, true);
+        const uint32_t sq = smem_u32(sm + Fwd3Smem::q), sk = smem_u32(sm + Fwd3Smem::k);
+        const uint32_t sv = smem_u32(sm + Fwd3Smem::v);
+        mbar_wait(q_full, 0);
+        for (int j = 0; j < nkv; ++j) {
+            mbar_wait(k_full, j & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    tc_mma(tmem, sdesc(sq + o, 16, 1024), sdesc(sk + o, 16, 1024), idesc_s, kk != 0);
+                }
+                tc_commit(s_full);
+                tc_commit(k_empty);
+            }
+            __syncwarp();
+            mbar_wait(p_full, j & 1);
+            mbar_wait(v_full, j & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 128, tmem + kk * 8, sdesc(sv + kk * 2048, 16384, 1024), idesc_o, (j | kk) != 0);
+                tc_commit(v_empty);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) tc_commit(o_full);
+        __syncwarp();
+    } else {
+        const uint32_t q4 = warp & 3;
+        const int r = int(q4 * 32 + lane_id());  // query row in tile == TMEM lane
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const float sl2 = scale * kLog2e;
+        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            mbar_wait(s_full, j & 1);
+            tc_fence_after();
+            const bool diag = j == nkv - 1;
+            // pass 1: row max (8 independent chains)
+            float mx8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float s[32];
+                tmem_ld32(tmem + lane_base + c * 32, s);
+                tmem_ld_wait();
+                if (__builtin_expect(diag, 0)) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (c * 32 + e > r) s[e] = -INFINITY;
+                }
+#pragma unroll
+                for (int e = 0; e < 32; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], s[e]);
+            }
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+            const float m_new = fmaxf(m_used, mx);
+            const bool rescale = (j > 0) && (m_new > m_used + 8.f);
+            if (__any_sync(0xffffffff, rescale)) {  // O stable: s_full(j) implies PV(j-1) retired
+                const float f = rescale ? exp2f(m_used - m_new) : 1.f;
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    float o[32];
+                    tmem_ld32(tmem + lane_base + 128 + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tmem + lane_base + 128 + c * 32, o);
+                }
+                tmem_st_wait();
+                if (rescale) {
+                    l *= f;
+                    m_used = m_new;
+                }
+            }
+            if (j == 0) m_used = m_new;
+            // pass 2: P = exp2(S*c - m) -> bf16 pairs over the consumed S columns [0,64)
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            float s[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + c * 32, s[c]);
+            tmem_ld_wait();  // every S column is in registers before P overwrites [0,64)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (__builtin_expect(diag, 0)) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (c * 32 + e > r) s[c][e] = -INFINITY;
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) {
+                    const float p0 = fast_exp2(fmaf(s[c][2 * e2], sl2, -m_used));
+                    const float p1 = fast_exp2(fmaf(s[c][2 * e2 + 1], sl2, -m_used));
+                    rs8[(2 * e2) & 7] += p0;
+                    rs8[(2 * e2 + 1) & 7] += p1;
+                    pk[e2] = pack_bf16(p0, p1);
+                }
+                tmem_st16u(tmem + lane_base + c * 16, pk);
+            }
+            l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(p_full);
+        }
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        const float inv = 1.f / l;
+        __nv_bfloat16* orow = out + size_t(row0 + r) * (H * D) + head * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float o[32];
+            tmem_ld32(tmem + lane_base + 128 + c * 32, o);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                                    pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+        }
+        lse2[size_t(head) * T + row0 + r] = m_used + log2f(l);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<256>(tmem);
+    }
+}
+
 
 // ------------------------------------------------------------------ forward v2 (two Q tiles per CTA)
 // One CTA per (256 queries = tiles A and B, head, sequence); 320 threads:
@@ -1562,11 +1770,25 @@ void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int 
     // PB_ATTN_FWD=2: the two-Q-tile ping-pong kernel (P in TMEM).  Correct (tested) but measured
     // slower than the single-tile kernel (467 vs 556 TFLOP/s at 2 x 2048 x 16 heads): its
     // softmax -> PV -> S chain per tile is longer than the double-buffered S/P overlap of v1.
-    static const bool v2 = [] {
+    // default: the two-CTA-per-SM kernel (v3) when the grid is at least ~3 CTAs per SM — it trades
+    // per-CTA latency for throughput, so a single short wave (e.g. 256 CTAs) stays on v1.
+    // PB_ATTN_FWD=1 / 2 / 3 forces a kernel.
+    static const int fenv = [] {
         const char* e = std::getenv("PB_ATTN_FWD");
-        return e && e[0] == '2';
+        return e && (e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }();
-    if (!v2 || seq % (2 * BQ)) {
+    const int nblk = seq / BQ * heads * batch;
+    const int fver = fenv ? fenv : (nblk >= 3 * num_sms() ? 3 : 1);
+    const bool v2 = fver == 2;
+    if (fver == 3) {
+        static bool attr3 = [] {
+            cudaFuncSetAttribute(attn_fwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Smem::total);
+            return true;
+        }();
+        (void)attr3;
+        launch_k(attn_fwd_tc3_kernel, dim3(seq / BQ * heads * batch), dim3(192), Fwd3Smem::total, s, 1, tm, out, lse2,
+                 seq, heads, T, 0.08838834764831845f);
+    } else if (!v2 || seq % (2 * BQ)) {
         dim3 grid(seq / BQ * heads * batch);
         static unsigned long long* trace = [] {
             unsigned long long* t = nullptr;

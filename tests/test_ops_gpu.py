@@ -37,7 +37,9 @@ def test_attention_forward(batch, seq, heads):
     assert (got_lse - lse).abs().max().item() < 2e-2
 
 
-@pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16)])
+# (2, 2048, 16) and (1, 4096, 8) are >= 3 CTAs per SM: the default path is the two-CTA-per-SM kernel (v3)
+@pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16),
+                                             (2, 2048, 16), (1, 4096, 8)])
 def test_attention_forward_tcgen05(batch, seq, heads):
     g = torch.Generator(device="cuda").manual_seed(seq * 3 + heads)
     qkv = (2 * torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g)).bfloat16()
@@ -221,3 +223,35 @@ def test_attention_backward_v4_matches_v3(tmp_path):
     H = 4 * 128
     assert torch.equal(outs["3"][:, H:], outs["4"][:, H:])  # dK, dV: same MMAs, same order
     assert rel(outs["4"][:, :H], outs["3"][:, :H]) < 1e-2  # dQ: fp32 reduce order
+
+
+_FWD_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+from tests import kernels as K
+g = torch.Generator(device="cuda").manual_seed(12)
+qkv = (2 * torch.randn(2 * 1024, 3 * 4 * 128, device="cuda", generator=g)).bfloat16()
+out, lse2 = K.attn_fwd_tc(qkv, 2, 1024, 4)
+torch.save((out.cpu(), lse2.cpu()), {path!r})
+"""
+
+
+@pytest.mark.parametrize("ver", ["1", "3"])
+def test_attention_forward_versions_match_reference(tmp_path, ver):
+    """Each forward kernel forced on a small grid (PB_ATTN_FWD=1: double-buffered single CTA per SM;
+    =3: single-buffered, two CTAs per SM) against the fp32 reference."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = str(tmp_path / "o.pt")
+    subprocess.run([sys.executable, "-c", _FWD_SCRIPT.format(root=root, path=path)],
+                   env=dict(os.environ, PB_ATTN_FWD=ver), check=True, timeout=300)
+    out, lse2 = torch.load(path)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    qkv = (2 * torch.randn(2 * 1024, 3 * 4 * 128, device="cuda", generator=g)).bfloat16()
+    ref, lse = ref_attention(qkv, 2, 1024, 4)
+    assert rel(out.cuda(), ref) < 1e-2
+    got = (lse2.cuda() * math.log(2)).view(4, 2, 1024).permute(1, 0, 2)
+    assert (got - lse).abs().max().item() < 2e-2
