@@ -1,4 +1,4 @@
-# final round-1 refresh with attention fwd v3 + bwd v4: tests, smoke, bench, breakdown, launch list, ncu, projections
+# Round-end GPU refresh (one B200): GPU tests, smoke, bench, step breakdown, ncu launch list + full capture, attention table, 1.5B/6B/14B projections -> gpurun_out/f3_*  (profiles/ is written from these)
 set -x
 timeout 1200 python -m pytest tests -m gpu --timeout 300 -q > gpurun_out/f3_pytest.log 2>&1; tail -3 gpurun_out/f3_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
