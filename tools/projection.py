@@ -73,6 +73,7 @@ def main():
                      "replayed in grid order (pb_replay) with comm = msg_bytes/nvlink_gbs + latency",
            "assumptions": {"nvlink_gbs": args.nvlink_gbs, "latency_us": args.latency_us, "msg_bytes": msg_bytes,
                            "comm_ms": comm_ms}, "runs": []}
+    out["power_cap"] = power_cap_factor(args, mcfg)
     for p in args.p:
         for name in args.schedules:
             t0 = time.time()
@@ -119,6 +120,10 @@ def main():
     if args.via_chunks:
         out["method"] = ("probe pipeline with the target's chunk shapes on one B200 (PB_FLAG_ISOLATE pass times, "
                          "mean per chunk class and kind), target schedule replayed with pb_replay")
+    # the same projection at the continuous (power-capped) pass speed
+    f = out["power_cap"]["factor"]
+    for r in out["runs"]:
+        r["projected_tokens_per_s_at_cap"] = r["projected_tokens_per_s"] / f
     # activation memory vs 1F1B at the same p (measured pool bytes, max over devices)
     for r in out["runs"]:
         base = next((b for b in out["runs"] if b["schedule"] == "1f1b" and b["p"] == r["p"]), None)
@@ -130,6 +135,37 @@ def main():
     if args.out:
         with open(args.out, "w") as f:
             f.write(text)
+
+
+def power_cap_factor(args, mcfg):
+    """Isolated passes run one at a time with a synchronise in between, so the GPU sits below its power
+    cap and clocks higher than in a continuous step.  Calibrate: a zb-h1 p=1 pipeline of the same layer
+    shapes (4 layers, real hidden / seq / vocab / micro-batch) runs once isolated and once continuously;
+    factor = continuous makespan / sum of isolated pass times (>= 1 when power-capped)."""
+    import torch
+
+    from paper_2405_15362_b200 import pipeblock as pb
+    from paper_2405_15362_b200.executor import ModelConfig, PipelineExecutor, synthetic_batch
+
+    cfg = ModelConfig(**dict(mcfg, layers=4), micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    m = 16
+    sched = pb.assemble(pb.build_entry("zb-h1", 1), m)
+    tokens, labels = synthetic_batch(cfg, m)
+    tok, lab = torch.from_numpy(tokens).cuda(), torch.from_numpy(labels).cuda()
+    ex = PipelineExecutor(cfg, sched, [0])
+    ex.set_flags(timeline=True)
+    for _ in range(3):
+        ex.step(tok, lab, on_host=False)
+    cont = [ex.step(tok, lab, on_host=False).per_device[1].step_ms for _ in range(3)]
+    ex.set_flags(timeline=True, serial=True)  # one device: a synchronise after every pass = isolated passes
+    ex.step(tok, lab, on_host=False)
+    iso = [sum(q.duration for q in ex.step(tok, lab, on_host=False).timeline) for _ in range(3)]
+    del ex
+    torch.cuda.synchronize()
+    c, i = sorted(cont)[1], sorted(iso)[1]
+    return {"factor": c / i, "continuous_ms": c, "isolated_sum_ms": i,
+            "what": "zb-h1 p=1, 4 layers of this model, m=16: continuous step / sum of isolated pass times "
+                    "(median of 3); projected_tokens_per_s_at_cap = projected / factor"}
 
 
 def chunk_class(stage: int, num_stages: int) -> str:
