@@ -52,6 +52,9 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--via-chunks", action="store_true", help="probe-pipeline projection (see module doc)")
     ap.add_argument("--balance", action="store_true", help="balanced_stage_layers (LM-head stage carries fewer layers)")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="override the model's layer count; with --via-chunks the last stage takes the remainder "
+                         "(e.g. 31 layers on 16 V stages: 2 per stage, 1 on the LM-head stage)")
     args = ap.parse_args()
 
     import torch
@@ -59,7 +62,9 @@ def main():
     from paper_2405_15362_b200 import pipeblock as pb
     from paper_2405_15362_b200.executor import ModelConfig, PipelineExecutor, synthetic_batch
 
-    mcfg = CONFIGS[args.model]
+    mcfg = dict(CONFIGS[args.model])
+    if args.layers:
+        mcfg["layers"] = args.layers
     cfg = ModelConfig(**mcfg, micro_batch=args.micro_batch, optimizer=True, timeline=True)
     T = cfg.tokens_per_microbatch
     m = args.microbatches
@@ -182,15 +187,18 @@ def project_via_chunks(args, mcfg, name, p, m, comm_ms):
 
     target = pb.assemble(pb.build_entry(name, p), m)
     S = target.topology.num_stages
-    if mcfg["layers"] % S:
-        raise SystemExit(f"{mcfg['layers']} layers do not split into {S} stages")
-    per_chunk = mcfg["layers"] // S
+    L = mcfg["layers"]
+    per_chunk = -(-L // S)                 # ceil: every stage but the LM-head one carries this many
+    last = L - per_chunk * (S - 1)         # the LM-head stage takes the remainder
+    if last < 1:
+        raise SystemExit(f"{L} layers do not split into {S} stages")
     v_shape = S == 2 * p
     probe_p = 2 if v_shape else 3
     probe_S = 2 * probe_p if v_shape else probe_p
     probe_m = min(m, 4 * probe_p)
-    cfg = ModelConfig(**dict(mcfg, layers=per_chunk * probe_S), micro_batch=args.micro_batch, optimizer=True,
-                      timeline=True)
+    cfg = ModelConfig(**dict(mcfg, layers=per_chunk * (probe_S - 1) + last), micro_batch=args.micro_batch,
+                      optimizer=True, timeline=True,
+                      stage_layers=tuple([per_chunk] * (probe_S - 1) + [last]) if last != per_chunk else None)
     probe = pb.assemble(pb.build_entry(name, probe_p), probe_m)
     tokens, labels = synthetic_batch(cfg, probe_m)
     tok, lab = torch.from_numpy(tokens).cuda(), torch.from_numpy(labels).cuda()
@@ -219,7 +227,8 @@ def project_via_chunks(args, mcfg, name, p, m, comm_ms):
         pool.append(int(pred[d - 1]) * (head_bytes if holds_last else mid_bytes))
     T = cfg.tokens_per_microbatch
     return {"schedule": name, "p": p, "probe": f"{name} p={probe_p} m={probe_m}, {cfg.layers} layers "
-                                                f"({per_chunk} per chunk)",
+                                                f"({per_chunk} per chunk, {last} on the LM-head chunk)",
+            "target_stage_layers": [per_chunk] * (S - 1) + [last],
             "projected_ms_per_step": rep.makespan, "projected_tokens_per_s": m * T / (rep.makespan / 1e3),
             "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
             "pipeline_roofline_frac": max(rep.busy) / rep.makespan, "ideal_ms": max(rep.busy),
