@@ -218,13 +218,15 @@ def project_via_chunks(args, mcfg, name, p, m, comm_ms):
     rep = pb.replay(target, durations, comm_ms)
     rep0 = pb.replay(target, durations, 0.0)
     pred = pb.exact_peak(target)
-    # a device's slot holds its largest stage (last-stage slots add logits); middle-class bytes otherwise
-    mid_bytes = min(slot_bytes.values())
-    head_bytes = max(slot_bytes.values())
+    # a device's activation slot is sized for its largest stage: take the slot bytes of the probe device
+    # that holds the same chunk classes (V: {first, last} / {middle}; straight: {first} / {middle} / {last})
+    def classes(topo, n_stages, d):
+        return frozenset(chunk_class(st, n_stages) for st in range(1, n_stages + 1) if topo.device_of(st) == d)
+
+    probe_bytes = {classes(probe.topology, probe_S, d): b for d, b in slot_bytes.items()}
     pool = []
     for d in range(1, p + 1):
-        holds_last = target.topology.device_of(S) == d
-        pool.append(int(pred[d - 1]) * (head_bytes if holds_last else mid_bytes))
+        pool.append(int(pred[d - 1]) * probe_bytes[classes(target.topology, S, d)])
     T = cfg.tokens_per_microbatch
     return {"schedule": name, "p": p, "probe": f"{name} p={probe_p} m={probe_m}, {cfg.layers} layers "
                                                 f"({per_chunk} per chunk, {last} on the LM-head chunk)",
