@@ -33,6 +33,9 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+#ifndef PB_GEMM_SMEM_KB
+#define PB_GEMM_SMEM_KB 200  // operand ring budget (KB): 6 stages of 32 KB for the CTA-pair 256-wide tiles
+#endif
 
 // BM2 = 2: each CTA holds TWO 128-row A sub-tiles (a CTA pair covers 512 x BN) sharing one B
 // stage, and the two accumulators fill all 512 TMEM columns (single-buffered): a quarter less
@@ -43,7 +46,7 @@ struct Cfg {
     static constexpr int kABytes = BM * BK * 2 * BM2;
     static constexpr int kBBytes = kBRows * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+    static constexpr int kStages = (PB_GEMM_SMEM_KB * 1024) / kStageBytes > 8 ? 8 : (PB_GEMM_SMEM_KB * 1024) / kStageBytes;
     static constexpr int kAccStride = BN <= 128 ? 128 : 256;  // accumulator buffer pitch (TMEM columns)
     static constexpr int kAccBufs = BM2 == 2 ? 1 : 2;          // double-buffered unless BM2 fills TMEM
     static constexpr int kTmemCols = 2 * kAccStride;           // (power of 2)
