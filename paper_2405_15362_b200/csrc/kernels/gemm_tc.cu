@@ -736,18 +736,20 @@ int gemm_f_bn(int M, int N) {
 }
 
 // 512 x 256 CTA-pair tiles (BM2 = 2) for full-tile launches (PB_GEMM_BM2=1 or the test hook);
-// a pair's epilogue is then not overlapped with its next tile's main loop.  Off by default:
+// a pair's epilogue is then not overlapped with its next tile's main loop.  Default: K >= 8192 only:
 // measured at T = 4096 it gains on long-K shapes (FC1 dX, K = 8192: 1399 -> 1454 TFLOP/s; FC2,
 // K = 8192: 1355 -> 1375) but loses more on K = 2048 (FC1 + GELU 1317 -> 1016), where the exposed
 // epilogue is a quarter of the tile; 82.5k vs 86.5k tokens/s in-step with it on everywhere.
 static int g_force_bm2 = -1;  // tests: -1 environment, 0 off, 1 on
 void gemm_force_bm2(int on) { g_force_bm2 = on; }
 static bool use_bm2(const GemmArgs& g) {
-    static const bool env = [] {
+    // PB_GEMM_BM2: 1 = every eligible launch, 0 = never, unset = long-K launches only (K >= 8192)
+    static const int env = [] {
         const char* e = std::getenv("PB_GEMM_BM2");
-        return e && e[0] == '1';
+        return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
     }();
-    const bool on = g_force_bm2 < 0 ? env : g_force_bm2 == 1;
+    const int mode = g_force_bm2 >= 0 ? g_force_bm2 : env;
+    const bool on = mode == 1 || (mode < 0 && g.K >= 8192);
     return on && g.M % 512 == 0 && g.N % 256 == 0 && sk_enabled() == 0;
 }
 
