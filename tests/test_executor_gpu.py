@@ -177,10 +177,12 @@ def test_unfolded_gamma_path_matches_oracle(monkeypatch):
     test_step_matches_oracle("v-half", 2)
 
 
-def test_vocab_half_tile_matches_oracle():
-    """vocab = 128 (mod 256): the LM-head GEMMs run on CTA pairs with a half-empty last tile."""
+@pytest.mark.parametrize("vocab", [1152, 8448])
+def test_vocab_half_tile_matches_oracle(vocab):
+    """vocab = 128 (mod 256): the LM-head GEMMs run on CTA pairs with a half-empty last tile; at
+    vocab >= 8192 the LM-head dX GEMM (K = vocab) takes the 512-row pair tile."""
     import dataclasses
-    cfg = dataclasses.replace(CFG, vocab=1152)
+    cfg = dataclasses.replace(CFG, vocab=vocab)
     sched = pb.assemble(pb.build_entry("v-half", 2), M)
     ex = PipelineExecutor(cfg, sched)
     tokens, labels = synthetic_batch(cfg, M)
