@@ -213,12 +213,15 @@ typedef struct pb_model_cfg {
 
 typedef struct pb_exec_stats {
     double loss;            /* mean CE over all tokens of the step (last-stage device; NaN elsewhere) */
-    double step_ms;         /* this device: first pass start .. last pass end (CUDA events) */
+    double step_ms;         /* this device: CUDA events from the start of the step's enqueue (before the
+                               token / label copies) to its end (after the gamma fold, AdamW and the loss
+                               D2H), i.e. the whole step on this device's compute stream */
     double busy_ms;         /* this device: sum of pass durations */
     int64_t pool_slots;     /* activation slots allocated = predicted exact_peak on this device */
     int64_t pool_peak;      /* slots live at once, counted while running */
     int64_t slot_bytes;     /* bytes per activation slot */
-    int64_t pool_bytes;     /* slot_bytes * pool_slots */
+    int64_t pool_bytes;     /* slot_bytes * pool_slots + the LM-head pool (head slot bytes * head slots,
+                               last-stage device only: final-norm output and logits) */
     int64_t peer_bytes;     /* bytes pulled from peers during the step */
     int64_t kernel_launches;/* kernels this device launched during the step */
     double gemm_ms;         /* PB_FLAG_GEMM_TIMING: summed GEMM launch durations (CUDA events, compute stream) */
@@ -246,6 +249,11 @@ int pb_exec_connect_ipc(pb_exec* e, const void* const* blobs, const size_t* lens
  * microbatch-major; host pointers when inputs_on_host != 0 (copied in on the
  * compute stream inside the step), else device pointers.  Only stage-1's
  * device reads tokens and only the last stage's device reads labels.
+ * Ids must lie in [0, vocab).  Host inputs are checked before anything is
+ * enqueued by every device that is given the arrays (pass the same arrays to
+ * every device of a group so they fail together): PB_EINVAL.  Device inputs
+ * are checked by the kernels that index with them (the row is skipped, never
+ * read or written out of bounds) and the step's sync returns PB_EINVAL.
  * timeline: NULL or an array of this device's pass count (canonical order). */
 int pb_exec_step(pb_exec* e, const int32_t* tokens, const int32_t* labels, int32_t inputs_on_host,
                  pb_timed_pass* timeline, size_t timeline_n, pb_exec_stats* stats);

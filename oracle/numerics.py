@@ -41,7 +41,7 @@ def attention(qkv, mbs, seq, heads):
     q, k, v = qkv.view(mbs, seq, 3, heads, 128).unbind(2)
     q, k, v = (t.transpose(1, 2) for t in (q, k, v))
     s = q @ k.transpose(-1, -2) / math.sqrt(128)
-    mask = torch.triu(torch.ones(seq, seq, dtype=torch.bool), 1)
+    mask = torch.triu(torch.ones(seq, seq, dtype=torch.bool, device=qkv.device), 1)
     p = torch.softmax(s.masked_fill(mask, float("-inf")), -1)
     return (p @ v).transpose(1, 2).reshape(T, heads * 128)
 
@@ -122,19 +122,30 @@ def rename_for(params: Dict[str, torch.Tensor], cfg, S_from: int, S_to: int, cfg
     return out
 
 
-def reference_step(params: Dict[str, torch.Tensor], tokens, labels, cfg, S: int):
-    """Non-pipelined fp32 loss and gradients.  params named for an S-stage split."""
-    p = {n: t.detach().float().clone().requires_grad_(True) for n, t in params.items()}
-    m, T = tokens.shape
-    scale = 1.0 / (m * T)
-    total = 0.0
-    for mb in range(m):
-        x = None
-        for s in range(1, S + 1):
-            x = stage_forward(s, S, x, p, cfg, torch.as_tensor(tokens[mb]).long(), torch.as_tensor(labels[mb]), scale)
-        x.backward()
-        total += x.item()
-    return total, {n: t.grad.detach().clone() for n, t in p.items()}
+def reference_step(params: Dict[str, torch.Tensor], tokens, labels, cfg, S: int, device: str = "cpu"):
+    """Non-pipelined fp32 loss and gradients.  params named for an S-stage split.
+
+    device="cuda" runs the same fp32 restatement on the GPU (full-fp32 matmuls, TF32 off) for the
+    real-shape parity cases (h up to 6144, s up to 6144) that would take minutes on host cores;
+    gradients are returned on the host either way."""
+    prec = torch.get_float32_matmul_precision()
+    torch.set_float32_matmul_precision("highest")
+    try:
+        p = {n: t.detach().to(device).float().clone().requires_grad_(True) for n, t in params.items()}
+        m, T = tokens.shape
+        scale = 1.0 / (m * T)
+        total = 0.0
+        for mb in range(m):
+            x = None
+            tok = torch.as_tensor(tokens[mb]).long().to(device)
+            lab = torch.as_tensor(labels[mb]).to(device)
+            for s in range(1, S + 1):
+                x = stage_forward(s, S, x, p, cfg, tok, lab, scale)
+            x.backward()
+            total += x.item()
+        return total, {n: t.grad.detach().cpu().clone() for n, t in p.items()}
+    finally:
+        torch.set_float32_matmul_precision(prec)
 
 
 def schedule_step(params: Dict[str, torch.Tensor], tokens, labels, cfg, passes: Iterable, S: int):

@@ -1,6 +1,9 @@
 // Kernel-level test entry points (include/pipeblock_b200_kernels.h).
 #include "../../include/pipeblock_b200_kernels.h"
 
+#include <climits>
+#include <cstdint>
+
 #include "capi_common.hpp"
 #include "kernels/gemm.hpp"
 #include "kernels/ops.hpp"
@@ -69,20 +72,20 @@ extern "C" int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, con
 }
 extern "C" int pbt_embed_fwd(const int32_t* tok, const void* emb, void* x, int32_t T, int32_t h, void* stream) {
     return pbx::guard([&] {
-        pbk::embed_fwd(tok, BF(emb), BFM(x), T, h, ST(stream));
+        pbk::embed_fwd(tok, BF(emb), BFM(x), T, h, INT32_MAX, nullptr, ST(stream));
         cuda_check("pbt_embed_fwd");
     });
 }
 extern "C" int pbt_embed_bwd(const int32_t* tok, const void* dx, float* demb, int32_t T, int32_t h, void* stream) {
     return pbx::guard([&] {
-        pbk::embed_bwd(tok, BF(dx), demb, T, h, ST(stream));
+        pbk::embed_bwd(tok, BF(dx), demb, T, h, INT32_MAX, nullptr, ST(stream));
         cuda_check("pbt_embed_bwd");
     });
 }
 extern "C" int pbt_cross_entropy(void* logits, const int32_t* labels, float* loss, int32_t T, int32_t V, float scale,
                                  void* stream) {
     return pbx::guard([&] {
-        pbk::cross_entropy(BFM(logits), labels, loss, T, V, scale, ST(stream));
+        pbk::cross_entropy(BFM(logits), labels, loss, T, V, scale, nullptr, ST(stream));
         cuda_check("pbt_cross_entropy");
     });
 }

@@ -478,7 +478,7 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
     const StageParams& P = sparams.at(s);
     __nv_bfloat16* x0 = bf(slot, L.x[0]);
     if (s == 1) {
-        timed("embed_fwd", [&] { pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, cs); });
+        timed("embed_fwd", [&] { pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, V, id_err(), cs); });
         ++launches;
     }
     for (int l = 0; l < Lc; ++l) {
@@ -500,7 +500,7 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), HB(mb, L.hf), HF(mb, L.rstdf), T, h, cs); });
         gemm(T, V, h, HB(mb, L.hf), false, W(P.head), false, HB(mb, L.logits), pbk::EPI_STORE);
         timed("cross_entropy", [&] { pbk::cross_entropy(HB(mb, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
-                           cs); });
+                           id_err(), cs); });
         launches += 2;
     }
 }
@@ -557,7 +557,7 @@ void Exec::pass_weight(int s, int mb, int slot) {
     if (s == S)
         gemm(V, h, T, HB(mb, L.logits), true, HB(mb, L.hf), true, GW(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
     if (s == 1) {
-        timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, cs); });
+        timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, V, id_err(), cs); });
         ++launches;
     }
 }
@@ -596,6 +596,19 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     ck(cudaEventRecord(ev_step0, cs), "event");
     const bool has_first = std::find(stages.begin(), stages.end(), 1) != stages.end();
     const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
+    if (on_host) {  // ids index the embedding / logits: reject out-of-range ids before anything is enqueued
+        auto check = [&](const int32_t* ids, const char* what) {
+            for (size_t i = 0; i < size_t(m) * T; ++i)
+                if (ids[i] < 0 || ids[i] >= V)
+                    throw std::invalid_argument(std::string(what) + " id " + std::to_string(ids[i]) + " at index " +
+                                                std::to_string(i) + " outside [0, " + std::to_string(V) + ")");
+        };
+        // every device given the arrays checks them (not only the stage-1 / stage-S holders), so all
+        // devices of a group that share the same host inputs fail together instead of waiting on a peer
+        if (tok) check(tok, "token");
+        if (lab) check(lab, "label");
+    }
+    ck(cudaMemsetAsync(loss_dev, 0, 8, cs), "loss");  // [0] loss, [1] out-of-range id flag (device inputs)
     if (has_first) {
         if (!tok) throw std::invalid_argument("tokens required on the device holding stage 1");
         ck(cudaMemcpyAsync(tokens, tok, nin, kind, cs), "tokens");
@@ -603,7 +616,6 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     if (has_last) {
         if (!lab) throw std::invalid_argument("labels required on the device holding the last stage");
         ck(cudaMemcpyAsync(labels, lab, nin, kind, cs), "labels");
-        ck(cudaMemsetAsync(loss_dev, 0, 4, cs), "loss");
     }
     const auto& ops = plan.dev_ops[dev];
     int live = 0;
@@ -725,7 +737,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
         ++launches;
         if (fold) timed("fold_weight", [&] { refold(); });
     }
-    if (has_last) ck(cudaMemcpyAsync(loss_host, loss_dev, 4, cudaMemcpyDeviceToHost, cs), "loss");
+    ck(cudaMemcpyAsync(loss_host, loss_dev, 8, cudaMemcpyDeviceToHost, cs), "loss");
     ck(cudaEventRecord(ev_step1, cs), "event");
     ck(cudaGetLastError(), "launch");
     ++steps_done;
@@ -738,6 +750,8 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
     ck(cudaStreamSynchronize(cs), "step");
     ck(cudaStreamSynchronize(xs), "step");
     pending = false;
+    if (reinterpret_cast<const int32_t*>(loss_host)[1])
+        throw std::invalid_argument("token or label id outside [0, " + std::to_string(V) + ") in the step's device inputs");
     const auto& ops = plan.dev_ops[dev];
     const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
     double busy = 0;

@@ -150,6 +150,7 @@ class Exec {
     uint32_t* flags = nullptr;
     __nv_bfloat16* scratch = nullptr;
     float *dsum = nullptr, *dq_acc = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
+    int* id_err() { return reinterpret_cast<int*>(loss_dev + 1); }  // out-of-range token/label flag
     int32_t *tokens = nullptr, *labels = nullptr;
     std::vector<void*> allocations;
     std::vector<cudaEvent_t> ev_start, ev_end, ev_pull, ev_free, ev_copy0, ev_copy1;

@@ -246,22 +246,38 @@ __global__ void rmsnorm_dgamma_sum_kernel(const float* __restrict__ partial, flo
     }
 }
 
+// Token / label ids come through the public C-ABI: an id outside [0, V) never indexes memory.
+// The row is zeroed (embed_fwd) or skipped (embed_bwd, CE) and *err is set; the executor turns
+// the flag into PB_EINVAL when the step is synchronised.
+__device__ __forceinline__ bool id_ok(int32_t id, int V, int* err) {
+    if (id >= 0 && id < V) return true;
+    if (err) atomicOr(err, 1);
+    return false;
+}
+
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ emb,
-                                 __nv_bfloat16* __restrict__ x, int T, int h) {
+                                 __nv_bfloat16* __restrict__ x, int T, int h, int V, int* err) {
     pdl_wait();
     pdl_launch();
     const int row = blockIdx.x;
-    const uint4* src = reinterpret_cast<const uint4*>(emb + size_t(tok[row]) * h);
+    const int32_t id = tok[row];
     uint4* dst = reinterpret_cast<uint4*>(x + size_t(row) * h);
+    if (!id_ok(id, V, threadIdx.x == 0 ? err : nullptr)) {
+        for (int c = threadIdx.x; c < (h >> 3); c += blockDim.x) dst[c] = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(emb + size_t(id) * h);
     for (int c = threadIdx.x; c < (h >> 3); c += blockDim.x) dst[c] = src[c];
 }
 
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
-                                 float* __restrict__ demb, int T, int h) {
+                                 float* __restrict__ demb, int T, int h, int V, int* err) {
     pdl_wait();
     pdl_launch();
     const int row = blockIdx.x;
-    float* dst = demb + size_t(tok[row]) * h;
+    const int32_t id = tok[row];
+    if (!id_ok(id, V, threadIdx.x == 0 ? err : nullptr)) return;
+    float* dst = demb + size_t(id) * h;
     const uint4* src = reinterpret_cast<const uint4*>(dx + size_t(row) * h);
     for (int c = threadIdx.x; c < (h >> 3); c += blockDim.x) {
         float f[8];
@@ -273,7 +289,7 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 
 // one block per row: loss += (lse - z[label]) * scale ; z <- (softmax(z) - onehot) * scale  (bf16, in place)
 __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ logits, const int32_t* __restrict__ labels,
-                                                 float* __restrict__ loss, int V, float scale) {
+                                                 float* __restrict__ loss, int V, float scale, int* err) {
     pdl_wait();
     pdl_launch();
     __shared__ float red[32];
@@ -318,7 +334,8 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
     __syncthreads();
     s = red[0];
     const int lab = labels[row];
-    const float zl = __bfloat162float(z[lab]);
+    const bool lab_ok = id_ok(lab, V, threadIdx.x == 0 ? err : nullptr);  // bad label: no loss, no one-hot
+    const float zl = lab_ok ? __bfloat162float(z[lab]) : 0.f;
     __syncthreads();
     const float inv = 1.f / s;
     for (int c = threadIdx.x; c < nch; c += blockDim.x) {
@@ -332,7 +349,7 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
         }
         z4[c] = pack8(f);
     }
-    if (threadIdx.x == 0) atomicAdd(loss, (m + __logf(s) - zl) * scale);
+    if (threadIdx.x == 0 && lab_ok) atomicAdd(loss, (m + __logf(s) - zl) * scale);
 }
 
 // AdamW on fp32 masters; refreshes the bf16 copy and zeroes the gradient.
@@ -493,16 +510,18 @@ void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float
              dgamma, nb, h);
 }
 
-void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s) {
-    launch_k(embed_fwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, emb, x, T, h);
+void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, int V, int* err,
+               cudaStream_t s) {
+    launch_k(embed_fwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, emb, x, T, h, V, err);
 }
-void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, cudaStream_t s) {
-    launch_k(embed_bwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, dx, demb, T, h);
+void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, int V, int* err,
+               cudaStream_t s) {
+    launch_k(embed_bwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, dx, demb, T, h, V, err);
 }
-void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale,
+void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale, int* err,
                    cudaStream_t s) {
     if (V % 8) throw std::invalid_argument("cross_entropy: V % 8");
-    launch_k(ce_kernel, dim3(T), dim3(512), 0, s, 1, logits, labels, loss, V, scale);
+    launch_k(ce_kernel, dim3(T), dim3(512), 0, s, 1, logits, labels, loss, V, scale, err);
 }
 void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
            float eps, float wd, int step, cudaStream_t s) {

@@ -34,10 +34,14 @@ void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfl
 // dgamma (fp32) += sum_t dy * x * rstd ; deterministic; scratch >= ceil(T/16) * h floats
 void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, float* scratch,
                     int T, int h, cudaStream_t s);
-void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, cudaStream_t s);
-void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, cudaStream_t s);
+// ids outside [0, V) are never dereferenced: the row is zeroed / skipped and *err (may be null) |= 1
+void embed_fwd(const int32_t* tok, const __nv_bfloat16* emb, __nv_bfloat16* x, int T, int h, int V, int* err,
+               cudaStream_t s);
+void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, int h, int V, int* err,
+               cudaStream_t s);
 // loss (fp32 scalar) += scale * sum_rows CE ; logits <- scale * (softmax - onehot), in place
-void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale,
+// (a label outside [0, V) adds no loss and no one-hot, and sets *err)
+void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale, int* err,
                    cudaStream_t s);
 void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
            float eps, float wd, int step, cudaStream_t s);

@@ -222,3 +222,29 @@ def test_more_schedules_match_oracle(entry, p, m, cfg):
     peaks = pb.exact_peak(sched)
     for d, st in res.per_device.items():
         assert st.pool_slots == int(peaks[d - 1]) and st.pool_peak == int(peaks[d - 1])
+
+
+@pytest.mark.parametrize("on_host", [True, False])
+@pytest.mark.parametrize("what,bad", [("tokens", 1024), ("labels", -1), ("tokens", 1 << 30)])
+def test_out_of_range_ids_rejected(on_host, what, bad):
+    """Ids index the embedding rows and the logits: an id outside [0, vocab) is PB_EINVAL, never an
+    out-of-bounds read or scatter-add (host inputs: rejected before enqueue; device inputs: the
+    kernels skip the row, flag it, and the step's sync raises). A following valid step is unaffected."""
+    from paper_2405_15362_b200._lib import PipeblockError
+    sched = pb.assemble(pb.build_entry("v-half", 2), M)
+    tokens, labels = synthetic_batch(CFG, M)
+    ex = PipelineExecutor(CFG, sched)
+    ref = ex.step(tokens, labels).loss
+    for d in ex.devices:
+        d.zero_grads()
+    bt, bl = tokens.copy(), labels.copy()
+    (bt if what == "tokens" else bl)[3, 17] = bad
+    if not on_host:
+        bt, bl = torch.from_numpy(bt).cuda(), torch.from_numpy(bl).cuda()
+        torch.cuda.synchronize()
+    with pytest.raises(PipeblockError, match="outside \\[0, 1024\\)"):
+        ex.step(bt, bl, on_host=on_host)
+    for d in ex.devices:
+        d.zero_grads()
+    again = ex.step(tokens, labels).loss
+    assert abs(again - ref) < 1e-6 * abs(ref)

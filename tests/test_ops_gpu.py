@@ -38,8 +38,9 @@ def test_attention_forward(batch, seq, heads):
 
 
 # (2, 2048, 16) and (1, 4096, 8) are >= 3 CTAs per SM: the default path is the two-CTA-per-SM kernel (v3)
+# (1, 4096, 32) / (1, 6144, 48): the 6B / 14B model shapes (seq x heads of one micro-batch)
 @pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16),
-                                             (2, 2048, 16), (1, 4096, 8)])
+                                             (2, 2048, 16), (1, 4096, 8), (1, 4096, 32), (1, 6144, 48)])
 def test_attention_forward_tcgen05(batch, seq, heads):
     g = torch.Generator(device="cuda").manual_seed(seq * 3 + heads)
     qkv = (2 * torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g)).bfloat16()
@@ -67,7 +68,8 @@ def test_attention_backward(batch, seq, heads):
         assert rel(dqkv[:, sl], gx[:, sl]) < 2e-2, name
 
 
-@pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16)])
+@pytest.mark.parametrize("batch,seq,heads", [(1, 128, 1), (2, 256, 2), (1, 1024, 4), (2, 2048, 2), (1, 2048, 16),
+                                             (2, 2048, 16), (1, 4096, 32), (1, 6144, 48)])
 def test_attention_backward_tcgen05(batch, seq, heads):
     g = torch.Generator(device="cuda").manual_seed(5 + seq + heads)
     qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g).bfloat16()
