@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--micro-batch", type=int, default=2)
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="target seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--compare", nargs="+", default=None,
+                    help="schedules run after the headline one in the same process group (default at N>1: 1f1b, "
+                         "v-zb, v-half, + v-min for --model 14b; 'none' to skip)")
     ap.add_argument("--even-split", action="store_true",
                     help="layers / num_stages per stage (default: balance the LM-head stage, N > 1)")
     return ap.parse_args()
@@ -121,42 +124,116 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_layer_sample(mcfg, target_s: float):
-    """Bounded CPU sample: one microbatch through one layer, F + B + W (fp32, torch CPU,
-    all host threads), via the oracle's F/B/W split; extrapolated to the whole model."""
+def _median_time(fn, budget_s, max_n=20):
+    fn()  # warm-up (thread pool, allocator)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= max_n:
+            return statistics.median(times), len(times)
+
+
+def cpu_baseline(mcfg, args, target_s=None, tiny_e2e=True):
+    """Bounded CPU sample of the same workload on all host threads (torch CPU fp32, the oracle port):
+    per sequence, one transformer layer F + B + W and the final norm + LM head + cross-entropy F + B + W;
+    AdamW over one layer's parameters.  The step is extrapolated as
+        (m * mbs) * (L * t_layer + t_head) + n_params * t_adamw_per_param
+    and, separately, config 1 (L=8, h=512, 4 heads, s=256, V=1024, mbs=2, V-Half p=4, m=8) runs END TO END
+    through oracle.numerics.schedule_step (the GridSchedule executed pass by pass) + AdamW."""
     import torch
     from types import SimpleNamespace
 
     from oracle import numerics as N
 
+    target_s = args.cpu_sample_s if target_s is None else target_s
     torch.set_num_threads(os.cpu_count() or 1)
     cfg = SimpleNamespace(layers=1, hidden=mcfg["hidden"], heads=mcfg["heads"], seq=mcfg["seq"],
                           vocab=mcfg["vocab"], micro_batch=1)
-    h = cfg.hidden
+    h, V, T, L = cfg.hidden, cfg.vocab, cfg.seq, mcfg["layers"]
     g = torch.Generator().manual_seed(0)
-    p = {f"s1.l0.{n}": (0.02 * torch.randn(shp, generator=g)).requires_grad_(True)
-         for n, shp in {"wqkv": (3 * h, h), "wo": (h, h), "w1": (4 * h, h), "w2": (h, 4 * h)}.items()}
+    shp = {"wqkv": (3 * h, h), "wo": (h, h), "w1": (4 * h, h), "w2": (h, 4 * h)}
+    p = {f"s1.l0.{n}": (0.02 * torch.randn(s, generator=g)).requires_grad_(True) for n, s in shp.items()}
     p["s1.l0.norm1"] = torch.ones(h, requires_grad=True)
     p["s1.l0.norm2"] = torch.ones(h, requires_grad=True)
-    T = cfg.seq
-    times = []
-    t_end = time.perf_counter() + target_s
-    while True:
-        x = torch.randn(T, h, requires_grad=True)
-        t0 = time.perf_counter()
-        y = N.layer_forward(x, p, "s1.l0.", cfg)                               # F
+    head = {"norm": torch.ones(h, requires_grad=True), "head": (0.02 * torch.randn(V, h, generator=g)).requires_grad_(True)}
+    x = torch.randn(T, h, requires_grad=True)
+    lab = torch.randint(0, V, (T,), generator=g)
+
+    def layer():
+        y = N.layer_forward(x, p, "s1.l0.", cfg)                           # F
         gy = torch.randn_like(y)
-        (gx,) = torch.autograd.grad(y, x, gy, retain_graph=True)              # B
-        gw = torch.autograd.grad(y, list(p.values()), gy)                     # W
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end or len(times) >= 20:
-            break
-    per_layer = statistics.median(times)
-    tokens_per_s = T / (per_layer * mcfg["layers"])
-    return {"value": tokens_per_s, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"1 sequence ({T} tokens) through 1 of {mcfg['layers']} layers, F+B+W in fp32 "
-                      f"(oracle/numerics.py, torch CPU), median of {len(times)} runs, x{mcfg['layers']} layers; "
-                      f"LM head and optimizer excluded"}
+        torch.autograd.grad(y, x, gy, retain_graph=True)                   # B
+        torch.autograd.grad(y, list(p.values()), gy)                       # W
+
+    def lm_head():
+        z = N.rmsnorm(x, head["norm"]) @ head["head"].t()
+        loss = torch.nn.functional.cross_entropy(z, lab, reduction="sum")
+        torch.autograd.grad(loss, [x], retain_graph=True)
+        torch.autograd.grad(loss, list(head.values()))
+
+    flat = [t.detach() for t in p.values()]
+    st = [(torch.zeros_like(t), torch.zeros_like(t), torch.randn_like(t)) for t in flat]
+
+    def adamw():
+        for w, (m1, m2, gr) in zip(flat, st):
+            m1.mul_(0.9).add_(gr, alpha=0.1)
+            m2.mul_(0.95).addcmul_(gr, gr, value=0.05)
+            w.addcdiv_(m1, m2.sqrt().add_(1e-8), value=-1e-4)
+
+    t_layer, n1 = _median_time(layer, 0.5 * target_s)
+    t_head, n2 = _median_time(lm_head, 0.3 * target_s)
+    t_adam, n3 = _median_time(adamw, 0.1 * target_s)
+    n_layer_params = sum(t.numel() for t in flat)
+    n_params = L * (12 * h * h + 2 * h) + 2 * V * h + h
+    seqs = args.microbatches * args.micro_batch
+    t_step = seqs * (L * t_layer + t_head) + n_params * t_adam / n_layer_params
+    out = {"value": seqs * T / t_step, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+           "sample": f"per sequence ({T} tokens): 1 of {L} layers F+B+W (median of {n1}), final norm + LM head + CE "
+                     f"F+B+W (median of {n2}), AdamW on one layer's {n_layer_params} parameters (median of {n3}); "
+                     f"step extrapolated to {seqs} sequences x {L} layers + head and AdamW over {n_params} parameters "
+                     f"(fp32, oracle/numerics.py on torch CPU)",
+           "ms_per_step_extrapolated": t_step * 1e3,
+           "parts_ms": {"layer_fbw_per_seq": t_layer * 1e3, "head_fbw_per_seq": t_head * 1e3,
+                        "adamw_per_layer_params": t_adam * 1e3}}
+    if tiny_e2e:
+        out["tiny_e2e"] = cpu_tiny_e2e()
+    return out
+
+
+def cpu_tiny_e2e():
+    """BASELINE configs[0] / SURVEY §8d config 1 end to end on host cores: V-Half p=4 m=8, L=8, h=512,
+    4 heads, s=256, V=1024, mbs=2; the whole GridSchedule pass by pass (oracle.numerics.schedule_step)
+    plus AdamW over every parameter."""
+    import torch
+    from types import SimpleNamespace
+
+    from oracle import numerics as N
+    from paper_2405_15362_b200 import pipeblock as pb
+
+    cfg = SimpleNamespace(layers=8, hidden=512, heads=4, seq=256, vocab=1024, micro_batch=2, stage_layers=None)
+    sched = pb.assemble(pb.build_entry("v-half", 4), 8)
+    S = sched.topology.num_stages
+    g = torch.Generator().manual_seed(0)
+    w = {n: (0.02 * torch.randn(s, generator=g)) for n, s in N.shapes(cfg, S).items()}
+    tok = torch.randint(0, cfg.vocab, (8, cfg.seq * cfg.micro_batch), generator=g)
+    lab = torch.randint(0, cfg.vocab, (8, cfg.seq * cfg.micro_batch), generator=g)
+    state = {n: (torch.zeros_like(t), torch.zeros_like(t)) for n, t in w.items()}
+
+    def step():
+        _, grads = N.schedule_step(w, tok.numpy(), lab.numpy(), cfg, sched.passes, S)
+        for n, gr in grads.items():
+            m1, m2 = state[n]
+            m1.mul_(0.9).add_(gr, alpha=0.1)
+            m2.mul_(0.95).addcmul_(gr, gr, value=0.05)
+            w[n].addcdiv_(m1, m2.sqrt().add_(1e-8), value=-1e-4)
+
+    t, n = _median_time(step, 3.0, max_n=5)
+    return {"value": 8 * cfg.seq * cfg.micro_batch / t, "unit": "tokens/s", "ms_per_step": t * 1e3,
+            "cores": torch.get_num_threads(), "runs": n,
+            "workload": "config 1: gpt L=8 h=512 4 heads s=256 V=1024, v-half p=4 m=8 mbs=2, whole step + AdamW"}
 
 
 def reference_schedule_time(entry, p, m):
@@ -183,15 +260,17 @@ def run_reference(args, rank, world):
     sched_info = reference_schedule_time(sched, args.gpus, args.microbatches) if refpy.available() else None
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_layer_sample(mcfg, target_s=max(2.0, args.cpu_sample_s / max(1, args.steps + args.warmup)))
+        r = cpu_baseline(mcfg, args, target_s=max(2.0, args.cpu_sample_s / max(1, args.steps + args.warmup)),
+                         tiny_e2e=False)
         if i >= args.warmup:
             vals.append(r["value"])
     v = statistics.median(vals)
+    tiny = cpu_tiny_e2e()
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f32",
             "data": "synthetic", "config": {"workload": workload_name(args, sched), "model": f"gpt-{args.model}"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "port",
-                             "sample": r["sample"]},
+                             "sample": r["sample"], "tiny_e2e": tiny},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_schedule": sched_info,
             "note": "the reference has no F/B/W execution; its schedule code (oracle/_ref) + the CPU oracle port"}
@@ -219,36 +298,23 @@ def transfer_summary(gathered):
             "peak_gbps_per_direction": 900.0}
 
 
-def main():
-    args = parse()
-    rank, world, local = dist_env()
-    if args.gpus != world and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
+def run_schedule(args, ctx, sched_name, headline):
+    """One schedule on this rank's pipeline device: build, warm up, time K steps (device-resident inputs,
+    CUDA events, max over ranks), then (headline only) the e2e host-input steps and the GEMM-timed step,
+    and always one timeline step.  Returns the rank-0 summary (None on other ranks).  The executor is
+    destroyed before returning, so the next schedule gets the whole HBM."""
+    import gc
 
-    import numpy as np
     import torch
 
     from paper_2405_15362_b200 import pipeblock as pb
-    from paper_2405_15362_b200.executor import DeviceExecutor, ModelConfig, synthetic_batch
+    from paper_2405_15362_b200.executor import DeviceExecutor, ModelConfig, balanced_stage_layers
 
-    if os.environ.get("PB_BENCH_SHARE_GPU"):  # test mode: every rank on cuda:0 (one-GPU box)
-        local = 0
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        if os.environ.get("PB_BENCH_SHARE_GPU"):
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    mcfg = CONFIGS[args.model]
-    p = args.gpus
-    sched_name = args.schedule or ("zb-h1" if p == 1 else "v-half")
-    schedule = pb.assemble(pb.build_entry(sched_name, p), args.microbatches)
-    cfg = ModelConfig(**mcfg, micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    rank, world, local, p, dist = ctx["rank"], ctx["world"], ctx["local"], args.gpus, ctx["dist"]
+    m = args.microbatches
+    schedule = pb.assemble(pb.build_entry(sched_name, p), m)
+    cfg = ModelConfig(**CONFIGS[args.model], micro_batch=args.micro_batch, optimizer=True, timeline=True)
     if p > 1 and not args.even_split:
-        from paper_2405_15362_b200.executor import balanced_stage_layers
         cfg = dataclasses.replace(cfg, stage_layers=balanced_stage_layers(cfg, schedule.topology))
     device = rank + 1
     ex = DeviceExecutor(cfg, schedule, device, local)
@@ -257,43 +323,15 @@ def main():
         dist.all_gather_object(blobs, ex.export_blob())
         ex.connect_ipc(blobs)
         dist.barrier()
-
     T = cfg.tokens_per_microbatch
-    m = args.microbatches
-    tokens_np, labels_np = synthetic_batch(cfg, m)
-    tok_host = torch.from_numpy(tokens_np).pin_memory()
-    lab_host = torch.from_numpy(labels_np).pin_memory()
-    tok_dev, lab_dev = tok_host.cuda(), lab_host.cuda()
-    torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    coll_dev = "cpu" if os.environ.get("PB_BENCH_SHARE_GPU") else "cuda"
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
+    tok_dev, lab_dev, tok_host, lab_host = ctx["inputs"]
+    barrier, max_over_ranks, sum_over_ranks = ctx["barrier"], ctx["max"], ctx["sum"]
     stream = torch.cuda.ExternalStream(ex.stream)
-    # warm-up (device-resident inputs)
     for _ in range(args.warmup):
         ex.step(tok_dev, lab_dev, on_host=False)
     barrier()
 
     # ---- device-timed region: K steps, inputs resident in HBM (weights+activations >> 126 MB L2)
-    launches = 0
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
@@ -305,68 +343,163 @@ def main():
         torch.cuda.synchronize()
         _, st = ex.sync()
         barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    ms = max_over_ranks(ms)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     launches = sum_over_ranks(st.kernel_launches * args.steps)
     tokens_per_step = m * T
-    value = tokens_per_step / (ms / 1e3)
+    out = {"schedule": sched_name, "ms_per_step": ms, "tokens_per_s": tokens_per_step / (ms / 1e3),
+           "launches": launches, "clocks": clk.summary(), "cfg": cfg, "sched": schedule}
 
-    # ---- e2e: the public step call with pinned HOST inputs, H2D + loss D2H inside, wall clock
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        _, est = ex.step(tok_host, lab_host, on_host=True)
-    barrier()
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
-    holds_first = schedule.topology.device_of(1) == device
-    holds_last = schedule.topology.device_of(schedule.topology.num_stages) == device
-    h2d = sum_over_ranks((m * T * 4 if holds_first else 0) + (m * T * 4 if holds_last else 0))
-    d2h = sum_over_ranks(4 if holds_last else 0)
+    if headline:
+        # ---- e2e: the public step call with pinned HOST inputs, H2D + loss D2H inside, wall clock
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ex.step(tok_host, lab_host, on_host=True)
+        barrier()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        holds_first = schedule.topology.device_of(1) == device
+        holds_last = schedule.topology.device_of(schedule.topology.num_stages) == device
+        out["e2e"] = {"value": tokens_per_step / e2e_s, "unit": "tokens/s",
+                      "h2d_bytes_per_step": int(sum_over_ranks((m * T * 4 if holds_first else 0)
+                                                               + (m * T * 4 if holds_last else 0))),
+                      "d2h_bytes_per_step": int(sum_over_ranks(8)),
+                      "def": "pb_exec_step with pinned host tokens/labels (H2D inside), loss + id-check flag D2H, "
+                             "wall clock, max over ranks"}
 
     # ---- timeline step (bubble, per-device busy) after a barrier, same inputs
     barrier()
     torch.cuda.synchronize()
     tl, tst = ex.step(tok_dev, lab_dev, on_host=False)
-    loss = tst.loss
+    mem = ex.memory()
+    uuid = str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)
+    mine = ([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss, tst.peer_bytes, tst.copy_ms, uuid, mem)
+    gathered = [mine]
     if world > 1:
         gathered = [None] * world
-        dist.all_gather_object(gathered, ([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss,
-                                          tst.peer_bytes, tst.copy_ms, str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)))
-    else:
-        gathered = [([tuple(q) for q in tl], tst.pool_bytes, tst.pool_slots, tst.loss, tst.peer_bytes, tst.copy_ms,
-                     None)]
+        dist.all_gather_object(gathered, mine)
 
-    # ---- GEMM roofline: one more step with CUDA events around every GEMM launch (compute stream)
-    barrier()
-    ex.set_flags(timeline=False, gemm_timing=True)
-    _, gst = ex.step(tok_dev, lab_dev, on_host=False)
-    ex.set_flags(timeline=True, gemm_timing=False)
-    gsum = [gst.gemm_ms, gst.gemm_flops, gst.gemm_launches, gst.step_ms]
-    if world > 1:
-        gall = [None] * world
-        dist.all_gather_object(gall, gsum)
-    else:
+    gall = None
+    if headline:
+        # ---- GEMM roofline: one more step with CUDA events around every GEMM launch (compute stream)
+        barrier()
+        ex.set_flags(timeline=False, gemm_timing=True)
+        _, gst = ex.step(tok_dev, lab_dev, on_host=False)
+        ex.set_flags(timeline=True, gemm_timing=False)
+        gsum = [gst.gemm_ms, gst.gemm_flops, gst.gemm_launches, gst.step_ms]
         gall = [gsum]
+        if world > 1:
+            gall = [None] * world
+            dist.all_gather_object(gall, gsum)
+    del ex, stream
+    gc.collect()
+    torch.cuda.synchronize()
+    barrier()
+    if rank != 0:
+        return None
 
+    from paper_2405_15362_b200.pipeblock import TimedPass, account
+    passes = [TimedPass(*q) for g in gathered for q in g[0]]
+    sim = account(schedule.topology, passes) if passes else None
+    pred = [int(x) for x in pb.exact_peak(schedule)]
+    mems = [g[7] for g in gathered]
+    GiB = 2 ** 30
+    out.update({
+        "loss": next((g[3] for g in gathered if g[3] == g[3]), None),
+        "bubble_rate": sim.bubble_rate if sim else None,
+        "makespan_ms": sim.makespan if sim else None,
+        "ideal_ms": max(sim.busy) if sim else None,
+        "predicted_slots_per_device": pred,
+        "measured_slots_per_device": [g[2] for g in gathered],
+        "pool_bytes_per_device": [g[1] for g in gathered],
+        "device_memory": {
+            "activation_gib_per_device": [(x["activation_pool"] + x["head_pool"]) / GiB for x in mems],
+            "executor_gib_per_device": [x["executor_total"] / GiB for x in mems],
+            "high_water_gib_per_device": [x["device_used_high"] / GiB for x in mems],
+            "baseline_gib_per_device": [x["device_used_at_create"] / GiB for x in mems],
+            "device_total_gib": mems[0]["device_total"] / GiB,
+            "breakdown_device_max": max(mems, key=lambda x: x["executor_total"]),
+            "def": "pb_exec_memory: executor allocations by category; high-water = cudaMemGetInfo total - free "
+                   "sampled after creation and after every synchronised step (whole device)"},
+        "transfer": transfer_summary(gathered),
+        "gathered": gathered, "gall": gall, "sim": sim,
+    })
+    return out
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    from paper_2405_15362_b200 import pipeblock as pb
+    from paper_2405_15362_b200.executor import ModelConfig, synthetic_batch
+
+    if os.environ.get("PB_BENCH_SHARE_GPU"):  # test mode: every rank on cuda:0 (one-GPU box)
+        local = 0
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        if os.environ.get("PB_BENCH_SHARE_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mcfg = CONFIGS[args.model]
+    p = args.gpus
+    m = args.microbatches
+    sched_name = args.schedule or ("zb-h1" if p == 1 else "v-half")
+    if args.compare is None:  # the north-star comparisons at N > 1 (the V blocks need d >= 2)
+        compare = [] if p == 1 else [s for s in ("1f1b", "v-zb", "v-half") + (("v-min",) if args.model == "14b" else ())
+                                     if s != sched_name]
+    else:
+        compare = [s for s in args.compare if s not in ("none", sched_name)]
+    base_cfg = ModelConfig(**mcfg, micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    T = base_cfg.tokens_per_microbatch
+    tokens_np, labels_np = synthetic_batch(base_cfg, m)
+    tok_host = torch.from_numpy(tokens_np).pin_memory()
+    lab_host = torch.from_numpy(labels_np).pin_memory()
+    tok_dev, lab_dev = tok_host.cuda(), lab_host.cuda()
+    torch.cuda.synchronize()
+    coll_dev = "cpu" if os.environ.get("PB_BENCH_SHARE_GPU") else "cuda"
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def reduce(x: float, op) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=coll_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    ctx = {"rank": rank, "world": world, "local": local, "dist": dist, "barrier": barrier,
+           "inputs": (tok_dev, lab_dev, tok_host, lab_host),
+           "max": lambda x: reduce(x, dist.ReduceOp.MAX) if dist else x,
+           "sum": lambda x: reduce(x, dist.ReduceOp.SUM) if dist else x}
+    head = run_schedule(args, ctx, sched_name, headline=True)
+    others = [run_schedule(args, ctx, s, headline=False) for s in compare]
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
 
-    from paper_2405_15362_b200.pipeblock import TimedPass, account
-    passes = [TimedPass(*q) for g in gathered for q in g[0]]
-    sim = account(schedule.topology, passes) if passes else None
-    peaks_pred = pb.exact_peak(schedule)
-    pool_bytes = [g[1] for g in gathered]
+    cfg, schedule, gathered, gall, sim = head["cfg"], head["sched"], head["gathered"], head["gall"], head["sim"]
+    ms, value = head["ms_per_step"], head["tokens_per_s"]
+    tokens_per_step = m * T
+    peaks_pred = head["predicted_slots_per_device"]
     # 1F1B at the same p: predicted slots per device (its slot = one straight stage = 2 V-chunks)
-    ref1 = pb.assemble(pb.build_entry("1f1b", p), m)
-    peaks_1f1b = pb.exact_peak(ref1)
+    peaks_1f1b = pb.exact_peak(pb.assemble(pb.build_entry("1f1b", p), m))
     chunk_units = 2 if schedule.topology.num_stages == 2 * p else 1
-    ours_units = max(peaks_pred) / chunk_units
-    peaks_meas_units = max(g[2] for g in gathered) / chunk_units
-    mem_vs_1f1b = ours_units / max(peaks_1f1b)
+    mem_vs_1f1b = max(peaks_pred) / chunk_units / max(peaks_1f1b)
+    meas_vs_1f1b = max(head["measured_slots_per_device"]) / chunk_units / max(peaks_1f1b)
 
     peaks, peak_kind = measured_peaks()
     roof = None
@@ -389,16 +522,38 @@ def main():
                 "gemm_share_of_device_time": g_ms / sum(g[3] for g in gall),
                 "launches": g_n, "flops_per_step": g_fl,
                 "def": "sum of 2MNK over all GEMM launches of one step / sum of their CUDA-event durations"}
-    # model FLOP utilisation (Megatron F/B/W counts)
+    # model FLOP utilisation (Megatron F/B/W counts: full, non-causal attention FLOPs)
     fl = cfg.flops_per_token()
     model_flops = tokens_per_step * (cfg.layers * (fl["F"] + fl["B"] + fl["W"]) + 3 * fl["head"])
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            cpu = cpu_layer_sample(mcfg, args.cpu_sample_s)
+            cpu = cpu_baseline(mcfg, args)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "error": str(e)}
-    clocks = clk.summary()
+
+    def sched_block(r):
+        dm = r["device_memory"]
+        act = max(dm["activation_gib_per_device"])
+        return {"tokens_per_s": r["tokens_per_s"], "ms_per_step": r["ms_per_step"], "bubble_rate": r["bubble_rate"],
+                "makespan_ms": r["makespan_ms"], "pipeline_roofline_frac": (r["ideal_ms"] / r["makespan_ms"])
+                if r["makespan_ms"] else None,
+                "predicted_slots_per_device": r["predicted_slots_per_device"],
+                "activation_gib_max": act, "high_water_gib_max": max(dm["high_water_gib_per_device"]),
+                "executor_gib_max": max(dm["executor_gib_per_device"]),
+                "transfer_gbps": (r["transfer"] or {}).get("achieved_gbps"),
+                "link": (r["transfer"] or {}).get("link"), "loss": r["loss"], "clocks": r["clocks"]}
+
+    schedules = None
+    if others:
+        schedules = {r["schedule"]: sched_block(r) for r in [head] + others}
+        b = schedules.get("1f1b")
+        if b:
+            for v in schedules.values():
+                v["tokens_per_s_vs_1f1b"] = v["tokens_per_s"] / b["tokens_per_s"]
+                v["activation_vs_1f1b"] = v["activation_gib_max"] / b["activation_gib_max"]
+                v["high_water_vs_1f1b"] = v["high_water_gib_max"] / b["high_water_gib_max"]
+    dm = head["device_memory"]
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": p, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -408,24 +563,33 @@ def main():
                    "schedule": sched_name, "microbatches": m, "micro_batch": args.micro_batch,
                    "stage_layers": list(cfg.stage_layers) if cfg.stage_layers else None,
                    "l2": "no flush: per-step working set (weights+grads+optimizer+activations, tens of GB) >> 126 MB L2"},
-        "bubble_rate": sim.bubble_rate if sim else None,
+        "bubble_rate": head["bubble_rate"],
         "bubble_def": "1 - sum busy / (d * makespan) over measured pass times (simulate.hpp:81-82)",
-        "makespan_ms": sim.makespan if sim else None,
-        "roofline_pipeline": {"ideal_ms": max(sim.busy) if sim else None,
-                              "frac": (max(sim.busy) / sim.makespan) if sim else None,
+        "makespan_ms": head["makespan_ms"],
+        "roofline_pipeline": {"ideal_ms": head["ideal_ms"],
+                              "frac": (head["ideal_ms"] / head["makespan_ms"]) if head["makespan_ms"] else None,
                               "def": "ideal zero-bubble time (max per-device busy) / measured makespan"},
-        "activation_memory": {"predicted_slots_per_device": peaks_pred, "measured_slots_max": max(g[2] for g in gathered),
-                              "pool_bytes_per_device": pool_bytes,
-                              "vs_1f1b": mem_vs_1f1b, "measured_vs_1f1b": peaks_meas_units / max(peaks_1f1b),
-                              "def": "peak activation units (whole-stage microbatches) / 1F1B's at the same p"},
+        "activation_memory": {"predicted_slots_per_device": peaks_pred,
+                              "measured_slots_max": max(head["measured_slots_per_device"]),
+                              "pool_bytes_per_device": head["pool_bytes_per_device"],
+                              "activation_gib_per_device": dm["activation_gib_per_device"],
+                              "device_high_water_gib_per_device": dm["high_water_gib_per_device"],
+                              "device_baseline_gib_per_device": dm["baseline_gib_per_device"],
+                              "executor_gib_per_device": dm["executor_gib_per_device"],
+                              "breakdown_device_max": dm["breakdown_device_max"],
+                              "vs_1f1b": mem_vs_1f1b, "measured_vs_1f1b": meas_vs_1f1b,
+                              "def": "slots: peak activation units (whole-stage microbatches) / 1F1B's predicted at the "
+                                     "same p; bytes: pb_exec_memory allocations and cudaMemGetInfo high-water"},
         "mfu": model_flops / (ms / 1e3) / (p * 1e12) / peaks.get("bf16_tflops", 1687.0),
-        "loss": loss,
-        "clocks": clocks,
-        "e2e": {"value": tokens_per_step / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "def": "pb_exec_step with pinned host tokens/labels, wall clock"},
-        "gpu_launches": int(launches),
+        "mfu_def": "Megatron F/B/W FLOPs (PAPER.md:575, full non-causal attention counted) / (N x measured "
+                   "bf16_tflops burst)",
+        "loss": head["loss"],
+        "clocks": head["clocks"],
+        "e2e": head["e2e"],
+        "gpu_launches": int(head["launches"]),
         "roofline": roof,
-        "transfer": transfer_summary(gathered),
+        "transfer": head["transfer"],
+        "schedules": schedules,
         "cpu_baseline": cpu,
         "reference_schedule": reference_schedule_time(sched_name, p, m),
     }

@@ -89,6 +89,10 @@ typedef struct pb_schedule pb_schedule;
  *   replaces gallery.hpp:499 build_entry + assemble.hpp:405 assemble. */
 int pb_schedule_build(const char* entry, int32_t devices, int32_t microbatches, int32_t do_squeeze,
                       int32_t do_reorder, pb_schedule** out);
+/* build_entry(entry, d) alone (gallery.hpp:499-557): validates the entry / device count and reports the
+ * block's microbatches per block (assemble needs a multiple of it) and whether it needs replicated
+ * weights (gems, chimera: generated and analysed, not executable). */
+int pb_build_info(const char* entry, int32_t devices, int32_t* microbatches_per_block, int32_t* replicated_weights);
 /* A caller-made GridSchedule (e.g. converted from pipeblock::GridSchedule);
  * validated like validate_schedule (assemble.hpp:138-183). */
 int pb_schedule_create(const pb_topology* topo, const pb_pass* passes, size_t n, int32_t microbatches,
@@ -207,6 +211,10 @@ typedef struct pb_model_cfg {
 #define PB_FLAG_TIMELINE 2   /* record per-pass CUDA events (TimedSchedule output) */
 #define PB_FLAG_GEMM_TIMING 4 /* CUDA events around every GEMM launch (roofline of the dominant kernel) */
 #define PB_FLAG_KERNEL_TIMING 8 /* CUDA events around every launch, per-kernel report (pb_exec_kernel_report) */
+#define PB_FLAG_SOLO 32      /* run this device's op list alone (no peers connected): cross-device inputs
+                                are not pulled (the receive slot keeps its contents) and outputs are not
+                                signalled.  Real kernels, real op order, real memory footprint — for
+                                memory / per-pass timing probes of one device of a p-device pipeline */
 #define PB_FLAG_ISOLATE 16   /* in-process group: one pass at a time over all devices (a group-wide GPU
                                 token taken after the pass's cross-device waits), each synchronised —
                                 clean stand-alone per-pass times for pb_replay */
@@ -273,6 +281,25 @@ int pb_exec_param_info(const pb_exec* e, int32_t i, char* name, size_t cap, int6
 int pb_exec_param_get(pb_exec* e, int32_t i, int32_t which /*0 weight bf16->f32, 1 grad f32*/, float* host);
 int pb_exec_param_set(pb_exec* e, int32_t i, const float* host); /* rounds to bf16, sets fp32 master */
 int pb_exec_zero_grads(pb_exec* e);
+
+/* Device memory of one executor.  The executor allocates everything at pb_exec_create (no
+ * allocation inside a step apart from the W-pass GEMM tables of the first step), so
+ * device_used_high (cudaMemGetInfo total - free, sampled after creation, after every
+ * synchronised step and at this call; whole device, all contexts) is the high-water mark. */
+typedef struct pb_exec_memory_t {
+    int64_t weights;          /* fp32 masters + bf16 compute copies */
+    int64_t grads;            /* fp32 gradients (+ the gamma-folded projection gradient buffer) */
+    int64_t optimizer;        /* AdamW first / second moments */
+    int64_t activation_pool;  /* lifespan pool: slot_bytes * exact_peak slots */
+    int64_t head_pool;        /* LM-head pool (final-norm output, logits), last-stage device */
+    int64_t transfer;         /* outbox slots + flag words of the stage-boundary protocol */
+    int64_t scratch;          /* attention / GEMM scratch, step inputs, loss */
+    int64_t executor_total;   /* every cudaMalloc of this executor (sum of the above) */
+    int64_t device_total;     /* cudaMemGetInfo total */
+    int64_t device_used_at_create; /* total - free just before this executor allocated */
+    int64_t device_used_high; /* max sampled total - free */
+} pb_exec_memory_t;
+int pb_exec_memory(pb_exec* e, pb_exec_memory_t* out);
 
 /* The host-side execution plan of one pipeline device — a pure function of the
  * schedule, so every rank derives its peers' outbox layout without talking

@@ -45,25 +45,38 @@ def main():
     full = {}
     for e, p, m in [(e, 4, 8) for e in ENTRIES] + [("v-half", 8, 16), ("v-zb", 2, 4), ("zb-h1", 1, 4)]:
         full[f"{e}/{p}/{m}"] = refpy.assemble(e, p, m)
+    # the other gallery entries (gallery.hpp:186-429): looped (interleaved-*), V with fused backward
+    # (1f1b-v), two microbatches per block (zb-2-3) and the twin-route replicated-weight blocks
+    more = ["interleaved-1f1b", "interleaved-1f1b-uniform", "interleaved-low-mem", "1f1b-v", "zb-2-3", "gems", "chimera"]
+    gallery = [cell(e, p, m) for e in more for p in (2, 3, 4, 8) for m in (4, 8, 16)
+               if not (e == "chimera" and p % 2)]
+    gallery += [cell(e, 1, m) for e in ("zb-2-3", "gems") for m in (2, 8)]
+    for e, p, m in [("interleaved-1f1b", 4, 8), ("interleaved-1f1b-uniform", 2, 4), ("interleaved-low-mem", 4, 8),
+                    ("1f1b-v", 4, 8), ("zb-2-3", 4, 8), ("gems", 2, 4), ("chimera", 4, 4)]:
+        full[f"{e}/{p}/{m}"] = refpy.assemble(e, p, m)
     squeeze_only = {f"{e}/4/16": max(st + du for _, _, _, _, st, du in refpy.assemble(e, 4, 16, True, False))
                     for e in ENTRIES}
     raw = {f"{e}/4/16": max(st + du for _, _, _, _, st, du in refpy.assemble(e, 4, 16, False, False))
            for e in ENTRIES}
-    docs = {f"{e}/{p}/{m}": refpy.emit(e, p, m) for e, p, m in [("v-half", 4, 8), ("1f1b", 2, 2), ("v-zb", 2, 3)]}
+    docs = {f"{e}/{p}/{m}": refpy.emit(e, p, m) for e, p, m in [("v-half", 4, 8), ("1f1b", 2, 2), ("v-zb", 2, 3),
+                                                                 ("interleaved-1f1b", 2, 4), ("zb-2-3", 2, 4),
+                                                                 ("chimera", 2, 2)]}
     errors = {}
-    for e, p, m in [("v-min", 1, 4), ("v-half", 1, 4), ("nope", 4, 4), ("1f1b", 0, 4), ("1f1b", 4, 0)]:
+    for e, p, m in [("v-min", 1, 4), ("v-half", 1, 4), ("nope", 4, 4), ("1f1b", 0, 4), ("1f1b", 4, 0),
+                    ("chimera", 3, 4), ("interleaved-1f1b", 1, 4), ("interleaved-low-mem", 1, 4), ("1f1b-v", 1, 4),
+                    ("zb-2-3", 4, 3), ("gems", 2, 5)]:
         try:
             refpy.assemble(e, p, m)
             errors[f"{e}/{p}/{m}"] = None
         except ValueError as ex:
             errors[f"{e}/{p}/{m}"] = str(ex)
     out = {"generator": "oracle/gen_golden.py over oracle/_ref/libpipeblock_ref.so (reference headers, unmodified)",
-           "paper_profile": PAPER, "sweep": sweep, "extra": extra, "passes": full, "squeeze_only_makespan": squeeze_only,
+           "paper_profile": PAPER, "sweep": sweep, "extra": extra, "gallery": gallery, "passes": full, "squeeze_only_makespan": squeeze_only,
            "raw_makespan": raw, "documents": docs, "errors": errors}
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as f:
         json.dump(out, f, separators=(",", ":"))
-    print(f"wrote {OUT}: {len(sweep)} sweep cells, {len(extra)} extra, {len(full)} full lists")
+    print(f"wrote {OUT}: {len(sweep)} sweep cells, {len(extra)} extra, {len(gallery)} gallery, {len(full)} full lists")
 
 
 if __name__ == "__main__":

@@ -17,7 +17,8 @@ from oracle import refpy
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "tests", "golden", "analysis.json")
-ENTRIES = ["1f1b", "zb-h1", "v-min", "v-half", "v-zb", "zb-h2", "eager-1f1b", "gpipe"]
+ENTRIES = ["1f1b", "zb-h1", "v-min", "v-half", "v-zb", "zb-h2", "eager-1f1b", "gpipe", "gems", "chimera",
+           "interleaved-1f1b", "interleaved-1f1b-uniform", "interleaved-low-mem", "1f1b-v", "zb-2-3"]
 PROFILES = [[1, 1, 1, 0], [12.96, 13.22, 9.76, 0], [1, 2, 1, 0], [1, 1, 1, 0.5], [2.1, 2.6, 1.9, 0.05],
             [1, 3, 0.5, 0], [3, 1, 1, 0.25]]
 SEARCHES = [dict(d=2, limit=4.0), dict(d=2, limit=3.0), dict(d=2, limit=2.0),
@@ -29,6 +30,9 @@ FRONTIERS = [dict(d=2, limits=[1.0, 2.0, 3.0, 3.5, 4.0, 8.0]),
              dict(d=4, limits=[3.0, 4.0, 5.0, 6.0, 8.0], delta_max=2, tau_max=2, profile=[1, 2, 1, 0])]
 RENDERS = [dict(entry=e, d=d, n=n) for e, d, n in [("v-half", 4, 8), ("v-min", 4, 16), ("1f1b", 4, 8),
                                                      ("zb-h1", 8, 32), ("v-zb", 8, 64), ("v-half", 2, 4)]]
+RENDERS += [dict(entry=e, d=d, n=n) for e, d, n in [("interleaved-1f1b", 4, 8), ("interleaved-low-mem", 4, 8),
+                                                      ("1f1b-v", 4, 8), ("zb-2-3", 4, 8), ("chimera", 4, 8),
+                                                      ("gems", 2, 4)]]
 RENDERS += [dict(entry="v-half", d=4, n=8, max_width=40), dict(entry="v-zb", d=2, n=4, color=True, title="a<b&c")]
 RENDERS += [dict(entry=e, d=d, n=n, timed=True, profile=p) for e, d, n, p in
             [("v-half", 4, 8, [12.96, 13.22, 9.76, 0]), ("1f1b", 4, 8, [2.1, 2.6, 1.9, 0.05]),

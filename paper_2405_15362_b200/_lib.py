@@ -52,14 +52,20 @@ class pb_exec_stats(C.Structure):
                 ("gemm_flops", C.c_double), ("gemm_launches", C.c_int64), ("copy_ms", C.c_double)]
 
 
+class pb_exec_memory_t(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("weights", "grads", "optimizer", "activation_pool", "head_pool", "transfer",
+                                         "scratch", "executor_total", "device_total", "device_used_at_create",
+                                         "device_used_high")]
+
+
 # every symbol include/pipeblock_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
-    "pb_last_error", "pb_abi_version", "pb_schedule_build", "pb_schedule_create", "pb_schedule_parse",
+    "pb_last_error", "pb_abi_version", "pb_schedule_build", "pb_build_info", "pb_schedule_create", "pb_schedule_parse",
     "pb_schedule_emit", "pb_schedule_info", "pb_schedule_topology", "pb_schedule_passes", "pb_schedule_exact_peak",
     "pb_simulate", "pb_account", "pb_schedule_destroy", "pb_exec_create", "pb_exec_connect_local",
     "pb_exec_export", "pb_exec_connect_ipc", "pb_exec_step", "pb_exec_step_async", "pb_exec_sync",
     "pb_exec_num_passes", "pb_exec_set_flags", "pb_exec_kernel_report", "pb_exec_stream", "pb_exec_param_count", "pb_exec_param_info", "pb_exec_param_get",
-    "pb_exec_param_set", "pb_exec_zero_grads", "pb_exec_destroy",
+    "pb_exec_param_set", "pb_exec_zero_grads", "pb_exec_memory", "pb_exec_destroy",
 ]
 
 

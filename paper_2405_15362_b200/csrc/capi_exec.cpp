@@ -27,6 +27,7 @@ extern "C" int pb_exec_create(const pb_model_cfg* cfg, const pb_schedule* plan, 
         e->gemm_timing = (cfg->flags & PB_FLAG_GEMM_TIMING) != 0;
         e->kernel_timing = (cfg->flags & PB_FLAG_KERNEL_TIMING) != 0;
         e->isolate = (cfg->flags & PB_FLAG_ISOLATE) != 0;
+        e->solo = (cfg->flags & PB_FLAG_SOLO) != 0;
         if (e->plan.topo.devices == 1) e->connect_local({e}, nullptr);
         *out = new pb_exec{e};
     });
@@ -89,6 +90,7 @@ extern "C" int pb_exec_set_flags(pb_exec* h, int32_t flags) {
         e.gemm_timing = (flags & PB_FLAG_GEMM_TIMING) != 0;
         e.kernel_timing = (flags & PB_FLAG_KERNEL_TIMING) != 0;
         e.isolate = (flags & PB_FLAG_ISOLATE) != 0;
+        e.solo = (flags & PB_FLAG_SOLO) != 0;
     });
 }
 
@@ -142,6 +144,35 @@ extern "C" int pb_exec_param_set(pb_exec* h, int32_t i, const float* host) {
         pbk::f32_to_bf16(e.master + t.off, e.wts + t.off, (t.numel + 3) / 4 * 4, e.cs);
         e.refold();
         cudaStreamSynchronize(e.cs);
+    });
+}
+
+extern "C" int pb_exec_memory(pb_exec* h, pb_exec_memory_t* out) {
+    return pbx::guard([&] {
+        if (!out) throw std::invalid_argument("null argument");
+        auto& e = X(h);
+        auto get = [&](std::initializer_list<const char*> keys) {
+            int64_t v = 0;
+            for (const char* k : keys) {
+                auto it = e.mem_alloc.find(k);
+                if (it != e.mem_alloc.end()) v += int64_t(it->second);
+            }
+            return v;
+        };
+        *out = {};
+        out->weights = get({"params"});
+        out->grads = get({"grads", "folded grads"});
+        out->optimizer = get({"adam"});
+        out->activation_pool = get({"activation pool"});
+        out->head_pool = get({"head pool"});
+        out->transfer = get({"outbox", "flags"});
+        out->executor_total = int64_t(e.mem_alloc_total);
+        out->scratch = out->executor_total - out->weights - out->grads - out->optimizer - out->activation_pool -
+                       out->head_pool - out->transfer;
+        e.sample_device_memory();
+        out->device_total = int64_t(e.mem_device_total);
+        out->device_used_at_create = int64_t(e.mem_used_at_create);
+        out->device_used_high = int64_t(e.mem_used_high);
     });
 }
 

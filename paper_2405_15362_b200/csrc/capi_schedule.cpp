@@ -47,6 +47,15 @@ pb_schedule* finish(Grid g, Document d) {
 
 }  // namespace
 
+extern "C" int pb_build_info(const char* entry, int32_t devices, int32_t* mpb, int32_t* replicated) {
+    return pbx::guard([&] {
+        if (!entry) throw std::invalid_argument("null argument");
+        Build b = build_entry(entry, devices);
+        if (mpb) *mpb = b.block.mb_per_block;
+        if (replicated) *replicated = b.replicated_weights ? 1 : 0;
+    });
+}
+
 extern "C" int pb_schedule_build(const char* entry, int32_t devices, int32_t microbatches, int32_t sq, int32_t re,
                                  pb_schedule** out) {
     return pbx::guard([&] {

@@ -158,6 +158,15 @@ void Exec::build_params() {
 
 Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda_dev)
     : cfg(c), plan(make_plan(grid)), dev(device), cuda(cuda_dev) {
+    try {
+        init(device);
+    } catch (...) {  // e.g. out of device memory part-way: give back what was allocated, then report
+        release();
+        throw;
+    }
+}
+
+void Exec::init(int device) {
     if (device < 1 || device > plan.topo.devices) throw std::invalid_argument("device out of range");
     S = plan.topo.num_stages;
     stage_L.assign(size_t(S) + 1, 0);
@@ -206,10 +215,26 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
     ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking), "stream");
 
+    {
+        size_t fr = 0, tot = 0;
+        ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+        mem_device_total = tot;
+        mem_used_at_create = tot - fr;
+    }
     auto dmalloc = [&](size_t bytes, const char* what) {
         void* p = nullptr;
-        ck(cudaMalloc(&p, std::max<size_t>(bytes, 256)), what);
+        const size_t n = std::max<size_t>(bytes, 256);
+        if (cudaMalloc(&p, n) != cudaSuccess) {
+            cudaGetLastError();
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            throw CudaError(std::string("out of device memory allocating ") + what + " (" + std::to_string(n) +
+                            " B; executor holds " + std::to_string(mem_alloc_total) + " B, device free " +
+                            std::to_string(fr) + " of " + std::to_string(tot) + " B)");
+        }
         allocations.push_back(p);
+        mem_alloc[what] += n;
+        mem_alloc_total += n;
         return p;
     };
     master = static_cast<float*>(dmalloc(n_params * 4, "params"));
@@ -248,6 +273,7 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
 
     nslots = plan.slots[dev];
     pool = static_cast<uint8_t*>(dmalloc(slot_bytes * size_t(std::max(nslots, 1)), "activation pool"));
+    ck(cudaMemsetAsync(pool, 0, slot_bytes * size_t(std::max(nslots, 1)), cs), "memset");  // defined receive slots (PB_FLAG_SOLO)
     // head pool: hf / rstd / logits of the last stage, a slot per live (S, mb) from F(S) to W(S),
     // coloured like the main pool but over stage S alone — a V device holding stages 1 and 2p
     // does not pay the logits in every one of its slots
@@ -307,9 +333,15 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
     peers.assign(size_t(plan.topo.devices) + 1, Peer{});
     peers[dev] = Peer{outbox, flags, false};
     ck(cudaStreamSynchronize(cs), "init");
+    sample_device_memory();
 }
 
-Exec::~Exec() {
+Exec::~Exec() { release(); }
+
+void Exec::release() noexcept {
+    if (released) return;
+    released = true;
+    if (cuda < 0) return;
     cudaSetDevice(cuda);
     cudaDeviceSynchronize();
     for (auto& kv : wgroups) pbk::gemm_group_destroy(kv.second);
@@ -325,9 +357,17 @@ Exec::~Exec() {
             cudaIpcCloseMemHandle(p.flags);
         }
     for (void* p : allocations) cudaFree(p);
+    allocations.clear();
     if (loss_host) cudaFreeHost(loss_host);
-    cudaStreamDestroy(cs);
-    cudaStreamDestroy(xs);
+    if (cs) cudaStreamDestroy(cs);
+    if (xs) cudaStreamDestroy(xs);
+    cudaGetLastError();
+}
+
+void Exec::sample_device_memory() {
+    size_t fr = 0, tot = 0;
+    ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    mem_used_high = std::max(mem_used_high, tot - fr);
 }
 
 // ------------------------------------------------------------------ gamma folding
@@ -572,7 +612,8 @@ uint32_t* Exec::ready_flag(uint32_t* base, int src, int k) const {
 }
 
 void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
-    if (!connected && plan.topo.devices > 1) throw StateError("pb_exec_step before peers are connected");
+    if (!connected && !solo && plan.topo.devices > 1) throw StateError("pb_exec_step before peers are connected");
+    if (solo && group) throw StateError("PB_FLAG_SOLO is for a device without peers (not a connected group)");
     ck(cudaSetDevice(cuda), "cudaSetDevice");
     const int64_t t = steps_done;
     if (group) {
@@ -594,6 +635,10 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     const size_t nin = size_t(m) * T * 4;
     const auto kind = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     ck(cudaEventRecord(ev_step0, cs), "event");
+    // cross-step WAR guard: this step's pulls (copy stream) write receive slots that the previous
+    // step's last users (W passes read dx.back(), F-input slots whose first use has free_op < 0) may
+    // still be reading on the compute stream — start the copy stream after everything enqueued so far
+    ck(cudaStreamWaitEvent(xs, ev_step0, 0), "wait");
     const bool has_first = std::find(stages.begin(), stages.end(), 1) != stages.end();
     const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
     if (on_host) {  // ids index the embedding / logits: reject out-of-range ids before anything is enqueued
@@ -635,7 +680,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
         __nv_bfloat16* in_dst = nullptr;
         const Msg* in = po.in_msg >= 0 ? &plan.msgs[po.in_msg] : nullptr;
         if (in) in_dst = o.kind == Kind::F ? bf(po.slot, L.x[0]) : bf(po.slot, L.dx.back());
-        if (in && !in->local()) {
+        if (in && !in->local() && !solo) {
             if (o.kind == Kind::F && po.free_op >= 0) {
                 ck(cudaStreamWaitEvent(xs, ev_free[size_t(pos_of[po.free_op])], 0), "wait");
             }
@@ -666,7 +711,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
         }
         // ---- outgoing: outbox slot must be drained by its previous (remote) consumer
         const Msg* out = po.out_msg >= 0 ? &plan.msgs[po.out_msg] : nullptr;
-        if (out && out->prev_remote && gen_total(*out) > 1) {
+        if (out && out->prev_remote && gen_total(*out) > 1 && !solo) {
             if (group) {
                 const int64_t tp = out->prev_cross_step ? t - 1 : t;
                 const size_t pm = size_t(out->prev_msg);
@@ -698,7 +743,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
                 break;
         }
         if (timeline) ck(cudaEventRecord(ev_end[j], cs), "event");
-        if (out && !out->local()) {
+        if (out && !out->local() && !solo) {
             if (group) {
                 const size_t mi = size_t(po.out_msg);
                 ck(cudaEventRecord(group->ready_ev[t & 1][mi], cs), "event");
@@ -750,6 +795,7 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
     ck(cudaStreamSynchronize(cs), "step");
     ck(cudaStreamSynchronize(xs), "step");
     pending = false;
+    sample_device_memory();
     if (reinterpret_cast<const int32_t*>(loss_host)[1])
         throw std::invalid_argument("token or label id outside [0, " + std::to_string(V) + ") in the step's device inputs");
     const auto& ops = plan.dev_ops[dev];
@@ -877,7 +923,14 @@ struct IpcBlob {
     int32_t cuda;
     uint64_t plan_ops;
     cudaIpcMemHandle_t outbox, flags;
+    unsigned char uuid[16];  // physical GPU: ranks on the same GPU share its SMs (shares_gpu)
 };
+
+static void gpu_uuid(int cuda, unsigned char out[16]) {
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, cuda), "cudaGetDeviceProperties");
+    std::memcpy(out, &prop.uuid, 16);
+}
 
 size_t Exec::export_blob(void* buf, size_t cap) {
     IpcBlob b{};
@@ -885,6 +938,7 @@ size_t Exec::export_blob(void* buf, size_t cap) {
     b.device = dev;
     b.cuda = cuda;
     b.plan_ops = plan.ops.size();
+    gpu_uuid(cuda, b.uuid);
     ck(cudaSetDevice(cuda), "cudaSetDevice");
     ck(cudaIpcGetMemHandle(&b.outbox, outbox), "cudaIpcGetMemHandle");
     ck(cudaIpcGetMemHandle(&b.flags, flags), "cudaIpcGetMemHandle");
@@ -896,13 +950,27 @@ size_t Exec::export_blob(void* buf, size_t cap) {
 }
 
 void Exec::connect_ipc(const std::vector<std::pair<const void*, size_t>>& blobs) {
+    if (connected) throw StateError("connect_ipc: already connected");
     if (int(blobs.size()) != plan.topo.devices) throw std::invalid_argument("connect_ipc: need one blob per device");
     ck(cudaSetDevice(cuda), "cudaSetDevice");
-    for (const auto& [p, n] : blobs) {
-        if (n < sizeof(IpcBlob)) throw std::invalid_argument("connect_ipc: short blob");
-        IpcBlob b;
-        std::memcpy(&b, p, sizeof b);
+    // validate everything before mapping anything: each device 1..D exactly once, same plan
+    std::vector<IpcBlob> bs(blobs.size());
+    std::vector<int> seen(size_t(plan.topo.devices) + 1, 0);
+    for (size_t i = 0; i < blobs.size(); ++i) {
+        if (!blobs[i].first || blobs[i].second < sizeof(IpcBlob)) throw std::invalid_argument("connect_ipc: short blob");
+        std::memcpy(&bs[i], blobs[i].first, sizeof(IpcBlob));
+        const IpcBlob& b = bs[i];
         if (b.magic != 0x50423230 || b.plan_ops != plan.ops.size()) throw std::invalid_argument("connect_ipc: bad blob");
+        if (b.device < 1 || b.device > plan.topo.devices || seen[size_t(b.device)]++)
+            throw std::invalid_argument("connect_ipc: device " + std::to_string(b.device) +
+                                        " missing, duplicated or out of range in the blob set");
+    }
+    if (!seen[size_t(dev)]) throw std::invalid_argument("connect_ipc: this device's own blob is missing");
+    unsigned char mine[16];
+    gpu_uuid(cuda, mine);
+    for (const IpcBlob& b : bs)
+        if (b.device != dev && std::memcmp(b.uuid, mine, 16) == 0) shares_gpu = true;
+    for (const IpcBlob& b : bs) {
         if (b.device == dev) continue;
         // only neighbours exchange messages, but every peer is mapped (cheap)
         void *ob = nullptr, *fl = nullptr;

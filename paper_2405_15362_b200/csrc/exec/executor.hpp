@@ -83,6 +83,9 @@ class Exec {
   public:
     Exec(const pb_model_cfg& cfg, const vsched::Grid& grid, int device, int cuda_dev);
     ~Exec();
+    void init(int device);
+    void release() noexcept;
+    bool released = false;
     void connect_local(const std::vector<Exec*>& all, std::shared_ptr<LocalGroup> grp);
     size_t export_blob(void* buf, size_t cap);
     void connect_ipc(const std::vector<std::pair<const void*, size_t>>& blobs);
@@ -102,6 +105,13 @@ class Exec {
     cudaStream_t cs = nullptr, xs = nullptr;
     bool shares_gpu = false;  // another pipeline device of the group runs on the same GPU
     bool timeline = true, serial = false, isolate = false, connected = false, pending = false, gemm_timing = false, kernel_timing = false;
+    // PB_FLAG_SOLO: run this device's op list alone — cross-device inputs are not pulled (the receive
+    // slot keeps its contents) and outputs are not signalled — at the device's real memory footprint
+    bool solo = false;
+    // device memory: executor allocations per category (dmalloc) and cudaMemGetInfo samples
+    std::map<std::string, size_t> mem_alloc;
+    size_t mem_alloc_total = 0, mem_device_total = 0, mem_used_at_create = 0, mem_used_high = 0;
+    void sample_device_memory();
     int adam_step = 0;
 
     int64_t steps_done = 0;

@@ -289,14 +289,193 @@ Block chain_block(int d, int64_t x, bool split) {
 
 }  // namespace
 
-std::vector<std::string> gallery_names() {
-    return {"1f1b", "eager-1f1b", "gpipe", "zb-h1", "zb-h2", "v-min", "v-half", "v-zb"};
+std::vector<std::string> gallery_names() {  // gallery.hpp:474-497 listing order
+    return {"1f1b", "eager-1f1b", "gpipe", "gems", "chimera", "interleaved-1f1b", "interleaved-1f1b-uniform",
+            "interleaved-low-mem", "zb-h1", "zb-h2", "1f1b-v", "zb-2-3", "v-min", "v-half", "v-zb"};
 }
 
-// gallery.hpp:499-557 for the entries this executor runs: the straight
-// baselines (1f1b, zb-h1 and their eager/gpipe/zb-h2 relatives) and the three
-// fixed V blocks.  Twin/looped entries (gems, chimera, interleaved-*,
-// 1f1b-v, zb-2-3) are outside the executor's scope and rejected by name.
+namespace {
+
+void put(Block& b, int stage, Kind k, int slot, int64_t at) { b.ops.push_back({stage, k, slot, at}); }
+
+// smallest interval >= 6 whose repetition is residue-clash free (gems / chimera, gallery.hpp:294-300,
+// 318-324); gives up past the block span + 2
+void smallest_clash_free_interval(Block& blk, int64_t span, const std::string& entry) {
+    for (int64_t t = 6;; ++t) {
+        blk.interval = t;
+        if (!residue_clash(blk)) return;
+        if (t > span + 2) throw std::invalid_argument(entry + ": no repeat interval found");
+    }
+}
+
+// gallery.hpp:252-302: replica 0 in 1f1b shape; replica 1's forward chain, then its fused backward
+// chain (reversed), each pass at the first free cell of its device at or after it is ready
+Block gems_block(int d) {
+    Block blk;
+    blk.topo = Topology::twin(d);
+    blk.mb_per_block = 2;
+    std::set<std::pair<int, int64_t>> busy;
+    auto occupy = [&](int stage, Kind k, int slot, int64_t at) {
+        put(blk, stage, k, slot, at);
+        for (int c = 0; c < width(k); ++c) busy.insert({blk.topo.device_of(stage), at + c});
+    };
+    for (int i = 1; i <= d; ++i) {
+        occupy(i, Kind::F, 0, i - 1);
+        occupy(i, Kind::BW, 0, d + 2LL * (d - i));
+    }
+    auto first_fit = [&](int stage, Kind k, int64_t ready) {
+        const int dev = blk.topo.device_of(stage);
+        int64_t at = ready;
+        auto clear = [&] {
+            for (int c = 0; c < width(k); ++c)
+                if (busy.count({dev, at + c})) return false;
+            return true;
+        };
+        while (!clear()) ++at;
+        occupy(stage, k, 1, at);
+        return at + width(k);
+    };
+    int64_t ready = 0;
+    for (int s = d + 1; s <= 2 * d; ++s) ready = first_fit(s, Kind::F, ready);
+    std::map<int, int64_t> f_end;
+    for (const auto& o : blk.ops)
+        if (o.slot == 1 && o.kind == Kind::F) f_end[o.stage] = o.offset + 1;
+    ready = f_end[2 * d];
+    for (int s = 2 * d; s >= d + 1; --s) ready = first_fit(s, Kind::BW, std::max(ready, f_end[s]));
+    int64_t span = 0;
+    for (const auto& o : blk.ops) span = std::max(span, o.offset + width(o.kind));
+    smallest_clash_free_interval(blk, span, "gems");
+    return blk;
+}
+
+Block chimera_block(int d) {  // gallery.hpp:306-326: two mirrored 1f1b half-pipelines
+    if (d % 2 != 0) throw std::invalid_argument("chimera: device count must be even");
+    Block blk;
+    blk.topo = Topology::twin(d);
+    blk.mb_per_block = 2;
+    for (int i = 1; i <= d; ++i) {
+        put(blk, i, Kind::F, 0, i - 1);
+        put(blk, i, Kind::BW, 0, d + 2LL * (d - i));
+    }
+    for (int k = 1; k <= d; ++k) {
+        put(blk, d + k, Kind::F, 1, k - 1);
+        put(blk, d + k, Kind::BW, 1, d + 2LL * (d - k));
+    }
+    smallest_clash_free_interval(blk, 3LL * d, "chimera");
+    return blk;
+}
+
+// gallery.hpp:328-349: depth-2 round robin; instance j starts at 6d*(j div d) + 3*(j mod d)
+Build interleaved_classic(int d) {
+    Build b;
+    b.name = "interleaved-1f1b";
+    b.block.topo = Topology::looped(d, 2);
+    b.block.interval = 6LL * d;
+    for (int i = 1; i <= d; ++i) {
+        put(b.block, i, Kind::F, 0, i - 1);
+        put(b.block, d + i, Kind::F, 0, 3LL * d + i - 1);
+        put(b.block, d + i, Kind::BW, 0, 6LL * d - 2 * i);
+        put(b.block, i, Kind::BW, 0, 9LL * d - 2 * i);
+    }
+    const int64_t dd = d;
+    b.explicit_starts = [dd](int n) {
+        std::vector<int64_t> st(size_t(std::max(n, 0)));
+        for (int j = 0; j < n; ++j) st[size_t(j)] = 6 * dd * (j / dd) + 3 * (j % dd);
+        return st;
+    };
+    return b;
+}
+
+// gallery.hpp:353-386: interval 6; second-chunk forward chain from f2, the second chunk's fused
+// backward head y (first cell with (y + 2d) mod 6 in {0, 3}) and the first chunk's head z (the other
+// class of the two)
+Block interleaved_interval6(int d, int64_t f2) {
+    Block blk;
+    blk.topo = Topology::looped(d, 2);
+    blk.interval = 6;
+    const int64_t two_d = 2LL * d;
+    int64_t y = f2 + d;
+    while ((y + two_d) % 6 != 0 && (y + two_d) % 6 != 3) ++y;
+    const int64_t want = ((3 - (y + two_d) % 6) % 6 + 6) % 6;
+    int64_t z = y + two_d;
+    while ((z + two_d) % 6 != want) ++z;
+    for (int i = 1; i <= d; ++i) {
+        put(blk, i, Kind::F, 0, i - 1);
+        put(blk, d + i, Kind::F, 0, f2 + i - 1);
+        put(blk, d + i, Kind::BW, 0, y + 2LL * (d - i));
+        put(blk, i, Kind::BW, 0, z + 2LL * (d - i));
+    }
+    return blk;
+}
+int64_t first_at_or_after_3_mod_6(int64_t x) {
+    while (x % 6 != 3) ++x;
+    return x;
+}
+
+// gallery.hpp:390-429: V placement, fused backward; the first (lifespan-sum, then lexicographic)
+// offset tuple whose block repeats clash-free and validates
+Block one_f_one_b_v_block(int d) {
+    struct Cand {
+        int64_t key[8];  // sum, df0, df1, db1, db0, t1, t2, t3
+    };
+    std::vector<Cand> cands;
+    for (int64_t a = 1; a <= 4; ++a)
+        for (int64_t b = 1; b <= 4; ++b)
+            for (int64_t c = 2; c <= 5; ++c)
+                for (int64_t e = 2; e <= 5; ++e)
+                    for (int64_t t1 = 1; t1 <= 6; ++t1)
+                        for (int64_t t2 = 1; t2 <= 6; ++t2)
+                            for (int64_t t3 = 2; t3 <= 7; ++t3)
+                                cands.push_back({{a + b + c + e + t1 + t2 + t3, a, b, c, e, t1, t2, t3}});
+    std::stable_sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) {
+        return std::lexicographical_compare(x.key, x.key + 8, y.key, y.key + 8);
+    });
+    for (const Cand& cd : cands) {
+        const int64_t df0 = cd.key[1], df1 = cd.key[2], db1 = cd.key[3], db0 = cd.key[4];
+        const int64_t t1 = cd.key[5], t2 = cd.key[6], t3 = cd.key[7];
+        Block blk;
+        blk.topo = Topology::v_shape(d);
+        blk.interval = 6;
+        std::vector<int64_t> f(size_t(2 * d)), bw(size_t(2 * d));
+        for (int i = 0; i < d; ++i) f[size_t(i)] = i * df0;                      // down leg
+        f[size_t(d)] = f[size_t(d - 1)] + t1;                                     // turn
+        for (int k = d + 1; k < 2 * d; ++k) f[size_t(k)] = f[size_t(k - 1)] + df1; // up leg
+        bw[size_t(2 * d - 1)] = f[size_t(2 * d - 1)] + t2;                       // loss turn-around
+        for (int k = 2 * d - 2; k >= d; --k) bw[size_t(k)] = bw[size_t(k + 1)] + db1;
+        bw[size_t(d - 1)] = bw[size_t(d)] + t3;
+        for (int k = d - 2; k >= 0; --k) bw[size_t(k)] = bw[size_t(k + 1)] + db0;
+        for (int s = 1; s <= 2 * d; ++s) {
+            put(blk, s, Kind::F, 0, f[size_t(s - 1)]);
+            put(blk, s, Kind::BW, 0, bw[size_t(s - 1)]);
+        }
+        if (residue_clash(blk)) continue;
+        if (first_block_violation(blk)) continue;
+        return blk;
+    }
+    throw std::invalid_argument("1f1b-v: no valid offsets in search range");
+}
+
+// gallery.hpp:241-256: two microbatches per block, backward chains at spacing 1, greedy W
+Block zb_2_3_block(int d) {
+    Block blk;
+    blk.topo = Topology::straight(d);
+    blk.interval = 6;
+    blk.mb_per_block = 2;
+    for (int i = 1; i <= d; ++i) {
+        put(blk, i, Kind::F, 0, i - 1);
+        put(blk, i, Kind::B, 0, 2LL * d - i);
+        put(blk, i, Kind::F, 1, i + 1);
+        put(blk, i, Kind::B, 1, 2LL * d + 2 - i);
+    }
+    if (!place_greedy_w(blk)) throw std::invalid_argument("zb-2-3: W placement failed");
+    return blk;
+}
+
+}  // namespace
+
+// gallery.hpp:499-557: all 15 entries.  The executor runs every single-route
+// topology (straight, V, looped); gems / chimera (twin routes over replicated
+// weights) are generated and analysed but rejected by the executor.
 Build build_entry(const std::string& name, int d, const std::map<std::string, int64_t>& params) {
     if (d < 1) throw std::invalid_argument("device count must be positive");
     for (const auto& kv : params)
@@ -342,10 +521,26 @@ Build build_entry(const std::string& name, int d, const std::map<std::string, in
         VChain c;  // gallery.hpp:454-464
         c.df0 = 4; c.df1 = 2; c.db1 = 4; c.db0 = 2;
         b.block = finish_v(v_block(d, c), "v-zb");
-    } else if (name == "gems" || name == "chimera" || name == "interleaved-1f1b" ||
-               name == "interleaved-1f1b-uniform" || name == "interleaved-low-mem" || name == "1f1b-v" ||
-               name == "zb-2-3") {
-        throw std::invalid_argument("gallery entry not supported by the B200 executor: " + name);
+    } else if (name == "gems") {
+        b.block = gems_block(d);
+        b.replicated_weights = true;
+    } else if (name == "chimera") {
+        b.block = chimera_block(d);
+        b.replicated_weights = true;
+    } else if (name == "interleaved-1f1b") {
+        need_two();
+        b = interleaved_classic(d);
+    } else if (name == "interleaved-1f1b-uniform") {
+        need_two();
+        b.block = interleaved_interval6(d, first_at_or_after_3_mod_6(3LL * d));
+    } else if (name == "interleaved-low-mem") {
+        need_two();
+        b.block = interleaved_interval6(d, first_at_or_after_3_mod_6(d));
+    } else if (name == "1f1b-v") {
+        need_two();
+        b.block = one_f_one_b_v_block(d);
+    } else if (name == "zb-2-3") {
+        b.block = zb_2_3_block(d);
     } else {
         throw std::invalid_argument("unknown gallery entry: " + name);
     }

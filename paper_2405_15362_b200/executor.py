@@ -31,6 +31,7 @@ PB_FLAG_TIMELINE = 2
 PB_FLAG_GEMM_TIMING = 4
 PB_FLAG_KERNEL_TIMING = 8
 PB_FLAG_ISOLATE = 16
+PB_FLAG_SOLO = 32
 
 
 @dataclass
@@ -51,6 +52,7 @@ class ModelConfig:
     timeline: bool = True
     serial: bool = False
     gemm_timing: bool = False
+    solo: bool = False  # PB_FLAG_SOLO: one device of a p-device pipeline run alone (memory / timing probe)
     stage_layers: Optional[tuple] = None  # layers per stage (None: layers / num_stages each)
 
     @property
@@ -59,7 +61,7 @@ class ModelConfig:
 
     def c(self) -> pb_model_cfg:
         flags = ((PB_FLAG_TIMELINE if self.timeline else 0) | (PB_FLAG_SERIAL if self.serial else 0)
-                 | (PB_FLAG_GEMM_TIMING if self.gemm_timing else 0))
+                 | (PB_FLAG_GEMM_TIMING if self.gemm_timing else 0) | (PB_FLAG_SOLO if self.solo else 0))
         sl = None
         if self.stage_layers is not None:
             sl = (C.c_int32 * len(self.stage_layers))(*self.stage_layers)
@@ -172,12 +174,22 @@ class DeviceExecutor:
         return self.timeline(), StepStats.of(st)
 
     def set_flags(self, timeline: bool = True, serial: bool = False, gemm_timing: bool = False,
-                  kernel_timing: bool = False, isolate: bool = False) -> None:
+                  kernel_timing: bool = False, isolate: bool = False, solo: Optional[bool] = None) -> None:
+        solo = self.cfg.solo if solo is None else solo
         flags = ((PB_FLAG_TIMELINE if timeline else 0) | (PB_FLAG_SERIAL if serial else 0)
                  | (PB_FLAG_GEMM_TIMING if gemm_timing else 0) | (PB_FLAG_KERNEL_TIMING if kernel_timing else 0)
-                 | (PB_FLAG_ISOLATE if isolate else 0))
+                 | (PB_FLAG_ISOLATE if isolate else 0) | (PB_FLAG_SOLO if solo else 0))
         check(lib().pb_exec_set_flags(self._h, flags))
-        self.cfg = __import__("dataclasses").replace(self.cfg, timeline=timeline, serial=serial, gemm_timing=gemm_timing)
+        self.cfg = __import__("dataclasses").replace(self.cfg, timeline=timeline, serial=serial, gemm_timing=gemm_timing,
+                                                     solo=solo)
+
+    def memory(self) -> Dict[str, int]:
+        """Device memory of this executor (pb_exec_memory): allocation per category, and the
+        device's cudaMemGetInfo used bytes before creation and at the high-water mark."""
+        from ._lib import pb_exec_memory_t
+        m = pb_exec_memory_t()
+        check(lib().pb_exec_memory(self._h, C.byref(m)))
+        return {n: int(getattr(m, n)) for n, _ in m._fields_}
 
     def kernel_report(self) -> Dict[str, list]:
         import json

@@ -96,6 +96,8 @@ class RunTimeProfile:  # model.hpp:189-206
 class BlockBuild:  # gallery.hpp:16-26 (the block itself lives in the library)
     entry: str
     devices: int
+    microbatches_per_block: int = 1
+    replicated_weights: bool = False
 
 
 @dataclass
@@ -163,10 +165,15 @@ def fnv1a64(data: bytes) -> str:
 
 def build_entry(name: str, d: int) -> BlockBuild:
     """Checks the entry/device-count combination now (gallery.hpp:499-557)."""
-    h = C.c_void_p()
-    check(lib().pb_schedule_build(name.encode(), d, 1, 0, 0, C.byref(h)))
-    lib().pb_schedule_destroy(h)
-    return BlockBuild(name, d)
+    mpb, rep = C.c_int32(), C.c_int32()
+    check(lib().pb_build_info(name.encode(), d, C.byref(mpb), C.byref(rep)))
+    return BlockBuild(name, d, mpb.value, bool(rep.value))
+
+
+def gallery_names() -> List[str]:
+    """The reference gallery's 15 entries in listing order (gallery.hpp:474-497)."""
+    return ["1f1b", "eager-1f1b", "gpipe", "gems", "chimera", "interleaved-1f1b", "interleaved-1f1b-uniform",
+            "interleaved-low-mem", "zb-h1", "zb-h2", "1f1b-v", "zb-2-3", "v-min", "v-half", "v-zb"]
 
 
 def assemble(build: BlockBuild, n: int, do_squeeze: bool = True, do_reorder: bool = True) -> GridSchedule:
@@ -271,7 +278,7 @@ class GrowthReport:  # growth.hpp:13-22
 
 def _block_schedule(x) -> GridSchedule:
     # a BlockBuild names a gallery block; one instance carries it (growth needs the block only)
-    return assemble(x, 1, False, False) if isinstance(x, BlockBuild) else x
+    return assemble(x, x.microbatches_per_block, False, False) if isinstance(x, BlockBuild) else x
 
 
 def growth_rate(block, profile: RunTimeProfile = RunTimeProfile()) -> GrowthReport:

@@ -1,6 +1,7 @@
 """The C-ABI library loads on a CPU-only host and exports every symbol the
 public headers declare (no compute calls here)."""
 import ctypes
+import pytest
 import os
 import re
 
@@ -49,3 +50,16 @@ def test_no_gpu_executor_fails_loudly():
     assert rc == _lib.PB_ECUDA
     assert lib.pb_last_error()
     lib.pb_schedule_destroy(h)
+
+
+def test_executor_rejects_replicated_weight_blocks():
+    """gems / chimera route microbatches over two weight replicas (twin topology, gallery.hpp:252-326):
+    generated and analysed bit-exactly, but the executor runs single-route models only."""
+    from paper_2405_15362_b200 import pipeblock as pb
+    from paper_2405_15362_b200._lib import ScheduleError
+    from paper_2405_15362_b200.executor import DeviceExecutor, ModelConfig
+    cfg = ModelConfig(layers=8, hidden=256, heads=2, seq=256, vocab=1024)
+    for e in ("gems", "chimera"):
+        sched = pb.assemble(pb.build_entry(e, 2), 4)
+        with pytest.raises(ScheduleError, match="single-route"):
+            DeviceExecutor(cfg, sched, 1, 0)

@@ -202,6 +202,11 @@ CFG16 = ModelConfig(layers=16, hidden=256, heads=2, seq=256, vocab=1024, micro_b
     ("zb-h2", 2, 8, CFG), ("gpipe", 2, 8, CFG), ("eager-1f1b", 2, 8, CFG),   # other straight gallery entries
     ("v-half", 2, 1, CFG), ("v-zb", 4, 3, CFG), ("v-min", 2, 5, CFG),       # m = 1 and m not a multiple of p
     ("v-half", 8, 8, CFG16), ("v-zb", 8, 8, CFG16), ("1f1b", 8, 8, CFG16),  # p = 8: 16 V stages of one layer
+    # looped placement (device i holds stages i and d+i; the F(d)->F(d+1) edge wraps to device 1),
+    # V with fused backward, two microbatches per block
+    ("interleaved-1f1b", 2, 4, CFG), ("interleaved-1f1b", 4, 8, CFG), ("interleaved-1f1b-uniform", 4, 8, CFG),
+    ("interleaved-low-mem", 2, 6, CFG), ("1f1b-v", 2, 8, CFG), ("1f1b-v", 4, 4, CFG), ("zb-2-3", 2, 8, CFG),
+    ("zb-2-3", 4, 4, CFG),
 ])
 def test_more_schedules_match_oracle(entry, p, m, cfg):
     """Executor parity beyond the main sweep: the straight zb-h2 / gpipe / eager-1f1b entries,
@@ -248,3 +253,46 @@ def test_out_of_range_ids_rejected(on_host, what, bad):
         d.zero_grads()
     again = ex.step(tokens, labels).loss
     assert abs(again - ref) < 1e-6 * abs(ref)
+
+
+def test_solo_device_probe_and_memory_accounting():
+    """PB_FLAG_SOLO: one device of a p=4 V-Half pipeline runs its own op list alone (no peers) at its
+    real footprint; pb_exec_memory reports the allocation by category and the device high-water."""
+    import dataclasses
+    from paper_2405_15362_b200.executor import DeviceExecutor
+    sched = pb.assemble(pb.build_entry("v-half", 4), M)
+    tokens, labels = synthetic_batch(CFG, M)
+    peaks = pb.exact_peak(sched)
+    for d in (1, 3):
+        ex = DeviceExecutor(dataclasses.replace(CFG, solo=True), sched, d, 0)
+        tl, st = ex.step(tokens, labels)
+        assert [(q.stage, q.kind, q.microbatch) for q in tl] == \
+            [(q.stage, q.kind, q.microbatch) for q in sched.device_passes(d)]
+        assert st.pool_slots == int(peaks[d - 1]) and st.peer_bytes == 0
+        mem = ex.memory()
+        assert mem["activation_pool"] == st.slot_bytes * st.pool_slots
+        assert (mem["head_pool"] > 0) == (d == 1)  # V: device 1 holds stage 2p (LM head)
+        parts = ("weights", "grads", "optimizer", "activation_pool", "head_pool", "transfer", "scratch")
+        assert sum(mem[k] for k in parts) == mem["executor_total"]
+        assert mem["device_used_high"] >= mem["device_used_at_create"] + mem["executor_total"]
+        assert mem["device_used_high"] <= mem["device_total"]
+        del ex
+
+
+def test_out_of_memory_is_reported_and_released():
+    """A pipeline device that does not fit in HBM fails pb_exec_create with PB_ECUDA and a message
+    naming the allocation, and gives back everything it had allocated (1F1B device 1 of the 14B
+    model at p=8 with micro-batch 5: ~8 x 4 layer-slots of 7.9 GB on top of ~44 GB of weights/state)."""
+    import gc
+    from paper_2405_15362_b200._lib import PipeblockError
+    from paper_2405_15362_b200.executor import DeviceExecutor
+    cfg = ModelConfig(layers=32, hidden=6144, heads=48, seq=6144, vocab=50304, micro_batch=5, solo=True)
+    sched = pb.assemble(pb.build_entry("1f1b", 8), 64)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    with pytest.raises(PipeblockError, match="out of device memory allocating activation pool"):
+        DeviceExecutor(cfg, sched, 1, 0)
+    gc.collect()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 >= free0 - (64 << 20)

@@ -33,8 +33,37 @@ def test_bench_torchrun_shared_gpu(n, sched):
     tr = line["transfer"]  # every stage crossing pulled once per step, timed on the copy stream
     assert tr["bytes_per_step"] > 0 and tr["copy_ms_per_step"] > 0 and tr["achieved_gbps"] > 0
     assert tr["link"].startswith("same-gpu")
+    # the north-star comparisons in the same process group: 1F1B, V-ZB, V-Half side by side
+    sc = line["schedules"]
+    assert set(sc) == {"1f1b", "v-zb", "v-half"}
+    for name, r in sc.items():
+        assert r["tokens_per_s"] > 0 and 0 <= r["bubble_rate"] < 1, name
+        assert r["high_water_gib_max"] >= r["executor_gib_max"] > r["activation_gib_max"] > 0, name
+        assert abs(r["tokens_per_s_vs_1f1b"] * sc["1f1b"]["tokens_per_s"] - r["tokens_per_s"]) < 1e-6 * r["tokens_per_s"]
+    am = line["activation_memory"]
+    assert len(am["device_high_water_gib_per_device"]) == n
 
 
 def test_ipc_step_matches_in_process():
     out = torchrun(2, "tests/_ipc_parity.py", timeout=300)
     assert "IPC_PARITY_OK" in out, out
+
+
+def test_ipc_pipelined_async_steps_with_optimizer():
+    """3 back-to-back pb_exec_step_async with AdamW before one sync (the bench's timed loop at N>1):
+    cross-step flag generations and the copy-stream WAR guard; loss and weight updates vs in-process."""
+    out = torchrun(2, "tests/_ipc_parity.py", "--async-opt", timeout=300)
+    assert "IPC_PARITY_OK" in out, out
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available() or __import__("torch").cuda.device_count() < 2,
+                    reason="needs two physical GPUs (the test box has one; the driver's multi-GPU runs have 8)")
+@pytest.mark.parametrize("mode", [[], ["--async-opt"]])
+def test_ipc_across_distinct_gpus(mode):
+    """Ranks on distinct GPUs: cudaIpcOpenMemHandle of a peer GPU's outbox / flags, pulls over NVLink P2P."""
+    env = dict(os.environ)
+    env.pop("PB_BENCH_SHARE_GPU", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29611", "tests/_ipc_parity.py", "--distinct", *mode]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "IPC_PARITY_OK distinct" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]

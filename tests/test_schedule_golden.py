@@ -35,6 +35,22 @@ def test_extra_cells_bit_exact(golden):
         _check_cell(c)
 
 
+def test_gallery_entries_bit_exact(golden):
+    # the other 10 gallery entries' newer half (gallery.hpp:186-429): interleaved-* (looped), 1f1b-v,
+    # zb-2-3 and the replicated-weight twin blocks gems / chimera
+    entries = {c["entry"] for c in golden["gallery"]}
+    assert entries == {"interleaved-1f1b", "interleaved-1f1b-uniform", "interleaved-low-mem", "1f1b-v", "zb-2-3",
+                       "gems", "chimera"}
+    for c in golden["gallery"]:
+        _check_cell(c)
+    assert pb.gallery_names()[:5] == ["1f1b", "eager-1f1b", "gpipe", "gems", "chimera"]
+    assert len(pb.gallery_names()) == 15
+    for e in pb.gallery_names():
+        b = pb.build_entry(e, 4)
+        assert b.replicated_weights == (e in ("gems", "chimera"))
+        assert b.microbatches_per_block == (2 if e in ("gems", "chimera", "zb-2-3") else 1)
+
+
 def test_full_op_lists(golden):
     for key, passes in golden["passes"].items():
         e, p, m = key.split("/")
