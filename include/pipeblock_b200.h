@@ -172,6 +172,10 @@ typedef struct pb_frontier_point { /* FrontierPoint (search.hpp:58-64) */
  * pb_exec_create unchanged; NULL when infeasible. */
 int pb_search(const pb_search_spec* spec, pb_search_result* out, char* message, size_t cap, size_t* len,
               pb_schedule** schedule);
+/* The family block of one parameter tuple (e.g. a pb_search winner, search.hpp:208-216 rebuild)
+ * assembled at `microbatches` (squeeze + reorder), validated like validate_block + residue check:
+ * runs on the executor at the step's own microbatch count. */
+int pb_search_assemble(int32_t devices, const pb_search_params* params, int32_t microbatches, pb_schedule** out);
 int pb_frontier(const pb_search_spec* spec, const double* limits, size_t n, pb_frontier_point* out); /* :240 */
 
 enum { PB_RENDER_SVG = 0, PB_RENDER_ASCII = 1 };

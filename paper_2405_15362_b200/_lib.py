@@ -60,7 +60,7 @@ class pb_exec_memory_t(C.Structure):
 
 # every symbol include/pipeblock_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
-    "pb_last_error", "pb_abi_version", "pb_schedule_build", "pb_build_info", "pb_schedule_create", "pb_schedule_parse",
+    "pb_last_error", "pb_abi_version", "pb_schedule_build", "pb_build_info", "pb_search_assemble", "pb_schedule_create", "pb_schedule_parse",
     "pb_schedule_emit", "pb_schedule_info", "pb_schedule_topology", "pb_schedule_passes", "pb_schedule_exact_peak",
     "pb_simulate", "pb_account", "pb_schedule_destroy", "pb_exec_create", "pb_exec_connect_local",
     "pb_exec_export", "pb_exec_connect_ipc", "pb_exec_step", "pb_exec_step_async", "pb_exec_sync",

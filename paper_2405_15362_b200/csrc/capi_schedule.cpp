@@ -302,6 +302,30 @@ extern "C" int pb_min_memory_for_od_bubble(int32_t d, double* out) {
     });
 }
 
+extern "C" int pb_search_assemble(int32_t devices, const pb_search_params* p, int32_t microbatches, pb_schedule** out) {
+    return pbx::guard([&] {
+        if (!p || !out) throw std::invalid_argument("null argument");
+        SearchParams sp;
+        sp.K = p->K;
+        sp.d0_lo = p->d0_lo;
+        sp.d1_lo = p->d1_lo;
+        sp.d0_hi = p->d0_hi;
+        sp.d1_hi = p->d1_hi;
+        sp.tau1 = p->tau1;
+        sp.tau2 = p->tau2;
+        sp.tau3 = p->tau3;
+        Build b;
+        b.name = "search";
+        b.block = search_block(devices, sp);
+        if (auto v = first_block_violation(b.block)) throw std::invalid_argument("search block: " + *v);
+        if (auto c = residue_clash(b.block))
+            throw std::invalid_argument("search block: repeat clash on device " + std::to_string(c->first));
+        Grid g = assemble(b, microbatches, true, true);
+        Document d = document_for_assembly(b, g, true, true);
+        *out = finish(std::move(g), std::move(d));
+    });
+}
+
 extern "C" int pb_search(const pb_search_spec* spec, pb_search_result* out, char* message, size_t cap, size_t* len,
                          pb_schedule** schedule) {
     return pbx::guard([&] {

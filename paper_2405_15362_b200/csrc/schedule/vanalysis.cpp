@@ -235,9 +235,14 @@ bool chain_cells_distinct(int d, const VEdges& e, int64_t T) {
 
 }  // namespace
 
-Block Family::rebuild(const SearchParams& p) const {
-    Block blk = v_block_edges(spec_.d, p.edges(spec_.d), kInterval);
-    if (!place_greedy_w(blk)) throw std::logic_error("search: W fill failed on rebuild");
+Block Family::rebuild(const SearchParams& p) const { return search_block(spec_.d, p); }
+
+// search.hpp:208-216 (FamilyEvaluation::rebuild) without the family: the block of one parameter
+// tuple, e.g. to assemble a searched winner at the step's own microbatch count
+Block search_block(int d, const SearchParams& p) {
+    if (d < 2) throw std::invalid_argument("search: d must be at least 2");
+    Block blk = v_block_edges(d, p.edges(d), 6);
+    if (!place_greedy_w(blk)) throw std::invalid_argument("search: W fill failed on rebuild");
     return blk;
 }
 

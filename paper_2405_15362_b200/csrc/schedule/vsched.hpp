@@ -272,6 +272,8 @@ struct FrontierPoint {
     double bubble_rate = 1.0, exact_peak = 0.0;
     SearchParams best;
 };
+Block search_block(int d, const SearchParams& p);  // one family member's block (search.hpp:208-216)
+
 class Family {  // search.hpp:121-206 FamilyEvaluation
   public:
     struct Eval {

@@ -377,6 +377,15 @@ def search(spec: SearchSpec) -> SearchResult:
                         bool(r.turn_devices_exercised))
 
 
+def search_assemble(d: int, params: "SearchParams", n: int) -> GridSchedule:
+    """The searched family block `params` at d devices assembled with n microbatches (run it on the executor)."""
+    from ._lib import pb_search_params
+    c = pb_search_params(*params)
+    h = C.c_void_p()
+    check(lib().pb_search_assemble(d, C.byref(c), n, C.byref(h)))
+    return GridSchedule(h)
+
+
 @dataclass
 class FrontierPoint:  # search.hpp:58-64
     limit: float

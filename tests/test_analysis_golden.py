@@ -115,3 +115,17 @@ def test_live_random_growth_vs_reference():
         g = refpy.analysis(op="growth", entry=e, d=d, profile=p)
         r = pb.growth_rate(pb.build_entry(e, d), prof(p))
         assert (r.growth, r.witness, r.cycle_length) == (g["growth"], g["witness"], g["cycle_length"])
+
+
+def test_search_assemble_reproduces_the_winner():
+    """pb_search_assemble(d, winner, eval_n) is the search's own winner schedule bit for bit; at another
+    microbatch count it is the same block repeated (what the executor runs)."""
+    r = pb.search(pb.SearchSpec(d=3, profile=pb.RunTimeProfile(1, 1.2, 0.8, 0), memory_limit=6.0, delta_max=3,
+                                tau_max=3))
+    assert r.feasible
+    same = pb.search_assemble(3, r.best, r.schedule.microbatches)
+    assert [tuple(x) for x in same.passes] == [tuple(x) for x in r.schedule.passes]
+    big = pb.search_assemble(3, r.best, 24)
+    assert big.microbatches == 24 and max(pb.exact_peak(big)) <= 6.0
+    with pytest.raises(pb.ScheduleError if hasattr(pb, "ScheduleError") else Exception):
+        pb.search_assemble(1, r.best, 8)

@@ -296,3 +296,28 @@ def test_out_of_memory_is_reported_and_released():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free1 >= free0 - (64 << 20)
+
+
+def test_search_winner_from_measured_profile_matches_oracle():
+    """§8f row 2: the adaptive search (search.hpp:235) driven by MEASURED per-kind pass times; its winner
+    block, assembled at the step's microbatch count, runs on the executor unchanged and matches the oracle."""
+    base = PipelineExecutor(CFG, pb.assemble(pb.build_entry("zb-h1", 1), M))
+    tokens, labels = synthetic_batch(CFG, M)
+    base.step(tokens, labels)
+    tl = base.step(tokens, labels).timeline
+    mean = {k: float(np.mean([q.duration for q in tl if q.kind == k])) for k in ("F", "B", "W")}
+    prof = pb.RunTimeProfile(mean["F"] / 8, mean["B"] / 8, mean["W"] / 8, 0.0)  # one pipeline stage = 1/8 of the model
+    r = pb.search(pb.SearchSpec(d=2, profile=prof, memory_limit=6.0, delta_max=4, tau_max=4))
+    assert r.feasible and r.exact_peak <= 6.0
+    sched = pb.search_assemble(2, r.best, M)
+    S = sched.topology.num_stages
+    ex = PipelineExecutor(CFG, sched)
+    res = ex.step(tokens, labels)
+    w = {n: torch.from_numpy(ex.get(n, "weight").reshape(N.shapes(CFG, S)[n])) for n in ex.params()}
+    loss_ref, grads_ref = N.reference_step(w, tokens, labels, CFG, S)
+    assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
+    for n in ex.params():
+        assert N.rel_l2(ex.get(n, "grad"), grads_ref[n].numpy().ravel()) < GRAD_REL_L2, n
+    peaks = pb.exact_peak(sched)
+    for d, st in res.per_device.items():
+        assert st.pool_slots == int(peaks[d - 1])

@@ -81,6 +81,46 @@ def probe_device(cfg, sched, d, tok, lab, steps):
         torch.cuda.synchronize()
 
 
+def probe_schedule(cfg, sched, name, devs, tok, lab, steps, comm_ms):
+    """Probe the listed pipeline devices of `sched`; when all p devices fit, replay their measured
+    per-pass durations (pb_replay, simulate.hpp:44-56) into the projected p-GPU step.  The returned
+    run keeps "durations" ((device, stage, kind, mb) -> ms) and "replay" (the SimResult) for callers."""
+    import sys as _sys
+
+    from paper_2405_15362_b200 import pipeblock as pb
+
+    T = cfg.tokens_per_microbatch
+    m = sched.microbatches
+    run = {"schedule": name, "stage_layers": list(cfg.stage_layers) if cfg.stage_layers else None,
+           "predicted_peak_units": [int(x) for x in pb.exact_peak(sched)], "devices": []}
+    for d in devs:
+        r = probe_device(cfg, sched, d, tok, lab, steps)
+        run["devices"].append(r)
+        print(json.dumps({"schedule": name, "device": d, "fits": r["fits"],
+                          "high_water_gib": r.get("high_water_gib"), "activation_gib": r.get("activation_gib"),
+                          "step_ms": r.get("step_ms"), "error": r.get("error")}), file=_sys.stderr, flush=True)
+    fits = [r for r in run["devices"] if r["fits"]]
+    run["all_fit"] = len(fits) == len(run["devices"])
+    if fits:
+        run["max_high_water_gib"] = max(r["high_water_gib"] for r in fits)
+        run["max_executor_gib"] = max(r["executor_gib"] for r in fits)
+        run["max_activation_gib"] = max(r["activation_gib"] for r in fits)
+    if run["all_fit"] and len(run["devices"]) == sched.topology.devices:
+        dur = {}
+        for r in run["devices"]:
+            for (s, k, mb, t) in r["passes"]:
+                dur[(r["device"], s, k, mb)] = t
+        durations = [dur[(q.device, q.stage, q.kind, q.microbatch)] for q in sched.passes]
+        rep = pb.replay(sched, durations, comm_ms)
+        rep0 = pb.replay(sched, durations, 0.0)
+        run.update({"projected_ms_per_step": rep.makespan,
+                    "projected_tokens_per_s": m * T / (rep.makespan / 1e3),
+                    "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
+                    "pipeline_roofline_frac": max(rep.busy) / rep.makespan, "ideal_ms": max(rep.busy),
+                    "busy_ms_per_device": rep.busy, "durations": dur, "replay": rep})
+    return run
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="1.5b", choices=sorted(CONFIGS))
@@ -127,36 +167,12 @@ def main():
         cfg = base
         if args.balance:
             cfg = dataclasses.replace(base, stage_layers=balanced_stage_layers(base, sched.topology))
-        devs = range(1, args.p + 1) if args.devices == "all" else [int(x) for x in args.devices.split(",")]
-        run = {"schedule": name, "stage_layers": list(cfg.stage_layers) if cfg.stage_layers else None,
-               "predicted_peak_units": [int(x) for x in pb.exact_peak(sched)], "devices": []}
-        for d in devs:
-            r = probe_device(cfg, sched, d, tok, lab, args.steps)
-            run["devices"].append(r)
-            print(json.dumps({"schedule": name, "device": d, "fits": r["fits"],
-                              "high_water_gib": r.get("high_water_gib"), "activation_gib": r.get("activation_gib"),
-                              "step_ms": r.get("step_ms"), "error": r.get("error")}), file=sys.stderr, flush=True)
-        fits = [r for r in run["devices"] if r["fits"]]
-        run["all_fit"] = len(fits) == len(run["devices"])
-        if fits:
-            run["max_high_water_gib"] = max(r["high_water_gib"] for r in fits)
-            run["max_executor_gib"] = max(r["executor_gib"] for r in fits)
-            run["max_activation_gib"] = max(r["activation_gib"] for r in fits)
-        if run["all_fit"] and len(run["devices"]) == args.p:
-            dur = {}
-            for r in run["devices"]:
-                for (s, k, mb, t) in r["passes"]:
-                    dur[(r["device"], s, k, mb)] = t
-            durations = [dur[(q.device, q.stage, q.kind, q.microbatch)] for q in sched.passes]
-            rep = pb.replay(sched, durations, comm_ms)
-            rep0 = pb.replay(sched, durations, 0.0)
-            run.update({"projected_ms_per_step": rep.makespan,
-                        "projected_tokens_per_s": m * T / (rep.makespan / 1e3),
-                        "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
-                        "pipeline_roofline_frac": max(rep.busy) / rep.makespan, "ideal_ms": max(rep.busy),
-                        "busy_ms_per_device": rep.busy})
+        devs = list(range(1, args.p + 1)) if args.devices == "all" else [int(x) for x in args.devices.split(",")]
+        run = probe_schedule(cfg, sched, name, devs, tok, lab, args.steps, comm_ms)
         for r in run["devices"]:
             r.pop("passes", None)
+        run.pop("durations", None)
+        run.pop("replay", None)
         out["runs"].append(run)
     for r in out["runs"]:
         b = next((x for x in out["runs"] if x["schedule"] == "1f1b"), None)
