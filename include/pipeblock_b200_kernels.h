@@ -22,18 +22,17 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
 /* Force the GEMM variant: 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2) per 256-row tile
  * where M and N allow it, -1 = automatic (default). Process-wide; for tests and benchmarks. */
 int pbt_gemm_set_cta_group(int32_t cg);
-int pbt_gemm_set_tile_n(int32_t bn);
-int pbt_gemm_set_pair_rows(int32_t rows); /* CTA-pair tile rows: 256, 512 (two A sub-tiles per CTA, M % 512 == 0), -1 = PB_GEMM_BM2 */  /* F-pass CTA-pair tile width: 0 = per-shape choice, 256 / 192 / 160 */
-/* stream-K split tiles: -1 = environment (PB_STREAMK), 0 off, 1 on, 2 hybrid (whole tiles for the full waves, split ragged last wave) */
-int pbt_gemm_set_stream_k(int32_t on);
-/* causal attention, head_dim 128: qkv [T,3h] -> out [T,h], lse2 [heads,T] (base-2 LSE of scaled scores) */
-int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
-/* same on tcgen05/TMEM (the executor's forward attention); seq % 128 == 0 */
+int pbt_gemm_set_pair_rows(int32_t rows); /* CTA-pair tile rows: 256, 512 (two A sub-tiles per CTA, M % 512 == 0), -1 = PB_GEMM_BM2 */
+/* pbt_gemm plus the folded-RMSNorm hooks: rs (may be NULL) = per-row sum of squares, the accumulator row
+ * is scaled by rsqrt(rs[row] * rs_inv_n + rs_eps) (epi 0 / 1 / 3); ss_out (may be NULL, epi 2) += the
+ * row's sum of squares of the stored bf16 outputs. */
+int pbt_gemm_rownorm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn, const void* B,
+                     int32_t ldb, int32_t b_mn, void* C, int32_t ldc, void* C2, const void* aux, int32_t ldaux,
+                     int32_t epi, const float* rs, float rs_inv_n, float rs_eps, float* ss_out, void* stream);
+/* causal attention, head_dim 128, tcgen05/TMEM (the executor's forward attention): qkv [T,3h] -> out [T,h],
+ * lse2 [heads,T] (base-2 LSE of scaled scores); seq % 128 == 0 */
 int pbt_attn_fwd_tc(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
-/* dqkv [T,3h]; dsum [heads,T], dq_acc [T,h] fp32 scratch */
-int pbt_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum, float* dq_acc,
-                 void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream);
-/* same on tcgen05/TMEM (the executor's backward attention) */
+/* backward on tcgen05/TMEM (the executor's): dqkv [T,3h]; dsum [heads,T], dq_acc [T,h] fp32 scratch */
 int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum, float* dq_acc,
                     void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream);
 int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h, void* stream);

@@ -31,24 +31,28 @@ extern "C" int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t 
     });
 }
 
+extern "C" int pbt_gemm_rownorm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn,
+                                const void* B, int32_t ldb, int32_t b_mn, void* C, int32_t ldc, void* C2,
+                                const void* aux, int32_t ldaux, int32_t epi, const float* rs, float rs_inv_n,
+                                float rs_eps, float* ss_out, void* stream) {
+    return pbx::guard([&] {
+        pbk::GemmArgs g;
+        g.M = M, g.N = N, g.K = K;
+        g.A = static_cast<const __nv_bfloat16*>(A), g.lda = lda, g.a_mn = a_mn != 0;
+        g.B = static_cast<const __nv_bfloat16*>(B), g.ldb = ldb, g.b_mn = b_mn != 0;
+        g.C = C, g.ldc = ldc, g.C2 = C2;
+        g.aux = static_cast<const __nv_bfloat16*>(aux), g.ldaux = ldaux;
+        g.epi = epi;
+        g.rs = rs, g.rs_inv_n = rs_inv_n, g.rs_eps = rs_eps, g.ss_out = ss_out;
+        pbk::gemm(g, static_cast<cudaStream_t>(stream));
+        cuda_check("pbt_gemm_rownorm");
+    });
+}
+
 #define BF(p) static_cast<const __nv_bfloat16*>(p)
 #define BFM(p) static_cast<__nv_bfloat16*>(p)
 #define ST(s) static_cast<cudaStream_t>(s)
 
-extern "C" int pbt_attn_fwd(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads,
-                            void* stream) {
-    return pbx::guard([&] {
-        pbk::attn_fwd(BF(qkv), BFM(out), lse2, batch, seq, heads, ST(stream));
-        cuda_check("pbt_attn_fwd");
-    });
-}
-extern "C" int pbt_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum,
-                            float* dq_acc, void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream) {
-    return pbx::guard([&] {
-        pbk::attn_bwd(BF(qkv), BF(out), BF(dout), lse2, dsum, dq_acc, BFM(dqkv), batch, seq, heads, ST(stream));
-        cuda_check("pbt_attn_bwd");
-    });
-}
 extern "C" int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h,
                                void* stream) {
     return pbx::guard([&] {
@@ -114,20 +118,9 @@ extern "C" int pbt_gemm_set_cta_group(int32_t cg) {
     return pbx::guard([&] { pbk::gemm_force_cta_group(cg); });
 }
 
-extern "C" int pbt_gemm_set_tile_n(int32_t bn) {
-    return pbx::guard([&] {
-        if (bn != 0 && bn != 256 && bn != 192 && bn != 160) throw std::invalid_argument("tile N must be 0, 256, 192 or 160");
-        pbk::gemm_force_bn(bn);
-    });
-}
-
 extern "C" int pbt_gemm_set_pair_rows(int32_t rows) {
     return pbx::guard([&] {
         if (rows != -1 && rows != 256 && rows != 512) throw std::invalid_argument("pair rows must be -1, 256 or 512");
         pbk::gemm_force_bm2(rows < 0 ? -1 : rows == 512 ? 1 : 0);
     });
-}
-
-extern "C" int pbt_gemm_set_stream_k(int32_t on) {
-    return pbx::guard([&] { pbk::gemm_force_stream_k(on); });
 }

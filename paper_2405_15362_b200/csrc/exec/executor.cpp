@@ -96,23 +96,36 @@ void Exec::build_layout() {
         L.layer.resize(Lc);
         for (int l = 0; l < Lc; ++l) {
             auto& y = L.layer[l];
-            y.a = add(cur, Th * 2);
+            if (!fold) y.a = add(cur, Th * 2);
             y.qkv = add(cur, 3 * Th * 2);
             y.o = add(cur, Th * 2);
             y.x1 = add(cur, Th * 2);
-            y.b = add(cur, Th * 2);
+            if (!fold) y.b = add(cur, Th * 2);
             y.u = add(cur, 4 * Th * 2);
             y.gl = add(cur, 4 * Th * 2);
             y.dqkv = add(cur, 3 * Th * 2);
             y.dx1 = add(cur, Th * 2);
-            y.rstd1 = add(cur, size_t(T) * 4);
-            y.rstd2 = add(cur, size_t(T) * 4);
+            if (!fold) {
+                y.rstd1 = add(cur, size_t(T) * 4);
+                y.rstd2 = add(cur, size_t(T) * 4);
+            }
             y.lse = add(cur, size_t(H) * T * 4);
+        }
+        if (fold) {  // one block of per-token sums of squares, zeroed at the start of every F pass
+            L.ss_bytes = size_t(2 * Lc + 1) * T * 4;
+            L.ss = add(cur, L.ss_bytes);
+            for (int l = 0; l < Lc; ++l) {
+                L.layer[l].ss1 = L.ss + size_t(2 * l) * T * 4;
+                L.layer[l].ss2 = L.ss + size_t(2 * l + 1) * T * 4;
+            }
+            L.ssf = L.ss + size_t(2 * Lc) * T * 4;
         }
         if (s == S) {  // LM-head buffers live in their own lifespan pool (head slots, see constructor)
             size_t hc = 0;
-            L.hf = add(hc, Th * 2);
-            L.rstdf = add(hc, size_t(T) * 4);
+            if (!fold) {
+                L.hf = add(hc, Th * 2);
+                L.rstdf = add(hc, size_t(T) * 4);
+            }
             L.logits = add(hc, size_t(T) * V * 2);
             head_bytes = hc;
         }
@@ -210,6 +223,7 @@ void Exec::init(int device) {
                                           std::to_string(prop.major * 10 + prop.minor));
     drv();
 
+    fold = std::getenv("PB_NO_FOLD") == nullptr;  // (decides the activation layout)
     build_layout();
     build_params();
     ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
@@ -249,7 +263,6 @@ void Exec::init(int device) {
     for (const auto& t : ptensors)
         pbk::init_normal(master + t.off, t.numel, cfg.seed * 1000003ull + uint64_t(t.id), t.std, t.constant, cs);
     pbk::f32_to_bf16(master, wts, n_params, cs);
-    fold = std::getenv("PB_NO_FOLD") == nullptr;
     if (fold) {
         size_t off = 0;
         for (int s : stages) {
@@ -427,8 +440,9 @@ void Exec::timed(const char* label, Fn&& fn) {
 }
 
 void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __nv_bfloat16* B, bool b_mn, void* C,
-                int epi, const __nv_bfloat16* aux, void* C2, int accumulate) {
+                int epi, const __nv_bfloat16* aux, void* C2, int accumulate, const float* rs, float* ss_out) {
     pbk::GemmArgs g;
+    g.rs = rs, g.rs_inv_n = 1.f / float(h), g.rs_eps = kNormEps, g.ss_out = ss_out;
     g.M = M, g.N = N, g.K = K;
     g.A = A, g.a_mn = a_mn, g.lda = a_mn ? M : K;
     g.B = B, g.b_mn = b_mn, g.ldb = b_mn ? N : K;
@@ -477,9 +491,9 @@ void Exec::build_w_groups() {
                 const auto& y = L.layer[l];
                 const auto& w = P.layers[l];
                 add(h, 4 * h, bf(slot, L.dx[l + 1]), bf(slot, y.gl), G(w.w2));
-                add(4 * h, h, bf(slot, y.u), bf(slot, y.b), GW(w.w1));
+                add(4 * h, h, bf(slot, y.u), bf(slot, fold ? y.x1 : y.b), GW(w.w1));
                 add(h, h, bf(slot, y.dx1), bf(slot, y.o), G(w.wo));
-                add(3 * h, h, bf(slot, y.dqkv), bf(slot, y.a), GW(w.wqkv));
+                add(3 * h, h, bf(slot, y.dqkv), bf(slot, fold ? L.x[l] : y.a), GW(w.wqkv));
             }
             bool ok = true;
             for (const auto& g : v) ok = ok && pbk::gemm_group_ok(g);
@@ -521,27 +535,59 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         timed("embed_fwd", [&] { pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, V, id_err(), cs); });
         ++launches;
     }
+    if (fold) {
+        // RMSNorm folded into the GEMMs around it (gamma is folded into the consuming weights, see
+        // fold_weight): the residual epilogues accumulate each row's sum of squares, the consuming
+        // projection scales its accumulator rows by rstd = rsqrt(ss / h + eps); x-hat is never stored.
+        ck(cudaMemsetAsync(f32(slot, L.ss), 0, L.ss_bytes, cs), "memset");
+        timed("row_sumsq", [&] { pbk::row_sumsq(x0, f32(slot, L.layer.empty() ? L.ssf : L.layer[0].ss1), T, h, cs); });
+        ++launches;
+    }
     for (int l = 0; l < Lc; ++l) {
         const auto& y = L.layer[l];
         const auto& w = P.layers[l];
         __nv_bfloat16* x = bf(slot, L.x[l]);
         __nv_bfloat16* xo = (l == Lc - 1 && s < S) ? out : bf(slot, L.x[l + 1]);
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(x, fold ? nullptr : W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs); });
+        if (fold) {
+            float* ss_next = l + 1 < Lc ? f32(slot, L.layer[l + 1].ss1) : (s == S ? f32(slot, L.ssf) : nullptr);
+            gemm(T, 3 * h, h, x, false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE, nullptr, nullptr, 0,
+                 f32(slot, y.ss1));
+            timed("attn_fwd", [&] { pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs); });
+            gemm(T, h, h, bf(slot, y.o), false, W(w.wo), false, bf(slot, y.x1), pbk::EPI_RESID, x, nullptr, 0, nullptr,
+                 f32(slot, y.ss2));
+            gemm(T, 4 * h, h, bf(slot, y.x1), false, W(w.w1), false, bf(slot, y.u), pbk::EPI_GELU, nullptr,
+                 bf(slot, y.gl), 0, f32(slot, y.ss2));
+            gemm(T, h, 4 * h, bf(slot, y.gl), false, W(w.w2), false, xo, pbk::EPI_RESID, bf(slot, y.x1), nullptr, 0,
+                 nullptr, ss_next);
+            ++launches;
+            continue;
+        }
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(x, W(w.g1), bf(slot, y.a), f32(slot, y.rstd1), T, h, cs); });
         gemm(T, 3 * h, h, bf(slot, y.a), false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE);
         timed("attn_fwd", [&] { pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs); });
         gemm(T, h, h, bf(slot, y.o), false, W(w.wo), false, bf(slot, y.x1), pbk::EPI_RESID, x);
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, y.x1), fold ? nullptr : W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs); });
+        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, y.x1), W(w.g2), bf(slot, y.b), f32(slot, y.rstd2), T, h, cs); });
         gemm(T, 4 * h, h, bf(slot, y.b), false, W(w.w1), false, bf(slot, y.u), pbk::EPI_GELU, nullptr,
              bf(slot, y.gl));
         gemm(T, h, 4 * h, bf(slot, y.gl), false, W(w.w2), false, xo, pbk::EPI_RESID, bf(slot, y.x1));
         launches += 3;
     }
     if (s == S) {
-        timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), HB(mb, L.hf), HF(mb, L.rstdf), T, h, cs); });
-        gemm(T, V, h, HB(mb, L.hf), false, W(P.head), false, HB(mb, L.logits), pbk::EPI_STORE);
-        timed("cross_entropy", [&] { pbk::cross_entropy(HB(mb, L.logits), labels + size_t(mb) * T, loss_dev, T, V, 1.f / float(size_t(m) * T),
-                           id_err(), cs); });
-        launches += 2;
+        const float scale = 1.f / float(size_t(m) * T);
+        if (fold) {
+            gemm(T, V, h, bf(slot, L.x[Lc]), false, W(P.head), false, HB(mb, L.logits), pbk::EPI_STORE, nullptr,
+                 nullptr, 0, f32(slot, L.ssf));
+            timed("cross_entropy", [&] {
+                pbk::cross_entropy(HB(mb, L.logits), labels + size_t(mb) * T, loss_dev, T, V, scale, id_err(), cs,
+                                   f32(slot, L.ssf), 1.f / float(h), kNormEps);
+            });
+            ++launches;
+        } else {
+            timed("rmsnorm_fwd", [&] { pbk::rmsnorm_fwd(bf(slot, L.x[Lc]), W(P.gf), HB(mb, L.hf), HF(mb, L.rstdf), T, h, cs); });
+            gemm(T, V, h, HB(mb, L.hf), false, W(P.head), false, HB(mb, L.logits), pbk::EPI_STORE);
+            timed("cross_entropy", [&] { pbk::cross_entropy(HB(mb, L.logits), labels + size_t(mb) * T, loss_dev, T, V, scale, id_err(), cs); });
+            launches += 2;
+        }
     }
 }
 
@@ -550,13 +596,43 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
     (void)mb;
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
+    if (fold) {
+        // Fold mode runs every normalised projection's backward on row-scaled output gradients
+        // (dY' = rstd * dY: the CE kernel, the dGELU epilogue and the attention backward apply it), so
+        // the dX GEMMs yield rstd * dX-hat and the weight GEMMs use the stored x: dW' = dY'^T x.
+        if (s == S) {
+            gemm(T, h, V, HB(mb, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
+            timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd_x(scratch, bf(slot, L.x[Lc]), f32(slot, L.ssf), nullptr, bf(slot, L.dx[Lc]), T, h, kNormEps, cs); });
+            ++launches;
+        }
+        for (int l = Lc - 1; l >= 0; --l) {
+            const auto& y = L.layer[l];
+            const auto& w = P.layers[l];
+            __nv_bfloat16* dy = bf(slot, L.dx[l + 1]);
+            __nv_bfloat16* dxo = (l == 0 && s > 1) ? out : bf(slot, L.dx[l]);
+            // du' = rstd2 * (dy . W2) * gelu'(u), written over u
+            gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u), nullptr, 0,
+                 f32(slot, y.ss2));
+            gemm(T, h, 4 * h, bf(slot, y.u), false, W(w.w1), true, scratch, pbk::EPI_STORE);
+            timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd_x(scratch, bf(slot, y.x1), f32(slot, y.ss2), dy, bf(slot, y.dx1), T, h, kNormEps, cs); });
+            gemm(T, h, h, bf(slot, y.dx1), false, W(w.wo), true, scratch, pbk::EPI_STORE);
+            timed("attn_bwd", [&] {
+                pbk::attn_bwd_tc(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv),
+                                 mbs, seq, H, cs, f32(slot, y.ss1), 1.f / float(h), kNormEps);
+            });
+            gemm(T, h, 3 * h, bf(slot, y.dqkv), false, W(w.wqkv), true, scratch, pbk::EPI_STORE);
+            timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd_x(scratch, bf(slot, L.x[l]), f32(slot, y.ss1), bf(slot, y.dx1), dxo, T, h, kNormEps, cs); });
+            launches += 6;
+        }
+        return;
+    }
     if (s == S) {
         // dhf = dlogits . Whead ; dx_L = rmsnorm_bwd(dhf)
         gemm(T, h, V, HB(mb, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), fold ? nullptr : W(P.gf), HF(mb, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), W(P.gf), HF(mb, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
                          cs); });
-        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), HF(mb, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
-        launches += fold ? 1 : 2;
+        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[Lc]), HF(mb, L.rstdf), G(P.gf), dq_acc, T, h, cs); });
+        launches += 2;
     }
     for (int l = Lc - 1; l >= 0; --l) {
         const auto& y = L.layer[l];
@@ -566,15 +642,15 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         // du = (dy . W2) * gelu'(u), written over u
         gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u));
         gemm(T, h, 4 * h, bf(slot, y.u), false, W(w.w1), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), fold ? nullptr : W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs); });
-        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), dq_acc, T, h, cs); });
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, y.x1), W(w.g2), f32(slot, y.rstd2), dy, bf(slot, y.dx1), T, h, cs); });
+        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, y.x1), f32(slot, y.rstd2), G(w.g2), dq_acc, T, h, cs); });
         gemm(T, h, h, bf(slot, y.dx1), false, W(w.wo), true, scratch, pbk::EPI_STORE);
         timed("attn_bwd", [&] { pbk::attn_bwd_tc(bf(slot, y.qkv), bf(slot, y.o), scratch, f32(slot, y.lse), dsum, dq_acc, bf(slot, y.dqkv), mbs,
                       seq, H, cs); });
         gemm(T, h, 3 * h, bf(slot, y.dqkv), false, W(w.wqkv), true, scratch, pbk::EPI_STORE);
-        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), fold ? nullptr : W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs); });
-        if (!fold) timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), dq_acc, T, h, cs); });
-        launches += fold ? 6 : 8;
+        timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[l]), W(w.g1), f32(slot, y.rstd1), bf(slot, y.dx1), dxo, T, h, cs); });
+        timed("rmsnorm_dgamma", [&] { pbk::rmsnorm_dgamma(scratch, bf(slot, L.x[l]), f32(slot, y.rstd1), G(w.g1), dq_acc, T, h, cs); });
+        launches += 8;
     }
 }
 
@@ -590,12 +666,13 @@ void Exec::pass_weight(int s, int mb, int slot) {
         const auto& y = L.layer[l];
         const auto& w = P.layers[l];
         gemm(h, 4 * h, T, bf(slot, L.dx[l + 1]), true, bf(slot, y.gl), true, G(w.w2), pbk::EPI_F32, nullptr, nullptr, 1);
-        gemm(4 * h, h, T, bf(slot, y.u), true, bf(slot, y.b), true, GW(w.w1), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(4 * h, h, T, bf(slot, y.u), true, bf(slot, fold ? y.x1 : y.b), true, GW(w.w1), pbk::EPI_F32, nullptr, nullptr, 1);
         gemm(h, h, T, bf(slot, y.dx1), true, bf(slot, y.o), true, G(w.wo), pbk::EPI_F32, nullptr, nullptr, 1);
-        gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, y.a), true, GW(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, fold ? L.x[l] : y.a), true, GW(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
     }
     if (s == S)
-        gemm(V, h, T, HB(mb, L.logits), true, HB(mb, L.hf), true, GW(P.head), pbk::EPI_F32, nullptr, nullptr, 1);
+        gemm(V, h, T, HB(mb, L.logits), true, fold ? bf(slot, L.x[Lc]) : HB(mb, L.hf), true, GW(P.head), pbk::EPI_F32,
+             nullptr, nullptr, 1);
     if (s == 1) {
         timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, V, id_err(), cs); });
         ++launches;
@@ -624,8 +701,6 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
             return true;
         });
     }
-    // concurrent passes of devices sharing this GPU: whole-tile GEMMs only (no stream-K spin waits)
-    pbk::gemm_allow_stream_k(isolate || !shares_gpu);
     launches = 0;
     peer_bytes = 0;
     copied.assign(plan.dev_ops[dev].size(), 0);

@@ -17,13 +17,17 @@
 
 namespace pbx {
 
+constexpr float kNormEps = 1e-5f;  // RMSNorm epsilon (oracle/numerics.py rmsnorm)
+
 struct LayerSlots {  // byte offsets inside an activation slot
-    size_t a, qkv, o, x1, b, u, gl, dqkv, dx1, rstd1, rstd2, lse;
+    size_t a, qkv, o, x1, b, u, gl, dqkv, dx1, rstd1, rstd2, lse;  // a, b, rstd1/2: unfolded path only
+    size_t ss1, ss2;  // fold mode: per-token sum of squares of x (norm1) and x1 (norm2)
 };
 struct StageLayout {
     std::vector<size_t> x, dx;  // Lc+1 residual-stream buffers and their gradients
     std::vector<LayerSlots> layer;
-    size_t hf = 0, rstdf = 0, logits = 0;
+    size_t hf = 0, rstdf = 0, logits = 0;  // hf, rstdf: unfolded path only
+    size_t ss = 0, ss_bytes = 0, ssf = 0;   // fold mode: the stage's sum-of-squares block, final norm's
     size_t bytes = 0;
 };
 struct LayerParams {
@@ -125,8 +129,11 @@ class Exec {
     __nv_bfloat16* outbox_ptr(int k) const;
     const __nv_bfloat16* W(size_t p) const { return wts + ptensors[p].off; }
     float* G(size_t p) const { return grads + ptensors[p].off; }
+    // rs: folded-RMSNorm row statistic of the A rows (sum of squares over h); ss_out: residual epilogue's
+    // sum of squares of the output rows (the next norm's statistic)
     void gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __nv_bfloat16* B, bool b_mn, void* C,
-              int epi, const __nv_bfloat16* aux = nullptr, void* C2 = nullptr, int accumulate = 0);
+              int epi, const __nv_bfloat16* aux = nullptr, void* C2 = nullptr, int accumulate = 0,
+              const float* rs = nullptr, float* ss_out = nullptr);
     void pass_forward(int s, int mb, int slot, __nv_bfloat16* out);
     void pass_backward(int s, int mb, int slot, __nv_bfloat16* out);
     void pass_weight(int s, int mb, int slot);

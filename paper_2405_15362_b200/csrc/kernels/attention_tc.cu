@@ -29,7 +29,6 @@ constexpr int D = 128;
 constexpr int BQ = 128;
 constexpr int BK = 128;
 constexpr int kTile = BQ * D * 2;  // 32 KB: two 128B-swizzled atoms of [128 rows][64]
-constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
 constexpr int kFwdStages = 3;  // K/V ring depth of the forward kernel
@@ -52,6 +51,42 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
         "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
+// ------------------------------------------------------------------ backward helpers
+// D[h][t] = sum_d dO * O (the softmax-backward row term) and zero the fp32 dQ accumulator.
+__global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
+                                    float* __restrict__ dsum, float* __restrict__ dq_acc, int H, int T) {
+    pdl_wait();
+    pdl_launch();
+    const int t = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int head = warp; head < H; head += blockDim.x >> 5) {
+        const size_t off = size_t(t) * H * D + head * D + lane * 4;
+        uint2 a = *reinterpret_cast<const uint2*>(dout + off);
+        uint2 b = *reinterpret_cast<const uint2*>(out + off);
+        float s = bf16_lo(a.x) * bf16_lo(b.x) + bf16_hi(a.x) * bf16_hi(b.x) + bf16_lo(a.y) * bf16_lo(b.y) +
+                  bf16_hi(a.y) * bf16_hi(b.y);
+#pragma unroll
+        for (int k = 16; k; k >>= 1) s += __shfl_xor_sync(0xffffffff, s, k);
+        if (lane == 0) dsum[size_t(head) * T + t] = s;
+        *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// dQ (bf16, into the q columns of dqkv) = scale * dq_acc, times the row's folded-RMSNorm factor
+// rsqrt(rs[t] * rs_inv_n + rs_eps) when rs is given (dqkv' = rstd1 * dqkv, see executor.cpp)
+__global__ void attn_dq_store_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int H,
+                                     float scale, const float* __restrict__ rs, float rs_inv_n, float rs_eps) {
+    pdl_wait();
+    pdl_launch();
+    const int t = blockIdx.x;
+    const float f = rs ? scale * rsqrtf(rs[t] * rs_inv_n + rs_eps) : scale;
+    for (int c = threadIdx.x * 4; c < H * D; c += blockDim.x * 4) {
+        float4 v = *reinterpret_cast<const float4*>(dq_acc + size_t(t) * H * D + c);
+        uint2 o = make_uint2(pack_bf16(v.x * f, v.y * f), pack_bf16(v.z * f, v.w * f));
+        *reinterpret_cast<uint2*>(dqkv + size_t(t) * 3 * H * D + c) = o;
+    }
+}
+
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -340,265 +375,11 @@ __global__ void __launch_bounds__(192, 1)
 // One CTA per (128-key tile kb, head, sequence), looping over query tiles qb >= kb:
 //   S^T  = K Q^T,  dP^T = V dO^T                       -> TMEM [0,128), [128,256)
 //   8 compute warps (2 per SM sub-partition, column halves; thread = key row):
-//        P^T = exp2(S^T*c - lse2[q]),  dS^T = P^T (dP^T - D[q])   -> bf16 smem, 128B-swizzled
+//        P^T = exp2(S^T*c - lse2[q]),  dS^T = P^T (dP^T - D[q])
 //   dV += P^T dO,  dK += dS^T Q                          -> TMEM [256,384), [384,512)
-//   dQ_tile = dS K  (A = dS^T read MN-major)             -> TMEM [0,128)
-//        -> fp32 smem (reusing the P^T/dS^T buffers) -> TMA bulk reduce-add into dq_acc
+//   dQ_tile = dS K                                       -> fp32 smem -> TMA bulk reduce-add into dq_acc
+// Shared memory: K, V, double-buffered Q / dO tiles, the dS^T tile and the lse / D rows.
 struct BwdSmem {
-    static constexpr int k = 0;
-    static constexpr int v = k + kTile;
-    static constexpr int q = v + kTile;
-    static constexpr int dO = q + kTile;
-    static constexpr int pt = dO + kTile;   // P^T, then (with dst) the 64 KB fp32 dQ staging tile
-    static constexpr int dst = pt + kTile;
-    static constexpr int lse = dst + kTile;  // [2][256] floats: lse2 | D
-    static constexpr int bars = lse + 2048;
-    static constexpr int total = bars + 256 + 1024;
-};
-constexpr int kBwdThreads = 320;
-constexpr int kBwd4Threads = 384;
-
-__device__ __forceinline__ void bar_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
-                       const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T,
-                       float scale) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::bars);
-    uint64_t* kv_full = bars + 0;
-    uint64_t* qdo_full = bars + 1;
-    uint64_t* qdo_empty = bars + 2;
-    uint64_t* s_full = bars + 3;
-    uint64_t* ds_full = bars + 4;
-    uint64_t* dq_full = bars + 5;
-    uint64_t* s_free = bars + 6;
-    uint64_t* dkv_full = bars + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-    float* sL = reinterpret_cast<float*>(sm + BwdSmem::lse);
-
-    const uint32_t warp = warp_id();
-    const int nqb = seq / BQ;
-    // 1-D grid, kb = 0 (most query tiles) of every (head, sequence) dispatched first
-    const int hb = int(blockIdx.x) % (H * (T / seq));
-    const int kb = int(blockIdx.x) / (H * (T / seq));
-    const int head = hb % H, b = hb / H;
-    const int tok0 = b * seq;
-    const int nq = nqb - kb;
-
-    if (warp == 0 && elect_one()) {
-        tma_prefetch(&tm_qkv);
-        tma_prefetch(&tm_do);
-        tma_prefetch(&tm_dq);
-        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 6) ? 8 : 1);
-        fence_barrier_init();
-    }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    pdl_wait();
-    pdl_launch();
-
-    if (warp == 0) {
-        if (elect_one()) {
-            const int ck = H * D + head * D, cv = 2 * H * D + head * D, cq = head * D;
-            const int kr = tok0 + kb * BK;
-            mbar_expect_tx(kv_full, 2 * kTile);
-            tma_load_2d(sm + BwdSmem::k, &tm_qkv, kv_full, ck, kr);
-            tma_load_2d(sm + BwdSmem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
-            tma_load_2d(sm + BwdSmem::v, &tm_qkv, kv_full, cv, kr);
-            tma_load_2d(sm + BwdSmem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
-            for (int i = 0; i < nq; ++i) {
-                if (i > 0) mbar_wait(qdo_empty, (i - 1) & 1);
-                const int qr = tok0 + (kb + i) * BQ;
-                mbar_expect_tx(qdo_full, 2 * kTile);
-                tma_load_2d(sm + BwdSmem::q, &tm_qkv, qdo_full, cq, qr);
-                tma_load_2d(sm + BwdSmem::q + 16384, &tm_qkv, qdo_full, cq + 64, qr);
-                tma_load_2d(sm + BwdSmem::dO, &tm_do, qdo_full, head * D, qr);
-                tma_load_2d(sm + BwdSmem::dO + 16384, &tm_do, qdo_full, head * D + 64, qr);
-            }
-        }
-    } else if (warp == 1) {
-        constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
-        constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
-        constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
-        const uint32_t sk = smem_u32(sm + BwdSmem::k), sv = smem_u32(sm + BwdSmem::v);
-        const uint32_t sq = smem_u32(sm + BwdSmem::q), sdo = smem_u32(sm + BwdSmem::dO);
-        const uint32_t spt = smem_u32(sm + BwdSmem::pt), sdst = smem_u32(sm + BwdSmem::dst);
-        mbar_wait(kv_full, 0);
-        for (int i = 0; i < nq; ++i) {
-            mbar_wait(qdo_full, i & 1);
-            if (i > 0) mbar_wait(s_free, (i - 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
-                }
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
-                }
-                tc_commit(s_full);
-            }
-            __syncwarp();
-            mbar_wait(ds_full, i & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 256, sdesc(spt + o, 16, 1024), sdesc(sdo + kk * 2048, 16384, 1024), id_kmn,
-                           (i | kk) != 0);
-                }
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
-                           (i | kk) != 0);
-                }
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma(tmem + 0, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
-                           id_mnmn, kk != 0);
-                tc_commit(qdo_empty);
-                tc_commit(dq_full);
-            }
-            __syncwarp();
-        }
-        if (elect_one()) tc_commit(dkv_full);
-        __syncwarp();
-    } else {
-        const uint32_t q4 = warp & 3;
-        const int hf = int(warp - 2) >> 2;  // column half handled by this warp
-        const int r = int(q4 * 32 + lane_id());
-        const uint32_t lane_base = (q4 * 32) << 16;
-        const float sl2 = scale * kLog2e;
-        uint8_t* spt = sm + BwdSmem::pt;
-        uint8_t* sdst = sm + BwdSmem::dst;
-        const bool issuer = threadIdx.x == 64;  // warp 2, lane 0: TMA reduce-add of dQ
-        const int key = kb * BK + r;           // key index within the sequence
-        for (int i = 0; i < nq; ++i) {
-            const int qb = kb + i;
-            if (issuer && i > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            float* Lb = sL + (i & 1) * 256;
-            Lb[hf * 128 + r] = hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r]
-                                       : dsum[size_t(head) * T + tok0 + qb * BQ + r];
-            bar_sync_compute();  // lse/D staged; previous dQ tile drained from the staging buffer
-            mbar_wait(s_full, i & 1);
-            tc_fence_after();
-            const bool diag = (qb == kb);
-#pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
-                const int c = hf * 2 + cc;
-                float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + c * 32, sv);
-                tmem_ld32(tmem + lane_base + 128 + c * 32, dp);
-                tmem_ld_wait();
-                float p[32], ds[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int ql = c * 32 + e;
-                    float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
-                    if (diag && key > qb * BQ + ql) v = 0.f;
-                    p[e] = v;
-                    ds[e] = v * (dp[e] - Lb[128 + ql]);
-                }
-#pragma unroll
-                for (int e8 = 0; e8 < 4; ++e8) {
-                    const int col = c * 32 + e8 * 8;
-                    *reinterpret_cast<uint4*>(spt + sw128(r, col)) =
-                        make_uint4(pack_bf16(p[e8 * 8], p[e8 * 8 + 1]), pack_bf16(p[e8 * 8 + 2], p[e8 * 8 + 3]),
-                                   pack_bf16(p[e8 * 8 + 4], p[e8 * 8 + 5]), pack_bf16(p[e8 * 8 + 6], p[e8 * 8 + 7]));
-                    *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
-                        make_uint4(pack_bf16(ds[e8 * 8], ds[e8 * 8 + 1]), pack_bf16(ds[e8 * 8 + 2], ds[e8 * 8 + 3]),
-                                   pack_bf16(ds[e8 * 8 + 4], ds[e8 * 8 + 5]), pack_bf16(ds[e8 * 8 + 6], ds[e8 * 8 + 7]));
-                }
-            }
-            fence_async_smem();
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(ds_full);
-            // dQ tile (thread = query row r): TMEM -> fp32 smem (4 swizzled [128][32] chunks) -> TMA reduce-add
-            mbar_wait(dq_full, i & 1);  // also: every MMA reading P^T / dS^T has retired
-            tc_fence_after();
-#pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
-                const int c = hf * 2 + cc;
-                float v[32];
-                tmem_ld32(tmem + lane_base + c * 32, v);
-                tmem_ld_wait();
-                uint8_t* chunk = spt + c * 16384 + r * 128;
-#pragma unroll
-                for (int g = 0; g < 8; ++g)
-                    *reinterpret_cast<float4*>(chunk + ((g ^ (r & 7)) << 4)) =
-                        make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(s_free);  // TMEM [0,256) free for the next S^T / dP^T
-            fence_async_smem();
-            bar_sync_compute();
-            if (issuer) {
-                const int row = tok0 + qb * BQ;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    asm volatile(
-                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tm_dq)),
-                        "r"(smem_u32(spt + c * 16384)), "r"(head * D + c * 32), "r"(row)
-                        : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-        }
-        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        // dV, dK rows (thread = key row, column half hf)
-        mbar_wait(dkv_full, 0);
-        tc_fence_after();
-        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c = hf * 2 + cc;
-            float v[32], k[32];
-            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
-            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
-            tmem_ld_wait();
-            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
-            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                dv[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
-                                   pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
-                dk[e] = make_uint4(pack_bf16(k[8 * e] * scale, k[8 * e + 1] * scale),
-                                   pack_bf16(k[8 * e + 2] * scale, k[8 * e + 3] * scale),
-                                   pack_bf16(k[8 * e + 4] * scale, k[8 * e + 5] * scale),
-                                   pack_bf16(k[8 * e + 6] * scale, k[8 * e + 7] * scale));
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_free<512>(tmem);
-    }
-}
-
-
-// ------------------------------------------------------------------ backward v3
-// Same decomposition as attn_bwd_tc_kernel (CTA per key tile, loop over query tiles), with
-//   * P^T kept in TMEM (bf16 pairs written over the consumed S^T columns) and fed to the
-//     dV MMA as the A operand straight from TMEM, which frees 32 KB of smem for
-//   * double-buffered Q / dO tiles: the TMA of tile i+1 overlaps tile i,
-//   * dQ staged (fp32) in the tile's consumed Q / dO buffers and sent with one TMA bulk
-//     reduce-add per 16 KB chunk; the producer refills that buffer once the reduce has read it.
-struct Bwd3Smem {
     static constexpr int k = 0;
     static constexpr int v = k + kTile;
     static constexpr int q = v + kTile;       // [2]
@@ -610,290 +391,13 @@ struct Bwd3Smem {
     // window starts 1 KB-aligned when the kernel has no static shared memory)
     static constexpr int total = bars + 256 + 512;
 };
-static_assert(Bwd3Smem::total <= 232448, "attn bwd v3: shared memory over the sm_100 opt-in limit");
+static_assert(BwdSmem::total <= 232448, "attn bwd: shared memory over the sm_100 opt-in limit");
+constexpr int kBwdThreads = 384;
 
+__device__ __forceinline__ void bar_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2, const float* __restrict__ dsum,
-                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
-    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (Bwd3Smem::total)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd3Smem::bars);
-    uint64_t* kv_full = bars + 0;
-    uint64_t* qdo_full = bars + 1;   // [2]
-    uint64_t* qdo_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;
-    uint64_t* ds_full = bars + 6;    // 8 compute warps
-    uint64_t* dq_full = bars + 7;
-    uint64_t* s_free = bars + 8;     // 8 compute warps
-    uint64_t* dkv_full = bars + 9;
-    uint64_t* dq_staged = bars + 10;  // 8 compute warps: this tile's dQ sits in the staging buffer
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
-    float* sL = reinterpret_cast<float*>(sm + Bwd3Smem::lse);
-
-    const uint32_t warp = warp_id();
-    const int nqb = seq / BQ;
-    const int hb = int(blockIdx.x) % (H * (T / seq));
-    const int kb = int(blockIdx.x) / (H * (T / seq));
-    const int head = hb % H, b = hb / H;
-    const int tok0 = b * seq;
-    const int nq = nqb - kb;
-
-    if (warp == 0 && elect_one()) {
-        tma_prefetch(&tm_qkv);
-        tma_prefetch(&tm_do);
-        tma_prefetch(&tm_dq);
-        for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 6 || i == 8 || i == 10) ? 8 : 1);
-        fence_barrier_init();
-    }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;  // [0,128) S^T -> P^T (bf16, cols 0-63) -> dQ ; [128,256) dP^T ; dV ; dK
-    pdl_wait();
-    pdl_launch();
-
-    if (warp == 0) {
-        if (lane_id() == 1) {
-            // dQ reducer: one TMA bulk reduce-add per 16 KB chunk of the staged tile; waiting for the
-            // staging reads here (not in a compute warp) keeps that latency off the tile loop
-            for (int i = 0; i < nq; ++i) {
-                mbar_wait(dq_staged, i & 1);
-                const int row = tok0 + (kb + i) * BQ;
-                uint8_t* stage_q = sm + Bwd3Smem::q + (i & 1) * kTile;
-                uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    asm volatile(
-                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tm_dq)),
-                        "r"(smem_u32((c < 2 ? stage_q : stage_d) + (c & 1) * 16384)), "r"(head * D + c * 32), "r"(row)
-                        : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                mbar_arrive(&qdo_empty[i & 1]);  // staging read out: the producer may refill this buffer
-                ATRACE(i, 7);
-            }
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        if (lane_id() == 0) {
-            const int ck = H * D + head * D, cv = 2 * H * D + head * D, cq = head * D;
-            const int kr = tok0 + kb * BK;
-            mbar_expect_tx(kv_full, 2 * kTile);
-            tma_load_2d(sm + Bwd3Smem::k, &tm_qkv, kv_full, ck, kr);
-            tma_load_2d(sm + Bwd3Smem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
-            tma_load_2d(sm + Bwd3Smem::v, &tm_qkv, kv_full, cv, kr);
-            tma_load_2d(sm + Bwd3Smem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
-            for (int i = 0; i < nq; ++i) {
-                const int st = i & 1;
-                if (i >= 2) mbar_wait(&qdo_empty[st], ((i - 2) >> 1) & 1);
-                const int qr = tok0 + (kb + i) * BQ;
-                uint8_t* qs = sm + Bwd3Smem::q + st * kTile;
-                uint8_t* ds = sm + Bwd3Smem::dO + st * kTile;
-                mbar_expect_tx(&qdo_full[st], 2 * kTile);
-                tma_load_2d(qs, &tm_qkv, &qdo_full[st], cq, qr);
-                tma_load_2d(qs + 16384, &tm_qkv, &qdo_full[st], cq + 64, qr);
-                tma_load_2d(ds, &tm_do, &qdo_full[st], head * D, qr);
-                tma_load_2d(ds + 16384, &tm_do, &qdo_full[st], head * D + 64, qr);
-            }
-        }
-    } else if (warp == 1) {
-        constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
-        constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
-        constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
-        const uint32_t sk = smem_u32(sm + Bwd3Smem::k), sv = smem_u32(sm + Bwd3Smem::v);
-        const uint32_t sdst = smem_u32(sm + Bwd3Smem::dst);
-        mbar_wait(kv_full, 0);
-        for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
-            const uint32_t sq = smem_u32(sm + Bwd3Smem::q + st * kTile);
-            const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + st * kTile);
-            if (lane_id() == 0) ATRACE(i, 8);
-            mbar_wait(&qdo_full[st], (i >> 1) & 1);
-            if (lane_id() == 0) ATRACE(i, 9);
-            tc_fence_after();
-            // dP^T first: [128,256) was read out before the previous tile's ds_full, so this MMA
-            // overlaps the previous tile's dQ drain; S^T waits for [0,128) (dQ) to be free
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
-                }
-            }
-            __syncwarp();
-            if (i > 0) mbar_wait(s_free, (i - 1) & 1);
-            tc_fence_after();
-            if (lane_id() == 0) ATRACE(i, 10);
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
-                }
-                tc_commit(s_full);
-            }
-            __syncwarp();
-            mbar_wait(ds_full, i & 1);
-            tc_fence_after();
-            if (lane_id() == 0) ATRACE(i, 12);
-            if (elect_one()) {
-                // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step; queries 0-63 in
-                // columns [0,32), 64-127 in [96,128))
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 256, tmem + (kk < 4 ? kk * 8 : 96 + (kk - 4) * 8),
-                              sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
-                // dK += dS^T Q
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 384, sdesc(sdst + o, 16, 1024), sdesc(sq + kk * 2048, 16384, 1024), id_kmn,
-                           (i | kk) != 0);
-                }
-                // dQ = dS K -> TMEM [0,128) (after the dV MMA has read P^T there: in-order pipe)
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma(tmem + 0, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
-                           id_mnmn, kk != 0);
-                tc_commit(dq_full);
-            }
-            __syncwarp();
-        }
-        if (elect_one()) tc_commit(dkv_full);
-        __syncwarp();
-    } else {
-        const uint32_t q4 = warp & 3;
-        const int hf = int(warp - 2) >> 2;  // query half (columns of S^T) handled by this warp
-        const int r = int(q4 * 32 + lane_id());
-        const uint32_t lane_base = (q4 * 32) << 16;
-        const float sl2 = scale * kLog2e;
-        uint8_t* sdst = sm + Bwd3Smem::dst;
-        const int key = kb * BK + r;
-        for (int i = 0; i < nq; ++i) {
-            const int qb = kb + i;
-            if (threadIdx.x == 64) ATRACE(i, 0);
-            float* Lb = sL + (i & 1) * 256;
-            Lb[hf * 128 + r] = hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r]
-                                       : dsum[size_t(head) * T + tok0 + qb * BQ + r];
-            bar_sync_compute();  // lse / D of this tile staged
-            if (threadIdx.x == 64) ATRACE(i, 1);
-            mbar_wait(s_full, i & 1);
-            tc_fence_after();
-            if (threadIdx.x == 64) ATRACE(i, 2);
-            const bool diag = (qb == kb);
-            // per 32-column chunk of this half: S^T / dP^T -> P^T (bf16 pairs) and dS^T; each half writes
-            // its P^T over its OWN consumed S^T columns (half 0 -> [0,32), half 1 -> [96,128)), so no
-            // barrier between the halves and only one chunk of S / dP live in registers
-            uint32_t pk[32];
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                const int c0 = hf * 64 + cc * 32;  // first query (column) of this chunk
-                float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + c0, sv);
-                tmem_ld32(tmem + lane_base + 128 + c0, dp);
-                tmem_ld_wait();
-                if (threadIdx.x == 64 && cc == 0) ATRACE(i, 3);
-                if (__builtin_expect(diag, 0)) {  // causal mask on the diagonal tile only
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (key > qb * BQ + c0 + e) sv[e] = -INFINITY;
-                }
-#pragma unroll
-                for (int e2 = 0; e2 < 16; ++e2) {
-                    float pv[2], dsv[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int e = 2 * e2 + u;
-                        const int ql = c0 + e;
-                        const float v = fast_exp2(fmaf(sv[e], sl2, -Lb[ql]));
-                        pv[u] = v;
-                        dsv[u] = v * (dp[e] - Lb[128 + ql]);
-                    }
-                    pk[cc * 16 + e2] = pack_bf16(pv[0], pv[1]);
-                    dp[2 * e2] = dsv[0];
-                    dp[2 * e2 + 1] = dsv[1];
-                }
-#pragma unroll
-                for (int e8 = 0; e8 < 4; ++e8) {
-                    const int col = c0 + e8 * 8;
-                    *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
-                        make_uint4(pack_bf16(dp[e8 * 8], dp[e8 * 8 + 1]), pack_bf16(dp[e8 * 8 + 2], dp[e8 * 8 + 3]),
-                                   pack_bf16(dp[e8 * 8 + 4], dp[e8 * 8 + 5]), pack_bf16(dp[e8 * 8 + 6], dp[e8 * 8 + 7]));
-                }
-            }
-            tmem_st32u(tmem + lane_base + (hf ? 96 : 0), pk);
-            tmem_st_wait();
-            fence_async_smem();
-            tc_fence_before();
-            __syncwarp();
-            if (threadIdx.x == 64) ATRACE(i, 4);
-            if (lane_id() == 0) mbar_arrive(ds_full);
-            // dQ tile (thread = query row r, column half hf): TMEM -> fp32 smem staged in this tile's
-            // consumed Q / dO buffers (4 swizzled [128][32] chunks) -> TMA bulk reduce-add into dq_acc
-            mbar_wait(dq_full, i & 1);  // every MMA of this tile retired: Q / dO no longer read
-            tc_fence_after();
-            if (threadIdx.x == 64) ATRACE(i, 5);
-            uint8_t* stage_q = sm + Bwd3Smem::q + (i & 1) * kTile;
-            uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
-#pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
-                const int c = hf * 2 + cc;
-                float v[32];
-                tmem_ld32(tmem + lane_base + c * 32, v);
-                tmem_ld_wait();
-                uint8_t* chunk = (c < 2 ? stage_q : stage_d) + (c & 1) * 16384 + r * 128;
-#pragma unroll
-                for (int g = 0; g < 8; ++g)
-                    *reinterpret_cast<float4*>(chunk + ((g ^ (r & 7)) << 4)) =
-                        make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (threadIdx.x == 64) ATRACE(i, 6);
-            if (lane_id() == 0) mbar_arrive(s_free);  // TMEM [0,256) free for the next S^T / dP^T
-            fence_async_smem();  // staging writes visible to the TMA reduce
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(dq_staged);
-        }
-        // dV, dK rows (thread = key row, column half hf)
-        mbar_wait(dkv_full, 0);
-        tc_fence_after();
-        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c = hf * 2 + cc;
-            float v[32], k[32];
-            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
-            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
-            tmem_ld_wait();
-            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
-            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                dv[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
-                                   pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
-                dk[e] = make_uint4(pack_bf16(k[8 * e] * scale, k[8 * e + 1] * scale),
-                                   pack_bf16(k[8 * e + 2] * scale, k[8 * e + 3] * scale),
-                                   pack_bf16(k[8 * e + 4] * scale, k[8 * e + 5] * scale),
-                                   pack_bf16(k[8 * e + 6] * scale, k[8 * e + 7] * scale));
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_free<512>(tmem);
-    }
-}
-
-// ------------------------------------------------------------------ backward v4
-// Same decomposition and TMEM map as v3, re-ordered so that the dQ drain, its reduce and the
+// ------------------------------------------------------------------ backward kernel
+// MMA order chosen so that the dQ drain, its reduce and the
 // lse / D loads leave the tensor pipe's critical path:
 //   * dQ(i) = dS K goes into the consumed dP^T columns [128,256) and is issued FIRST after dS^T
 //     lands; the compute warps read it out (registers), release the columns, then stage it (fp32)
@@ -911,15 +415,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // Measured dead ends: staging dQ in both Q(i) and dO(i) (as v3) stalls S^T(i+1) on the Q reload
 // behind the reduce; splitting the elementwise phase to run P^T under the MMAs, and draining dQ
 // with red.global.add from registers (L2 atomics issue-bound, ~2.7k cycles per tile), were slower.
-__global__ void __launch_bounds__(kBwd4Threads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc4_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                         const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
                         const float* __restrict__ dsum,
-                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale) {
+                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale,
+                        const float* __restrict__ rs, float rs_inv_n, float rs_eps) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
-    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (Bwd3Smem::total)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd3Smem::bars);
+    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (BwdSmem::total)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::bars);
     uint64_t* kv_full = bars + 0;
     uint64_t* q_full = bars + 1;     // [2]
     uint64_t* do_full = bars + 3;    // [2]
@@ -935,7 +440,7 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
     uint64_t* dq_staged = bars + 16;  // 8 compute warps: dQ(i) staged (fp32) in dO(i) / dS^T buffers
     uint64_t* ds_buf = bars + 17;     // reducer: the dS^T-buffer half of the staging read out
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
-    float* sL = reinterpret_cast<float*>(sm + Bwd3Smem::lse);
+    float* sL = reinterpret_cast<float*>(sm + BwdSmem::lse);
 
     const uint32_t warp = warp_id();
     const int nqb = seq / BQ;
@@ -967,8 +472,8 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             for (int i = 0; i < nq; ++i) {
                 mbar_wait(dq_staged, i & 1);
                 const int row = tok0 + (kb + i) * BQ;
-                uint8_t* stage_d = sm + Bwd3Smem::dO + (i & 1) * kTile;
-                uint8_t* stage_s = sm + Bwd3Smem::dst;
+                uint8_t* stage_d = sm + BwdSmem::dO + (i & 1) * kTile;
+                uint8_t* stage_s = sm + BwdSmem::dst;
 #pragma unroll
                 for (int c = 3; c >= 0; --c) {
                     asm volatile(
@@ -990,7 +495,7 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             for (int i = 0; i < nq; ++i) {
                 const int st = i & 1;
                 if (i >= 2) mbar_wait(&do_empty[st], ((i - 2) >> 1) & 1);
-                uint8_t* ds = sm + Bwd3Smem::dO + st * kTile;
+                uint8_t* ds = sm + BwdSmem::dO + st * kTile;
                 const int qr = tok0 + (kb + i) * BQ;
                 mbar_expect_tx(&do_full[st], kTile);
                 tma_load_2d(ds, &tm_do, &do_full[st], head * D, qr);
@@ -1003,14 +508,14 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             const int ck = H * D + head * D, cv = 2 * H * D + head * D;
             const int kr = tok0 + kb * BK;
             mbar_expect_tx(kv_full, 2 * kTile);
-            tma_load_2d(sm + Bwd3Smem::k, &tm_qkv, kv_full, ck, kr);
-            tma_load_2d(sm + Bwd3Smem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
-            tma_load_2d(sm + Bwd3Smem::v, &tm_qkv, kv_full, cv, kr);
-            tma_load_2d(sm + Bwd3Smem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
+            tma_load_2d(sm + BwdSmem::k, &tm_qkv, kv_full, ck, kr);
+            tma_load_2d(sm + BwdSmem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
+            tma_load_2d(sm + BwdSmem::v, &tm_qkv, kv_full, cv, kr);
+            tma_load_2d(sm + BwdSmem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
             for (int i = 0; i < nq; ++i) {
                 const int st = i & 1;
                 if (i >= 2) mbar_wait(&q_empty[st], ((i - 2) >> 1) & 1);
-                uint8_t* qs = sm + Bwd3Smem::q + st * kTile;
+                uint8_t* qs = sm + BwdSmem::q + st * kTile;
                 const int qr = tok0 + (kb + i) * BQ;
                 mbar_expect_tx(&q_full[st], kTile);
                 tma_load_2d(qs, &tm_qkv, &q_full[st], cq, qr);
@@ -1021,10 +526,10 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
         constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
         constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
         constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
-        const uint32_t sk = smem_u32(sm + Bwd3Smem::k), sv = smem_u32(sm + Bwd3Smem::v);
-        const uint32_t sdst = smem_u32(sm + Bwd3Smem::dst);
+        const uint32_t sk = smem_u32(sm + BwdSmem::k), sv = smem_u32(sm + BwdSmem::v);
+        const uint32_t sdst = smem_u32(sm + BwdSmem::dst);
         auto issue_s = [&](int i) {  // S^T(i) = K Q(i)^T -> [0,128)
-            const uint32_t sq = smem_u32(sm + Bwd3Smem::q + (i & 1) * kTile);
+            const uint32_t sq = smem_u32(sm + BwdSmem::q + (i & 1) * kTile);
             mbar_wait(&q_full[i & 1], (i >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
@@ -1038,7 +543,7 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             __syncwarp();
         };
         auto issue_dp = [&](int i) {  // dP^T(i) = V dO(i)^T -> [128,256)
-            const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + (i & 1) * kTile);
+            const uint32_t sdo = smem_u32(sm + BwdSmem::dO + (i & 1) * kTile);
             mbar_wait(&do_full[i & 1], (i >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
@@ -1056,8 +561,8 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
         issue_dp(0);
         for (int i = 0; i < nq; ++i) {
             const int st = i & 1;
-            const uint32_t sq = smem_u32(sm + Bwd3Smem::q + st * kTile);
-            const uint32_t sdo = smem_u32(sm + Bwd3Smem::dO + st * kTile);
+            const uint32_t sq = smem_u32(sm + BwdSmem::q + st * kTile);
+            const uint32_t sdo = smem_u32(sm + BwdSmem::dO + st * kTile);
             mbar_wait(ds_full, i & 1);
             tc_fence_after();
             if (lane_id() == 0) ATRACE(i, 8);
@@ -1101,7 +606,7 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
         const int r = int(q4 * 32 + lane_id());
         const uint32_t lane_base = (q4 * 32) << 16;
         const float sl2 = scale * kLog2e;
-        uint8_t* sdst = sm + Bwd3Smem::dst;
+        uint8_t* sdst = sm + BwdSmem::dst;
         const int key = kb * BK + r;
         auto lse_of = [&](int qb) {  // this thread's staged value: lse2 (half 0) or D (half 1) of query row r
             return hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r] : dsum[size_t(head) * T + tok0 + qb * BQ + r];
@@ -1178,7 +683,7 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
                 if (lane_id() == 0) mbar_arrive(dq_free);  // [128,256) free for dP^T(i+1)
                 if (threadIdx.x == 64) ATRACE(i, 5);
                 mbar_wait(qdo_used, i & 1);               // dK(i) retired: dO(i) / dS^T may be overwritten
-                uint8_t* stage = hf == 0 ? sm + Bwd3Smem::dO + (i & 1) * kTile : sm + Bwd3Smem::dst;
+                uint8_t* stage = hf == 0 ? sm + BwdSmem::dO + (i & 1) * kTile : sm + BwdSmem::dst;
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
                     uint8_t* chunk = stage + cc * 16384 + r * 128;
@@ -1202,6 +707,9 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
         mbar_wait(dkv_full, 0);
         tc_fence_after();
         const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
+        // folded RMSNorm of the QKV input: dqkv' = rstd1(row) * dqkv (executor.cpp, fold mode)
+        const float fv = rs ? rsqrtf(rs[tok0 + kb * BK + r] * rs_inv_n + rs_eps) : 1.f;
+        const float fk = fv * scale;
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {
             const int c = hf * 2 + cc;
@@ -1213,12 +721,12 @@ __global__ void __launch_bounds__(kBwd4Threads, 1)
             uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                dv[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
-                                   pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
-                dk[e] = make_uint4(pack_bf16(k[8 * e] * scale, k[8 * e + 1] * scale),
-                                   pack_bf16(k[8 * e + 2] * scale, k[8 * e + 3] * scale),
-                                   pack_bf16(k[8 * e + 4] * scale, k[8 * e + 5] * scale),
-                                   pack_bf16(k[8 * e + 6] * scale, k[8 * e + 7] * scale));
+                dv[e] = make_uint4(pack_bf16(v[8 * e] * fv, v[8 * e + 1] * fv), pack_bf16(v[8 * e + 2] * fv, v[8 * e + 3] * fv),
+                                   pack_bf16(v[8 * e + 4] * fv, v[8 * e + 5] * fv), pack_bf16(v[8 * e + 6] * fv, v[8 * e + 7] * fv));
+                dk[e] = make_uint4(pack_bf16(k[8 * e] * fk, k[8 * e + 1] * fk),
+                                   pack_bf16(k[8 * e + 2] * fk, k[8 * e + 3] * fk),
+                                   pack_bf16(k[8 * e + 4] * fk, k[8 * e + 5] * fk),
+                                   pack_bf16(k[8 * e + 6] * fk, k[8 * e + 7] * fk));
             }
         }
     }
@@ -1439,251 +947,49 @@ __global__ void __launch_bounds__(192, 2)
 }
 
 
-// ------------------------------------------------------------------ forward v2 (two Q tiles per CTA)
-// One CTA per (256 queries = tiles A and B, head, sequence); 320 threads:
-//   warp 0     TMA: Q_A, Q_B once, then a 2-stage ring of K/V tiles shared by both Q tiles
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer, ping-ponging the two tiles:
-//                S_A(j) S_B(j) | PV_A(j) S_A(j+1) | PV_B(j) S_B(j+1) | ...
-//   warps 2-5  softmax of tile A, warps 6-9 softmax of tile B (thread = query row = TMEM lane)
-// TMEM: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).  P (bf16) is written back over
-// the consumed S columns and read by the PV MMA as its A operand straight from TMEM, so smem only
-// holds Q_A, Q_B and the K/V ring.  While one tile's softmax runs, the tensor pipe works on the
-// other tile.  The MMA pipe executes in issue order, so when S_X(j) is complete PV_X(j-1) is too:
-// the lazy O rescale needs no extra wait.
-struct Fwd2Smem {
-    static constexpr int qa = 0;
-    static constexpr int qb = kTile;
-    static constexpr int k0 = 2 * kTile;             // [2]
-    static constexpr int v0 = k0 + kStages * kTile;  // [2]
-    static constexpr int bars = v0 + kStages * kTile;
-    static constexpr int total = bars + 256 + 1024;
-};
+}  // namespace
 
-__global__ void __launch_bounds__(320, 1)
-    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
-                        float* __restrict__ lse2, int seq, int H, int T, float scale) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Fwd2Smem::bars);
-    uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2] per tile
-    uint64_t* p_full = bars + 7;    // [2] per tile (4 softmax warps)
-    uint64_t* o_full = bars + 9;    // [2] per tile
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
-
-    const uint32_t warp = warp_id();
-    const int npair = seq / (2 * BQ);
-    const int hb = int(blockIdx.x) % (H * (T / seq));
-    const int c = npair - 1 - int(blockIdx.x) / (H * (T / seq));  // heaviest pair of tiles first (LPT)
-    const int head = hb % H, b = hb / H;
-    const int row0 = b * seq + c * 2 * BQ;  // first query row of tile A
-    const int nA = 2 * c + 1, nB = 2 * c + 2;  // causal key tiles of A and B
-
-    if (warp == 0 && elect_one()) {
-        tma_prefetch(&tm);
-        mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 4);
-            mbar_init(&o_full[i], 1);
-        }
-        fence_barrier_init();
+// Phase-stamp buffer of block 0 (PB_ATTN_TRACE / PB_ATTN_TRACE_FWD with a -DPB_ATTN_TRACE_BUILD library)
+static unsigned long long* trace_buffer(const char* env) {
+    unsigned long long* t = nullptr;
+    if (std::getenv(env)) {
+        cudaMalloc(&t, 32 * 16 * 8);
+        cudaMemset(t, 0, 32 * 16 * 8);
+        cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    pdl_wait();
-    pdl_launch();
-
-    if (warp == 0) {
-        if (elect_one()) {
-            const int cq = head * D, ck = H * D + head * D, cv = 2 * H * D + head * D;
-            mbar_expect_tx(q_full, 2 * kTile);
-            tma_load_2d(sm + Fwd2Smem::qa, &tm, q_full, cq, row0);
-            tma_load_2d(sm + Fwd2Smem::qa + 16384, &tm, q_full, cq + 64, row0);
-            tma_load_2d(sm + Fwd2Smem::qb, &tm, q_full, cq, row0 + BQ);
-            tma_load_2d(sm + Fwd2Smem::qb + 16384, &tm, q_full, cq + 64, row0 + BQ);
-            for (int j = 0; j < nB; ++j) {
-                const int st = j & 1;
-                if (j >= kStages) mbar_wait(&kv_empty[st], ((j - kStages) >> 1) & 1);
-                mbar_expect_tx(&kv_full[st], 2 * kTile);
-                const int kr = b * seq + j * BK;
-                uint8_t* ks = sm + Fwd2Smem::k0 + st * kTile;
-                uint8_t* vs = sm + Fwd2Smem::v0 + st * kTile;
-                tma_load_2d(ks, &tm, &kv_full[st], ck, kr);
-                tma_load_2d(ks + 16384, &tm, &kv_full[st], ck + 64, kr);
-                tma_load_2d(vs, &tm, &kv_full[st], cv, kr);
-                tma_load_2d(vs + 16384, &tm, &kv_full[st], cv + 64, kr);
-            }
-        }
-    } else if (warp == 1) {
-        constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
-        constexpr uint32_t idesc_o = idesc_bf16(128, 128, false, true);
-        mbar_wait(q_full, 0);
-        auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T -> TMEM [t*128, +128)
-            mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t sq = smem_u32(sm + (t ? Fwd2Smem::qb : Fwd2Smem::qa));
-                const uint32_t sk = smem_u32(sm + Fwd2Smem::k0 + (j & 1) * kTile);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + t * 128, sdesc(sq + o, 16, 1024), sdesc(sk + o, 16, 1024), idesc_s, kk != 0);
-                }
-                tc_commit(&s_full[t]);
-            }
-            __syncwarp();
-        };
-        auto issue_pv = [&](int t, int j, bool release_kv) {  // O_t += P_t(j) V_j, P from TMEM
-            mbar_wait(&p_full[t], j & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t sv = smem_u32(sm + Fwd2Smem::v0 + (j & 1) * kTile);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc(sv + kk * 2048, 16384, 1024),
-                              idesc_o, (j | kk) != 0);
-                if (release_kv) tc_commit(&kv_empty[j & 1]);
-            }
-            __syncwarp();
-        };
-        issue_s(0, 0);
-        issue_s(1, 0);
-        for (int j = 0; j < nB; ++j) {
-            if (j < nA) {
-                issue_pv(0, j, false);
-                if (j + 1 < nA) issue_s(0, j + 1);
-            }
-            issue_pv(1, j, true);  // tile B reads every K/V tile last
-            if (j + 1 < nB) issue_s(1, j + 1);
-        }
-        if (elect_one()) {
-            tc_commit(&o_full[0]);
-            tc_commit(&o_full[1]);
-        }
-        __syncwarp();
-    } else {
-        // ------------------------------------------------------------ softmax (tile t)
-        const int t = int(warp - 2) >> 2;
-        const uint32_t q4 = warp & 3;
-        const int r = int(q4 * 32 + lane_id());
-        const uint32_t lane_base = (q4 * 32) << 16;
-        const uint32_t ts = tmem + lane_base + t * 128;      // S_t / P_t
-        const uint32_t to = tmem + lane_base + 256 + t * 128;  // O_t
-        const int nkv = t ? nB : nA;
-        const float sl2 = scale * kLog2e;
-        float m_used = -INFINITY, l = 0.f;
-        for (int j = 0; j < nkv; ++j) {
-            mbar_wait(&s_full[t], j & 1);  // S_t(j) done, and with it PV_t(j-1): O_t stable
-            tc_fence_after();
-            // two passes over S_t (TMEM reads are cheap, registers are not: 10 warps leave 168 per
-            // thread): row max over all 128 columns, then exp / pack per 64-column half
-            float mx8[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
-            const bool diag = (j == nkv - 1);
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                float v[32];
-                tmem_ld32(ts + cc * 32, v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const float x = (diag && cc * 32 + e > r) ? -INFINITY : v[e];
-                    mx8[e & 7] = fmaxf(mx8[e & 7], x);
-                }
-            }
-            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
-            const float m_new = fmaxf(m_used, mx);
-            const bool rescale = (j > 0) && (m_new > m_used + 8.f);
-            if (__any_sync(0xffffffff, rescale)) {
-                const float f = rescale ? exp2f(m_used - m_new) : 1.f;
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    float o[32];
-                    tmem_ld32(to + cc * 32, o);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st32(to + cc * 32, o);
-                }
-                if (rescale) {
-                    l *= f;
-                    m_used = m_new;
-                }
-            }
-            if (j == 0) m_used = m_new;
-            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                float sv[64];
-                tmem_ld32(ts + h2 * 64, *reinterpret_cast<float(*)[32]>(&sv[0]));
-                tmem_ld32(ts + h2 * 64 + 32, *reinterpret_cast<float(*)[32]>(&sv[32]));
-                tmem_ld_wait();
-                uint32_t pk[32];
-#pragma unroll
-                for (int e2 = 0; e2 < 32; ++e2) {
-                    const int c0 = h2 * 64 + 2 * e2;
-                    const float x0 = (diag && c0 > r) ? -INFINITY : sv[2 * e2];
-                    const float x1 = (diag && c0 + 1 > r) ? -INFINITY : sv[2 * e2 + 1];
-                    const float p0 = fast_exp2(fmaf(x0, sl2, -m_used));
-                    const float p1 = fast_exp2(fmaf(x1, sl2, -m_used));
-                    rs8[(2 * e2) & 7] += p0;
-                    rs8[(2 * e2 + 1) & 7] += p1;
-                    pk[e2] = pack_bf16(p0, p1);
-                }
-                // P_t bf16 pairs over S_t columns [h2*32, +32): S columns already consumed
-                tmem_st32u(ts + h2 * 32, pk);
-            }
-            l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(&p_full[t]);
-        }
-        mbar_wait(&o_full[t], 0);
-        tc_fence_after();
-        const float inv = 1.f / l;
-        const int qrow = row0 + t * BQ + r;
-        __nv_bfloat16* orow = out + size_t(qrow) * (H * D) + head * D;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            float o[32];
-            tmem_ld32(to + cc * 32, o);
-            tmem_ld_wait();
-            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
-                                    pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
-        }
-        lse2[size_t(head) * T + qrow] = m_used + log2f(l);
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_free<512>(tmem);
+    return t;
+}
+static void trace_dump(unsigned long long* t, const char* what, cudaStream_t s) {
+    if (!t) return;
+    unsigned long long h[32 * 16];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
+        std::fprintf(stderr, "%s trace it %2d: t0=%lld", what, i, (long long)(h[i * 16] - h[0]));
+        for (int e = 1; e < 16; ++e)
+            if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
+        std::fprintf(stderr, "\n");
     }
 }
 
-}  // namespace
+void attn_bwd_pre(const __nv_bfloat16* dout, const __nv_bfloat16* out, float* dsum, float* dq_acc, int heads, int T,
+                  cudaStream_t s) {
+    launch_k(attn_bwd_pre_kernel, dim3(T), dim3(256), 0, s, 1, dout, out, dsum, dq_acc, heads, T);
+}
+
+void attn_dq_store(const float* dq_acc, __nv_bfloat16* dqkv, int heads, int T, cudaStream_t s, const float* rs,
+                   float rs_inv_n, float rs_eps) {
+    launch_k(attn_dq_store_kernel, dim3(T), dim3(256), 0, s, 1, dq_acc, dqkv, heads, 0.08838834764831845f, rs,
+             rs_inv_n, rs_eps);
+}
 
 void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse2,
-                 float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s) {
+                 float* dsum, float* dq_acc, __nv_bfloat16* dqkv, int batch, int seq, int heads, cudaStream_t s,
+                 const float* rs, float rs_inv_n, float rs_eps) {
     if (seq % 128) throw std::invalid_argument("attention: seq must be a multiple of 128");
     attn_bwd_pre(dout, out, dsum, dq_acc, heads, batch * seq, s);
     static bool once = [] {
-        cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::total);
-        cudaFuncSetAttribute(attn_bwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd3Smem::total);
+        cudaFuncSetAttribute(attn_bwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::total);
         return true;
     }();
     (void)once;
@@ -1692,130 +998,42 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     const CUtensorMap td = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 128);
     const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
                                        uint64_t(heads) * D, 32, 128);
-    dim3 grid(seq / BK * heads * batch);
-    // PB_ATTN_BWD=2 / =3: the earlier kernels (v2: smem P^T; v3: serial elementwise phase)
-    static const int ver = [] {
-        const char* e = std::getenv("PB_ATTN_BWD");
-        return e && (e[0] == '2' || e[0] == '3') ? e[0] - '0' : 4;
-    }();
-    if (ver == 4) {
-        static bool attr4 = [] {
-            cudaFuncSetAttribute(attn_bwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd3Smem::total);
-            return true;
-        }();
-        (void)attr4;
-        static unsigned long long* trace4 = [] {
-            unsigned long long* t = nullptr;
-            if (std::getenv("PB_ATTN_TRACE")) {
-                cudaMalloc(&t, 32 * 16 * 8);
-                cudaMemset(t, 0, 32 * 16 * 8);
-                cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
-            }
-            return t;
-        }();
-        launch_k(attn_bwd_tc4_kernel, grid, dim3(kBwd4Threads), Bwd3Smem::total, s, 1, tq, td, tdq, lse2,
-                 static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
-        if (trace4) {
-            unsigned long long h[32 * 16];
-            cudaStreamSynchronize(s);
-            cudaMemcpy(h, trace4, sizeof(h), cudaMemcpyDeviceToHost);
-            for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
-                std::fprintf(stderr, "attn_bwd4 trace it %2d: t0=%lld", i, (long long)(h[i * 16] - h[0]));
-                for (int e = 1; e < 16; ++e)
-                    if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
-                std::fprintf(stderr, "\n");
-            }
-        }
-    } else if (ver == 2)
-        launch_k(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq, lse2,
-                 static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
-    else {
-        static unsigned long long* trace = [] {
-            unsigned long long* t = nullptr;
-            if (std::getenv("PB_ATTN_TRACE")) {
-                cudaMalloc(&t, 32 * 16 * 8);
-                cudaMemset(t, 0, 32 * 16 * 8);
-                cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
-            }
-            return t;
-        }();
-        launch_k(attn_bwd_tc3_kernel, grid, dim3(kBwdThreads), Bwd3Smem::total, s, 1, tq, td, tdq, lse2,
-                 static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f);
-        if (trace) {
-            unsigned long long h[32 * 16];
-            cudaStreamSynchronize(s);
-            cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
-            for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
-                std::fprintf(stderr, "attn_bwd trace it %2d: t0=%lld", i, (long long)(h[i * 16] - h[0]));
-                for (int e = 1; e < 16; ++e)
-                    if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
-                std::fprintf(stderr, "\n");
-            }
-        }
-    }
-    attn_dq_store(dq_acc, dqkv, heads, T, s);
+    static unsigned long long* trace = trace_buffer("PB_ATTN_TRACE");
+    launch_k(attn_bwd_tc4_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq,
+             lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs, rs_inv_n, rs_eps);
+    trace_dump(trace, "attn_bwd", s);
+    attn_dq_store(dq_acc, dqkv, heads, T, s, rs, rs_inv_n, rs_eps);
 }
 
+// Two forward kernels, same contract: the single-CTA-per-SM kernel with double-buffered S / P
+// (attn_fwd_tc_kernel, lowest per-tile latency: small grids) and the two-CTAs-per-SM kernel
+// (attn_fwd_tc3_kernel: one CTA's MMAs run under the other's softmax) for grids of >= ~3 CTAs per
+// SM.  PB_ATTN_FWD=1 / 3 forces one.
 void attn_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse2, int batch, int seq, int heads,
                  cudaStream_t s) {
     if (seq % 128) throw std::invalid_argument("attention: seq must be a multiple of 128");
     static bool once = [] {
         cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::total);
-        cudaFuncSetAttribute(attn_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::total);
+        cudaFuncSetAttribute(attn_fwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Smem::total);
         return true;
     }();
     (void)once;
     const int T = batch * seq;
     const CUtensorMap tm = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
-    // PB_ATTN_FWD=2: the two-Q-tile ping-pong kernel (P in TMEM).  Correct (tested) but measured
-    // slower than the single-tile kernel (467 vs 556 TFLOP/s at 2 x 2048 x 16 heads): its
-    // softmax -> PV -> S chain per tile is longer than the double-buffered S/P overlap of v1.
-    // default: the two-CTA-per-SM kernel (v3) when the grid is at least ~3 CTAs per SM — it trades
-    // per-CTA latency for throughput, so a single short wave (e.g. 256 CTAs) stays on v1.
-    // PB_ATTN_FWD=1 / 2 / 3 forces a kernel.
     static const int fenv = [] {
         const char* e = std::getenv("PB_ATTN_FWD");
-        return e && (e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
+        return e && (e[0] == '1' || e[0] == '3') ? e[0] - '0' : 0;
     }();
     const int nblk = seq / BQ * heads * batch;
     const int fver = fenv ? fenv : (nblk >= 3 * num_sms() ? 3 : 1);
-    const bool v2 = fver == 2;
     if (fver == 3) {
-        static bool attr3 = [] {
-            cudaFuncSetAttribute(attn_fwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Smem::total);
-            return true;
-        }();
-        (void)attr3;
-        launch_k(attn_fwd_tc3_kernel, dim3(seq / BQ * heads * batch), dim3(192), Fwd3Smem::total, s, 1, tm, out, lse2,
-                 seq, heads, T, 0.08838834764831845f);
-    } else if (!v2 || seq % (2 * BQ)) {
-        dim3 grid(seq / BQ * heads * batch);
-        static unsigned long long* trace = [] {
-            unsigned long long* t = nullptr;
-            if (std::getenv("PB_ATTN_TRACE_FWD")) {
-                cudaMalloc(&t, 32 * 16 * 8);
-                cudaMemset(t, 0, 32 * 16 * 8);
-                cudaMemcpyToSymbol(g_attn_trace, &t, sizeof(t));
-            }
-            return t;
-        }();
-        launch_k(attn_fwd_tc_kernel, grid, dim3(192), FwdSmem::total, s, 1, tm, out, lse2, seq, heads, T,
+        launch_k(attn_fwd_tc3_kernel, dim3(nblk), dim3(192), Fwd3Smem::total, s, 1, tm, out, lse2, seq, heads, T,
                  0.08838834764831845f);
-        if (trace) {
-            unsigned long long h[32 * 16];
-            cudaStreamSynchronize(s);
-            cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
-            for (int i = 0; i < 32 && h[i * 16 + 0]; ++i) {
-                std::fprintf(stderr, "attn_fwd trace it %2d: t0=%lld", i, (long long)(h[i * 16] - h[0]));
-                for (int e = 1; e < 16; ++e)
-                    if (h[i * 16 + e]) std::fprintf(stderr, " e%d=%lld", e, (long long)(h[i * 16 + e] - h[i * 16 + 0]));
-                std::fprintf(stderr, "\n");
-            }
-        }
     } else {
-        dim3 grid(seq / (2 * BQ) * heads * batch);
-        launch_k(attn_fwd_tc2_kernel, grid, dim3(320), Fwd2Smem::total, s, 1, tm, out, lse2, seq, heads, T,
+        static unsigned long long* trace = trace_buffer("PB_ATTN_TRACE_FWD");
+        launch_k(attn_fwd_tc_kernel, dim3(nblk), dim3(192), FwdSmem::total, s, 1, tm, out, lse2, seq, heads, T,
                  0.08838834764831845f);
+        trace_dump(trace, "attn_fwd", s);
     }
 }
 

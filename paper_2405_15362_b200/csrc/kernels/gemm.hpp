@@ -30,13 +30,14 @@ struct GemmArgs {
     int ldaux = 0;
     int epi = EPI_STORE;
     int accumulate = 0;
+    // folded RMSNorm (STORE / GELU / DGELU): acc(row, :) *= rsqrt(rs[row] * rs_inv_n + rs_eps)
+    const float* rs = nullptr;
+    float rs_inv_n = 0.f, rs_eps = 0.f;
+    // RESID: ss_out[row] += sum of squares of the row's stored (bf16) outputs (atomic, per tile)
+    float* ss_out = nullptr;
 };
 
 void gemm(const GemmArgs& g, cudaStream_t s);
-// Stream-K split tiles for ragged last waves (PB_STREAMK=1 enables; off by default).  Per host
-// thread: off while other streams may run GEMMs concurrently on the same GPU (see gemm_tc.cu).
-void gemm_allow_stream_k(bool on);
-void gemm_force_stream_k(int on);  // tests: -1 environment, 0 off, 1 on
 
 // Grouped weight-gradient GEMMs: independent dW (+)= dY^T X problems (A and B MN-major,
 // fp32 epilogue) run as ONE persistent CTA-pair launch over their concatenated tiles,
@@ -57,8 +58,6 @@ int num_sms();
 // tests: force the 1-CTA (1) or CTA-pair (2) variant where shapes allow; -1 = automatic
 void gemm_force_cta_group(int cg);
 void gemm_force_bm2(int on);  // tests: 512 x 256 CTA-pair tiles, -1 = PB_GEMM_BM2
-void gemm_force_bn(int bn);  // tests: F-pass pair tile width, 0 = per-shape choice (gemm_f_bn)
-int gemm_f_bn(int M, int N);
 // 2-D bf16 tensor map [outer][inner], row stride ld elements, box_inner x box_outer, 128B swizzle
 CUtensorMap make_map_t(const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t inner, uint64_t outer,
                        uint64_t ld, uint32_t box_inner, uint32_t box_outer);

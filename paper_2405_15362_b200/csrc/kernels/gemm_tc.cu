@@ -18,6 +18,7 @@
 
 #include <cstdlib>
 #include <map>
+#include <unordered_map>
 #include <mutex>
 #include <vector>
 #include <stdexcept>
@@ -69,14 +70,12 @@ struct KParams {
     int accumulate;
     const GroupProblem* group;  // grouped launch: tiles come from this table
     int ngroup, total_tiles;
-    // stream-K (non-grouped launches): pair c owns k-block units [c*U/P, (c+1)*U/P) of the
-    // tile-major (tile, k-block) space; partial tiles meet in `sk_ws` (one 128 x BN fp32
-    // slot per CTA, written by the pair's first segment) under per-CTA epoch flags
-    float* sk_ws;
-    uint32_t* sk_flag;
-    uint32_t sk_epoch;
-    int sk;
-    int sk_dp;  // hybrid: tiles [0, sk_dp) are whole (one per pair, the full waves); stream-K covers the rest
+    // row scale (RMSNorm folded into the consuming GEMM): acc(row, :) *= rsqrt(rs[row] * rs_inv_n + rs_eps),
+    // rs = the row's sum of squares over the normalised width
+    const float* rs;
+    float rs_inv_n, rs_eps;
+    // EPI_RESID: ss_out[row] += sum over this tile's columns of bf16(out)^2 (the next RMSNorm's statistic)
+    float* ss_out;
 };
 
 // Resolves tile t of the launch: its problem's descriptors, origin, K blocks, output.
@@ -99,40 +98,14 @@ __device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensor
     return TileRef{&g.ta, &g.tb, g.C, lt % g.num_m, lt / g.num_m, g.K / BK, g.ldc};
 }
 
-// Work of one CTA (pair) as segments (tile, k-blocks [kb0, kb1)): whole tiles
-// round-robin, or a contiguous stream-K range of (tile, k-block) units.
-struct SegIter {
-    long long u, u1;  // stream-K
-    int nk;
-    int t, step, num_tiles, dp;  // whole tiles
-    bool sk;
-    __device__ SegIter(const KParams& p, int num_tiles_, int cid, int ncl) {
-        sk = p.sk != 0;
-        num_tiles = num_tiles_;
-        t = cid;
-        step = ncl;
-        nk = p.K / BK;
-        dp = sk ? p.sk_dp : 0;
-        const long long U = (long long)(num_tiles - dp) * nk;
-        u = U * cid / ncl;
-        u1 = U * (cid + 1) / ncl;
-    }
-    __device__ bool next(int& tile, int& kb0, int& kb1) {
-        if (!sk || t < dp) {
-            if (t >= (sk ? dp : num_tiles)) return false;
-            tile = t;
-            kb0 = 0;
-            kb1 = -1;  // whole tile (resolved per problem)
-            t += step;
-            return true;
-        }
-        if (u >= u1) return false;
-        tile = dp + int(u / nk);
-        const long long ts = (long long)(tile - dp) * nk;  // first unit of this tile
-        const long long end = u1 < ts + nk ? u1 : ts + nk;
-        kb0 = int(u - ts);
-        kb1 = int(end - ts);
-        u = end;
+// Whole tiles round-robin over the persistent CTAs (pairs).
+struct TileIter {
+    int t, step, num_tiles;
+    __device__ TileIter(int num_tiles_, int cid, int ncl) : t(cid), step(ncl), num_tiles(num_tiles_) {}
+    __device__ bool next(int& tile) {
+        if (t >= num_tiles) return false;
+        tile = t;
+        t += step;
         return true;
     }
 };
@@ -190,15 +163,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int cursor = 0;
-            SegIter it(p, num_tiles, cid, ncl);
-            int t, kb0, kb1;
-            while (it.next(t, kb0, kb1)) {
+            TileIter it(num_tiles, cid, ncl);
+            int t;
+            while (it.next(t)) {
                 const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor);
                 const CUtensorMap* pa = tr.ta;
                 const CUtensorMap* pb = tr.tb;
-                const int num_k = kb1 < 0 ? tr.num_k : kb1;
+                const int num_k = tr.num_k;
                 const int m0 = tr.m_blk * kPairRows * BM2 + int(rank) * BM, n0 = tr.n_blk * BN + int(rank) * C_::kBRows;
-                for (int kb = kb0; kb < num_k; ++kb) {
+                for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * C_::kStageBytes;
                     uint8_t* sb = sa + C_::kABytes;
@@ -257,14 +230,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             int cursor = 0;
-            SegIter it(p, num_tiles, cid, ncl);
-            int t, kb0, kb1;
-            while (it.next(t, kb0, kb1)) {
-                const int num_k = kb1 < 0 ? resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor).num_k : kb1;
+            TileIter it(num_tiles, cid, ncl);
+            int t;
+            while (it.next(t)) {
+                const int num_k = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor).num_k;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C_::kAccStride;  // (BM2 = 2: sub-tile s2 at + s2 * 256)
-                for (int kb = kb0; kb < num_k; ++kb) {
+                for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (elect_one()) {
@@ -273,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k) {
                             const uint64_t bd = B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
-                            const bool accum = kb != kb0 || k != 0;
+                            const bool accum = kb != 0 || k != 0;
 #pragma unroll
                             for (int s2 = 0; s2 < BM2; ++s2) {
                                 const uint32_t sa2 = sa + s2 * 16384;
@@ -305,12 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int cursor = 0;
-        SegIter it(p, num_tiles, cid, ncl);
-        int t, kb0, kb1;
-        const int nk = p.K / BK;
-        const int sk_dp = p.sk ? p.sk_dp : 0;
-        const long long U = (long long)(num_tiles - sk_dp) * nk;
-        while (it.next(t, kb0, kb1)) {
+        TileIter it(num_tiles, cid, ncl);
+        int t;
+        while (it.next(t)) {
             const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor);
             const int m0 = tr.m_blk * kPairRows * BM2 + int(rank) * BM, n0 = tr.n_blk * BN;
             void* const Cout = tr.C;
@@ -319,48 +289,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int row0 = m0 + row_in_tile;
             const uint32_t tbase0 = tmem_base + ((q * 32) << 16) + acc * C_::kAccStride;
-            if (kb1 >= 0 && kb0 > 0) {
-                // stream-K contributor (this pair's first segment): park the partial tile, publish
-                float* slot = p.sk_ws + (size_t(cid) * CG + rank) * (BM * BN) + size_t(row_in_tile) * BN;
-#pragma unroll 1
-                for (int c = 0; c < BN; c += 32) {
-                    float v[32];
-                    tmem_ld32(tbase0 + c, v);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        __stcg(reinterpret_cast<float4*>(slot + c) + j,
-                               make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane_id() == 0) {
-                    if constexpr (CG == 1)
-                        mbar_arrive(&tempty[acc]);
-                    else
-                        mbar_arrive_cluster(map_peer(smem_u32(&tempty[acc]), 0));
-                }
-                __threadfence();
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
-                if (warp == 2 && lane_id() == 0)
-                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flag + size_t(cid) * CG + rank),
-                                 "r"(p.sk_epoch)
-                                 : "memory");
-                if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
-                continue;
-            }
-            // stream-K owner of a split tile: pairs cid+1 .. whose ranges start inside this tile contributed
-            int c_last = cid;
-            if (kb1 >= 0 && kb1 < nk) {
-                while (c_last + 1 < ncl && U * (c_last + 1) / ncl < (long long)(t - sk_dp + 1) * nk) ++c_last;
-                for (int c = cid + 1; c <= c_last; ++c) {
-                    const uint32_t* f = p.sk_flag + size_t(c) * CG + rank;
-                    uint32_t e;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(f) : "memory");
-                    } while (e != p.sk_epoch);
-                }
-            }
             // residual / pre-activation operand of the next 32 columns is loaded one chunk ahead
             // (each element is read and written by the same thread, so C may alias aux)
             constexpr bool kAux = EPI == EPI_RESID || EPI == EPI_DGELU;
@@ -368,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int s2 = 0; s2 < BM2; ++s2) {  // BM2 = 2: the CTA's second 128-row sub-tile is 256 rows on
             const int row = row0 + s2 * kPairRows;
             const uint32_t tbase = tbase0 + s2 * 256;
+            const float rsc = (p.rs && row < p.M) ? rsqrtf(p.rs[row] * p.rs_inv_n + p.rs_eps) : 1.f;
+            float ssq = 0.f;  // EPI_RESID with ss_out: sum of squares of this row's stored outputs
             uint4 aux_next[4];
             // (aux epilogues run only on full tiles: layer GEMMs have M = tokens, N = h or 4h)
             if constexpr (kAux) {
@@ -390,14 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
                 tmem_ld32(tbase + c, v);
                 tmem_ld_wait();
-                for (int cc = cid + 1; cc <= c_last; ++cc) {
-                    const float4* src = reinterpret_cast<const float4*>(
-                        p.sk_ws + (size_t(cc) * CG + rank) * (BM * BN) + size_t(row_in_tile) * BN + c);
+                if (p.rs) {  // warp-uniform: folded RMSNorm of this row
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 a = __ldcg(src + j);
-                        v[4 * j] += a.x, v[4 * j + 1] += a.y, v[4 * j + 2] += a.z, v[4 * j + 3] += a.w;
-                    }
+                    for (int e = 0; e < 32; ++e) v[e] *= rsc;
                 }
                 const int col = n0 + c;
                 // partial last tile (M or N = 128 mod 256): nothing to store outside the matrix
@@ -438,9 +363,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + size_t(row) * p.ldc + col);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        d4[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
-                                           pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                    for (int j = 0; j < 4; ++j) {
+                        const uint4 o = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                                   pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                        d4[j] = o;
+                        if constexpr (EPI == EPI_RESID) {
+                            if (p.ss_out) {
+                                const uint32_t w4[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float lo = bf16_lo(w4[e]), hi = bf16_hi(w4[e]);
+                                    ssq = fmaf(lo, lo, fmaf(hi, hi, ssq));
+                                }
+                            }
+                        }
+                    }
                     if constexpr (EPI == EPI_GELU) {
                         // activation from the bf16-rounded pre-activation, as the backward sees it
                         uint4* g4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C2) + size_t(row) * p.ldc + col);
@@ -455,6 +392,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+            }
+            if constexpr (EPI == EPI_RESID) {
+                if (p.ss_out && row < p.M) atomicAdd(p.ss_out + row, ssq);
             }
             }  // s2
             tc_fence_before();
@@ -492,8 +432,35 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D tensor [outer][inner] with row stride `ld` elements; box = box_inner x box_outer; 128B swizzle.
+// Descriptors are pure functions of these arguments, so they are cached per host thread (the
+// executor re-issues the same few hundred GEMM / attention shapes on the same buffers every step:
+// one hash lookup instead of a driver encode per operand per launch).
+namespace {
+struct MapKey {
+    const void* base;
+    uint64_t inner, outer, ld;
+    uint32_t box_inner, box_outer, dt;
+    bool operator==(const MapKey& o) const {
+        return base == o.base && inner == o.inner && outer == o.outer && ld == o.ld && box_inner == o.box_inner &&
+               box_outer == o.box_outer && dt == o.dt;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        uint64_t h = reinterpret_cast<uint64_t>(k.base) * 0x9E3779B97F4A7C15ull;
+        for (uint64_t v : {k.inner, k.outer, k.ld, uint64_t(k.box_inner) << 32 | k.box_outer, uint64_t(k.dt)})
+            h = (h ^ v) * 0x100000001B3ull;
+        return size_t(h);
+    }
+};
+}  // namespace
+
 CUtensorMap make_map_t(const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t inner, uint64_t outer,
                        uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+    thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    const MapKey key{base, inner, outer, ld, box_inner, box_outer, uint32_t(dt) | (esize << 8)};
+    if (auto it = cache.find(key); it != cache.end()) return it->second;
+    if (cache.size() > 8192) cache.clear();
     CUtensorMap m;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {ld * esize};
@@ -503,6 +470,7 @@ CUtensorMap make_map_t(const void* base, CUtensorMapDataType dt, uint32_t esize,
                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    cache.emplace(key, m);
     return m;
 }
 
@@ -523,47 +491,6 @@ int sm_count() {
     return n;
 }
 
-// Stream-K scratch, one per (device, stream): GEMMs on one stream are ordered, so a
-// launch's partial tiles and epoch flags are never shared with a concurrent launch.
-struct SkWorkspace {
-    float* ws = nullptr;
-    uint32_t* flags = nullptr;
-    uint32_t epoch = 0;
-};
-SkWorkspace& sk_workspace(cudaStream_t s) {
-    // one 128 x 256 fp32 partial tile per CTA of a full-GPU launch (the largest BN)
-    const size_t floats = size_t(sm_count()) * BM * 256;
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, SkWorkspace> all;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
-    SkWorkspace& w = all[{dev, s}];
-    if (!w.ws) {
-        if (cudaMalloc(&w.ws, floats * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&w.flags, 1024 * sizeof(uint32_t)) != cudaSuccess ||
-            cudaMemset(w.flags, 0, 1024 * sizeof(uint32_t)) != cudaSuccess)
-            throw std::runtime_error("gemm: stream-K workspace allocation failed");
-    }
-    return w;
-}
-// Stream-K owners spin on their contributors, which is safe only while every CTA of the launch
-// can be resident: launches from OTHER streams on the same GPU could hold the SMs a contributor
-// needs while their own owners spin.  Callers that share a GPU across concurrently running
-// streams turn it off for their thread (gemm_allow_stream_k).
-thread_local bool t_sk_allowed = true;
-// Off by default: on the 1.5B step it measured slower in-step (57k vs 70k tokens/s) although
-// isolated launches are on par; PB_STREAMK=1 enables it.
-int g_force_sk = -1;  // tests: -1 environment, 0 off, 1 stream-K, 2 hybrid
-int sk_enabled() {
-    static const int on = [] {
-        const char* e = std::getenv("PB_STREAMK");
-        return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
-    }();
-    if (!t_sk_allowed) return 0;
-    return g_force_sk < 0 ? on : g_force_sk;
-}
-
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2 = 1>
 void launch(const GemmArgs& g, cudaStream_t s) {
     using C_ = Cfg<BN, CG, BM2>;
@@ -577,26 +504,10 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
-               nullptr, nullptr, 0, 0, 0};
+               g.rs, g.rs_inv_n, g.rs_eps, g.ss_out};
     const int tiles = ((g.M + BM * CG * BM2 - 1) / (BM * CG * BM2)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
-    int grid = (tiles < slots ? tiles : slots) * CG;
-    // stream-K when whole tiles would leave a ragged last wave (and a k split is possible)
-    // (>= 2 k-blocks of work per pair, so no pair's range is empty: an owner waits on every pair
-    // whose range starts inside its tile)
-    // hybrid (PB_STREAMK=2): the full waves run whole tiles, only the ragged last wave is split
-    const int sk_mode = sk_enabled();
-    const int dp = sk_mode == 2 ? (tiles / slots) * slots : 0;
-    if (BM2 == 1 && sk_mode && tiles % slots != 0 && tiles < 8 * slots && g.K / BK >= 4 &&
-        (long long)(tiles - dp) * (g.K / BK) >= 2LL * slots) {
-        SkWorkspace& w = sk_workspace(s);
-        kp.sk = 1;
-        kp.sk_dp = dp;
-        kp.sk_ws = w.ws;
-        kp.sk_flag = w.flags;
-        kp.sk_epoch = ++w.epoch;
-        grid = slots * CG;
-    }
+    const int grid = (tiles < slots ? tiles : slots) * CG;
     launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, CG, ta, tb, kp);
 }
 
@@ -687,7 +598,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     }();
     (void)attr;
     KParams kp{0, 0, 0, nullptr, nullptr, nullptr, 0, 0, g.accumulate,
-               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, nullptr, 0, 0, 0};
+               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, 0.f, 0.f, nullptr};
     const int slots = sm_count() / 2;
     const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
     CUtensorMap dummy{};
@@ -700,40 +611,8 @@ void gemm_group_destroy(GemmGroup& g) {
     g.n = 0;
 }
 
-void gemm_allow_stream_k(bool on) { t_sk_allowed = on; }
-void gemm_force_stream_k(int on) { g_force_sk = on; }
-
 static int g_force_cg = -1;  // tests: -1 auto, 1 or 2 forced
 void gemm_force_cta_group(int cg) { g_force_cg = cg; }
-
-// F-pass pair GEMMs (both operands K-major) can pick the tile width that minimises
-// waves x width on the GPU's CTA pairs: e.g. at T = 4096 the QKV projection (N = 3h = 6144)
-// runs 512 tiles of 256 x 192 in 7 waves instead of 384 of 256 x 256 in 6 (5.2 used), and the
-// N = h = 2048 projections 208 tiles of 256 x 160 in 3 waves instead of 128 in 2 (1.73 used).
-// The last column tile may be partial (TMA zero-fills B rows >= N, the epilogue skips them).
-// Off by default (PB_GEMM_BN=1 enables it): measured at T = 4096 the narrower tiles lose more per
-// tile than the waves gain (QKV 1431 -> 1446 TFLOP/s, FC2 1399 -> 1334 on 256 x 160), consistent
-// with the extra A-panel traffic (13 instead of 8 column tiles re-read A from L2).
-static int g_force_bn = 0;  // tests: 0 = PB_GEMM_BN, else 256 / 192 / 160
-void gemm_force_bn(int bn) { g_force_bn = bn; }
-int gemm_f_bn(int M, int N) {
-    if (g_force_bn) return g_force_bn;
-    static const bool on = [] {
-        const char* e = std::getenv("PB_GEMM_BN");
-        return e && e[0] == '1';
-    }();
-    if (!on) return 256;
-    const int pairs = sm_count() / 2;
-    const int mt = M / 256;
-    auto cost = [&](int bn) {
-        const long long tiles = (long long)mt * ((N + bn - 1) / bn);
-        return double((tiles + pairs - 1) / pairs) * bn * (bn == 256 ? 1.0 : 1.03);  // narrower tiles: more A reuse traffic
-    };
-    int best = 256;
-    for (int bn : {192, 160})
-        if (cost(bn) < cost(best)) best = bn;
-    return best;
-}
 
 // 512 x 256 CTA-pair tiles (BM2 = 2) for full-tile launches (PB_GEMM_BM2=1 or the test hook);
 // a pair's epilogue is then not overlapped with its next tile's main loop.  Default: K >= 8192 only:
@@ -750,7 +629,7 @@ static bool use_bm2(const GemmArgs& g) {
     }();
     const int mode = g_force_bm2 >= 0 ? g_force_bm2 : env;
     const bool on = mode == 1 || (mode < 0 && g.K >= 8192);
-    return on && g.M % 512 == 0 && g.N % 256 == 0 && sk_enabled() == 0;
+    return on && g.M % 512 == 0 && g.N % 256 == 0;
 }
 
 void gemm(const GemmArgs& g, cudaStream_t s) {
@@ -762,21 +641,10 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     const bool full = g.M % 256 == 0 && g.N % 256 == 0;
     const bool pair_ok = full || (g.M >= 256 && g.N >= 256 && g.epi != EPI_RESID && g.epi != EPI_DGELU);
     const int cg = g_force_cg > 0 ? (pair_ok ? g_force_cg : 1) : (pair_ok ? 2 : 1);
-    const bool f_pass = !g.a_mn && !g.b_mn && (g.epi == EPI_STORE || g.epi == EPI_GELU || g.epi == EPI_RESID);
-    const int fbn = cg == 2 && f_pass && g.M % 256 == 0 ? gemm_f_bn(g.M, g.N) : 256;
-    if (cg == 2 && fbn == 192) {
-        switch (g.epi) {
-            case EPI_STORE: return launch<192, false, false, EPI_STORE, 2>(g, s);
-            case EPI_GELU: return launch<192, false, false, EPI_GELU, 2>(g, s);
-            default: return launch<192, false, false, EPI_RESID, 2>(g, s);
-        }
-    } else if (cg == 2 && fbn == 160) {
-        switch (g.epi) {
-            case EPI_STORE: return launch<160, false, false, EPI_STORE, 2>(g, s);
-            case EPI_GELU: return launch<160, false, false, EPI_GELU, 2>(g, s);
-            default: return launch<160, false, false, EPI_RESID, 2>(g, s);
-        }
-    } else if (cg == 2 && use_bm2(g))
+    if (g.rs && (g.epi == EPI_RESID || g.epi == EPI_F32))
+        throw std::invalid_argument("gemm: a row scale applies to the store / GELU / dGELU epilogues");
+    if (g.ss_out && g.epi != EPI_RESID) throw std::invalid_argument("gemm: ss_out needs the residual epilogue");
+    if (cg == 2 && use_bm2(g))
         dispatch<256, 2, 2>(g, s);
     else if (cg == 2)
         dispatch<256, 2>(g, s);

@@ -94,91 +94,60 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const _
     reinterpret_cast<uint4*>(dx + size_t(row) * h)[c] = pack8(o);
 }
 
-// Warp-per-row variants for h = 256 * CH (CH 16-byte chunks per lane, all loads in flight at
-// once, shuffle reductions only): no block barriers, 8 rows per 256-thread CTA.
-template <int CH>
-__global__ void __launch_bounds__(256) rmsnorm_fwd_warp_kernel(const __nv_bfloat16* __restrict__ x,
-                                                               const __nv_bfloat16* __restrict__ g,
-                                                               __nv_bfloat16* __restrict__ y, float* __restrict__ rstd,
-                                                               int T, float eps) {
+// ---- RMSNorm folded into the neighbouring GEMMs (executor.cpp, fold mode).  The forward never
+// materialises the normalised rows: the producer's residual epilogue accumulates ss = sum x^2, the
+// consumer GEMM scales its accumulator rows by rstd = rsqrt(ss / h + eps).  Only a stage's input
+// (pulled from the previous stage or embedded) needs this standalone statistic.
+// ss[row] = sum_c x[row, c]^2 ; one warp per row
+__global__ void __launch_bounds__(256) row_sumsq_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ ss,
+                                                        int T, int h) {
     pdl_wait();
     pdl_launch();
     const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (row >= T) return;
-    constexpr int h = 256 * CH;
     const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h);
-    uint4 xv[CH];
-#pragma unroll
-    for (int k = 0; k < CH; ++k) xv[k] = xr[k * 32 + lane];
-    float ss = 0.f;
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
+    float acc = 0.f;
+    for (int c = lane; c < (h >> 3); c += 32) {
         float f[8];
-        unpack8(xv[k], f);
+        unpack8(xr[c], f);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+        for (int i = 0; i < 8; ++i) acc = fmaf(f[i], f[i], acc);
     }
-    ss = warp_sum(ss);
-    const float r = rsqrtf(ss / float(h) + eps);
-    if (lane == 0) rstd[row] = r;
-    uint4* yr = reinterpret_cast<uint4*>(y + size_t(row) * h);
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-        float f[8], w[8] = {1, 1, 1, 1, 1, 1, 1, 1};
-        unpack8(xv[k], f);
-        if (g) unpack8(reinterpret_cast<const uint4*>(g)[k * 32 + lane], w);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = f[i] * r * w[i];
-        yr[k * 32 + lane] = pack8(f);
-    }
+    acc = warp_sum(acc);
+    if (lane == 0) ss[row] = acc;
 }
 
-template <int CH>
-__global__ void __launch_bounds__(256) rmsnorm_bwd_warp_kernel(const __nv_bfloat16* __restrict__ dy,
-                                                               const __nv_bfloat16* __restrict__ x,
-                                                               const __nv_bfloat16* __restrict__ g,
-                                                               const float* __restrict__ rstd,
-                                                               const __nv_bfloat16* __restrict__ dres,
-                                                               __nv_bfloat16* __restrict__ dx, int T) {
+// Backward of y = rstd * x (gamma folded away) given dy' = rstd * dy (the consuming projection's
+// dX GEMM ran on row-scaled output gradients):  dx = dy' - x * rstd^2 * mean(dy' * x) + dres,
+// rstd = rsqrt(ss / h + eps).  One CTA per row, one 16-byte chunk per thread.
+__global__ void rmsnorm_bwd_x_kernel(const __nv_bfloat16* __restrict__ dyp, const __nv_bfloat16* __restrict__ x,
+                                     const float* __restrict__ ss, const __nv_bfloat16* __restrict__ dres,
+                                     __nv_bfloat16* __restrict__ dx, int h, float eps) {
     pdl_wait();
     pdl_launch();
-    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (row >= T) return;
-    constexpr int h = 256 * CH;
-    const uint4* ar = reinterpret_cast<const uint4*>(dy + size_t(row) * h);
-    const uint4* br = reinterpret_cast<const uint4*>(x + size_t(row) * h);
-    uint4 av[CH], bv[CH];
+    __shared__ float red[32];
+    const int row = blockIdx.x, c = threadIdx.x;
+    float a[8], b[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(dyp + size_t(row) * h)[c], a);
+    unpack8(reinterpret_cast<const uint4*>(x + size_t(row) * h)[c], b);
+    if (dres) {
+        unpack8(reinterpret_cast<const uint4*>(dres + size_t(row) * h)[c], o);
+    } else {
 #pragma unroll
-    for (int k = 0; k < CH; ++k) {
-        av[k] = ar[k * 32 + lane];
-        bv[k] = br[k * 32 + lane];
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
     }
-    const float r = rstd[row];
+    const float inv_h = 1.f / float(h);
+    const float r2 = 1.f / (ss[row] * inv_h + eps);
     float dot = 0.f;
 #pragma unroll
-    for (int k = 0; k < CH; ++k) {
-        float a[8], b[8], w[8] = {1, 1, 1, 1, 1, 1, 1, 1};
-        unpack8(av[k], a);
-        unpack8(bv[k], b);
-        if (g) unpack8(reinterpret_cast<const uint4*>(g)[k * 32 + lane], w);
+    for (int i = 0; i < 8; ++i) dot = fmaf(a[i], b[i], dot);
+    dot = block_sum(dot, red);
+    const float k = dot * r2 * inv_h;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dot += w[i] * a[i] * b[i];
-    }
-    dot = warp_sum(dot);
-    const float kk = dot * r * r * r / float(h);
-    uint4* dr = reinterpret_cast<uint4*>(dx + size_t(row) * h);
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-        float a[8], b[8], w[8] = {1, 1, 1, 1, 1, 1, 1, 1}, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        unpack8(av[k], a);
-        unpack8(bv[k], b);
-        if (g) unpack8(reinterpret_cast<const uint4*>(g)[k * 32 + lane], w);
-        if (dres) unpack8(reinterpret_cast<const uint4*>(dres + size_t(row) * h)[k * 32 + lane], o);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] += r * w[i] * a[i] - b[i] * kk;
-        dr[k * 32 + lane] = pack8(o);
-    }
+    for (int i = 0; i < 8; ++i) o[i] += a[i] - b[i] * k;
+    reinterpret_cast<uint4*>(dx + size_t(row) * h)[c] = pack8(o);
 }
+
 
 // dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t], deterministic two-stage column reduction:
 // stage 1: thread = 8 columns x `rows_per_block` rows -> partial[row_block][h] (no atomics)
@@ -289,7 +258,8 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 
 // one block per row: loss += (lse - z[label]) * scale ; z <- (softmax(z) - onehot) * scale  (bf16, in place)
 __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ logits, const int32_t* __restrict__ labels,
-                                                 float* __restrict__ loss, int V, float scale, int* err) {
+                                                 float* __restrict__ loss, int V, float scale, int* err,
+                                                 const float* __restrict__ rs, float rs_inv_n, float rs_eps) {
     pdl_wait();
     pdl_launch();
     __shared__ float red[32];
@@ -338,6 +308,8 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
     const float zl = lab_ok ? __bfloat162float(z[lab]) : 0.f;
     __syncthreads();
     const float inv = 1.f / s;
+    // folded final RMSNorm: dlogits' = rstd_f * dlogits (the head's dX and dW GEMMs then use x, not x-hat)
+    const float gsc = rs ? scale * rsqrtf(rs[row] * rs_inv_n + rs_eps) : scale;
     for (int c = threadIdx.x; c < nch; c += blockDim.x) {
         float f[8];
         unpack8(z4[c], f);
@@ -345,7 +317,7 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
         for (int i = 0; i < 8; ++i) {
             float p = __expf(f[i] - m) * inv;
             if (c * 8 + i == lab) p -= 1.f;
-            f[i] = p * scale;
+            f[i] = p * gsc;
         }
         z4[c] = pack8(f);
     }
@@ -466,37 +438,27 @@ int grid_for(size_t n, int per_thread, int block) {
 
 }  // namespace
 
-// Warp-per-row variants measured neutral in-step (84.9k vs 84.9k tokens/s at 1.5B): the norms sit
-// between dependent GEMMs and are bound by the PDL hand-off, not by their own bandwidth.
-// Off by default; PB_RMSNORM_WARP=1 selects them.
-static bool rmsnorm_warp_rows() {
-    static const bool on = [] {
-        const char* e = std::getenv("PB_RMSNORM_WARP");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 void rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
                  cudaStream_t s) {
     if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
-    const dim3 grid((T + 7) / 8);
-    if (rmsnorm_warp_rows() && h == 2048)
-        return launch_k(rmsnorm_fwd_warp_kernel<8>, grid, dim3(256), 0, s, 1, x, g, y, rstd, T, 1e-5f);
-    if (rmsnorm_warp_rows() && h == 4096)
-        return launch_k(rmsnorm_fwd_warp_kernel<16>, grid, dim3(256), 0, s, 1, x, g, y, rstd, T, 1e-5f);
     launch_k(rmsnorm_fwd_kernel, dim3(T), dim3(h / 8), 0, s, 1, x, g, y, rstd, T, h, 1e-5f);
 }
 
 void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
                  const __nv_bfloat16* dres, __nv_bfloat16* dx, int T, int h, cudaStream_t s) {
     if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
-    const dim3 grid((T + 7) / 8);
-    if (rmsnorm_warp_rows() && h == 2048)
-        return launch_k(rmsnorm_bwd_warp_kernel<8>, grid, dim3(256), 0, s, 1, dy, x, g, rstd, dres, dx, T);
-    if (rmsnorm_warp_rows() && h == 4096)
-        return launch_k(rmsnorm_bwd_warp_kernel<16>, grid, dim3(256), 0, s, 1, dy, x, g, rstd, dres, dx, T);
     launch_k(rmsnorm_bwd_kernel, dim3(T), dim3(h / 8), 0, s, 1, dy, x, g, rstd, dres, dx, T, h);
+}
+
+void row_sumsq(const __nv_bfloat16* x, float* ss, int T, int h, cudaStream_t s) {
+    if (h % 8) throw std::invalid_argument("row_sumsq: h % 8");
+    launch_k(row_sumsq_kernel, dim3((T + 7) / 8), dim3(256), 0, s, 1, x, ss, T, h);
+}
+
+void rmsnorm_bwd_x(const __nv_bfloat16* dyp, const __nv_bfloat16* x, const float* ss, const __nv_bfloat16* dres,
+                   __nv_bfloat16* dx, int T, int h, float eps, cudaStream_t s) {
+    if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
+    launch_k(rmsnorm_bwd_x_kernel, dim3(T), dim3(h / 8), 0, s, 1, dyp, x, ss, dres, dx, h, eps);
 }
 
 void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, float* scratch,
@@ -519,9 +481,9 @@ void embed_bwd(const int32_t* tok, const __nv_bfloat16* dx, float* demb, int T, 
     launch_k(embed_bwd_kernel, dim3(T), dim3(128), 0, s, 1, tok, dx, demb, T, h, V, err);
 }
 void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, int T, int V, float scale, int* err,
-                   cudaStream_t s) {
+                   cudaStream_t s, const float* rs, float rs_inv_n, float rs_eps) {
     if (V % 8) throw std::invalid_argument("cross_entropy: V % 8");
-    launch_k(ce_kernel, dim3(T), dim3(512), 0, s, 1, logits, labels, loss, V, scale, err);
+    launch_k(ce_kernel, dim3(T), dim3(512), 0, s, 1, logits, labels, loss, V, scale, err, rs, rs_inv_n, rs_eps);
 }
 void adamw(float* w, __nv_bfloat16* wb, float* g, float* m, float* v, size_t n, float lr, float b1, float b2,
            float eps, float wd, int step, cudaStream_t s) {

@@ -1,37 +1,81 @@
-"""Attention micro-benchmark (causal, head_dim 128): TFLOP/s of fwd kernels (causal FLOPs = 2*s^2*h per seq)."""
+"""Attention micro-benchmark (causal, head_dim 128): our tcgen05 forward / backward vs torch SDPA
+(cuDNN and flash backends) on the same box, same shapes.  Causal FLOPs: fwd 2*s^2*h per sequence
+(4*s^2*d*H / 2), bwd 2.5x fwd.  Every kernel is timed alone with CUDA events (median of 20 after 5
+warm-up launches).
+
+    python -m tests.bench_attn [out.json]
+"""
 import json
+import statistics
 import sys
 
 import torch
 
 from tests import kernels as K
-from tests.bench_gemm import timeit
+
+SHAPES = [(2, 2048, 16), (1, 4096, 32), (1, 6144, 48), (1, 2048, 16)]
+
+
+def timeit(fn, iters=20, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return statistics.median(ts)
+
+
+def sdpa_times(batch, seq, heads, backend):
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    q = torch.randn(batch, heads, seq, 128, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+    k, v = torch.randn_like(q, requires_grad=True), torch.randn_like(q, requires_grad=True)
+    sd = torch.nn.functional.scaled_dot_product_attention
+    be = {"cudnn": SDPBackend.CUDNN_ATTENTION, "flash": SDPBackend.FLASH_ATTENTION}[backend]
+    try:
+        with sdpa_kernel([be]):
+            t_f = timeit(lambda: sd(q, k, v, is_causal=True))
+            o = sd(q, k, v, is_causal=True)
+            go = torch.randn_like(o)
+            t_b = timeit(lambda: torch.autograd.grad(o, (q, k, v), go, retain_graph=True))
+        return t_f, t_b
+    except RuntimeError as e:  # backend unavailable for this shape
+        return None, str(e).splitlines()[0]
 
 
 def main():
-    for batch, seq, heads in [(1, 2048, 16), (2, 2048, 16), (1, 4096, 32), (1, 6144, 48)]:
+    rows = []
+    for batch, seq, heads in SHAPES:
         qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda").bfloat16()
-        fl = 2.0 * seq * seq * heads * 128 * batch  # causal fwd: 4*s^2*d*H/2
-        t_old = timeit(lambda: K.attn_fwd(qkv, batch, seq, heads))
-        t_new = timeit(lambda: K.attn_fwd_tc(qkv, batch, seq, heads))
-        out, lse2 = K.attn_fwd(qkv, batch, seq, heads)
+        fl = 2.0 * seq * seq * heads * 128 * batch
+        t_f = timeit(lambda: K.attn_fwd_tc(qkv, batch, seq, heads))
+        out, lse2 = K.attn_fwd_tc(qkv, batch, seq, heads)
         dout = torch.randn_like(out)
-        t_bwd = timeit(lambda: K.attn_bwd(qkv, out, dout, lse2, batch, seq, heads))
-        t_bwd_tc = timeit(lambda: K.attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads))
-        # library reference point (cuDNN / flash SDPA through torch), fwd and fwd+bwd
-        q = torch.randn(batch, heads, seq, 128, device="cuda", dtype=torch.bfloat16, requires_grad=True)
-        k, v = torch.randn_like(q, requires_grad=True), torch.randn_like(q, requires_grad=True)
-        sd = torch.nn.functional.scaled_dot_product_attention
-        t_sdpa = timeit(lambda: sd(q, k, v, is_causal=True))
-        o = sd(q, k, v, is_causal=True)
-        go = torch.randn_like(o)
-        t_sdpa_fb = timeit(lambda: torch.autograd.grad(sd(q, k, v, is_causal=True), (q, k, v), go))
-        print(json.dumps({"sdpa_fwd_tflops": fl / t_sdpa / 1e9, "sdpa_bwd_tflops_est": 2.5 * fl / max(1e-9, t_sdpa_fb - t_sdpa) / 1e9}))
-        print(json.dumps({"batch": batch, "seq": seq, "heads": heads, "fwd_mma_sync_us": t_old * 1e3,
-                          "fwd_tcgen05_us": t_new * 1e3, "fwd_mma_sync_tflops": fl / t_old / 1e9,
-                          "fwd_tcgen05_tflops": fl / t_new / 1e9, "bwd_mma_sync_us": t_bwd * 1e3,
-                          "bwd_mma_sync_tflops": 2.5 * fl / t_bwd / 1e9,
-                          "bwd_tcgen05_us": t_bwd_tc * 1e3, "bwd_tcgen05_tflops": 2.5 * fl / t_bwd_tc / 1e9}), flush=True)
+        t_b = timeit(lambda: K.attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads))
+        row = {"batch": batch, "seq": seq, "heads": heads, "fwd_us": t_f * 1e3, "bwd_us": t_b * 1e3,
+               "fwd_tflops": fl / t_f / 1e9, "bwd_tflops": 2.5 * fl / t_b / 1e9}
+        for be in ("cudnn", "flash"):
+            sf, sb = sdpa_times(batch, seq, heads, be)
+            if sf is None:
+                row[f"sdpa_{be}"] = {"unavailable": sb}
+            else:
+                row[f"sdpa_{be}"] = {"fwd_us": sf * 1e3, "bwd_us": sb * 1e3, "fwd_tflops": fl / sf / 1e9,
+                                     "bwd_tflops": 2.5 * fl / sb / 1e9}
+        best = [row[f"sdpa_{b}"] for b in ("cudnn", "flash") if "fwd_tflops" in row[f"sdpa_{b}"]]
+        if best:
+            row["fwd_vs_best_sdpa"] = row["fwd_tflops"] / max(b["fwd_tflops"] for b in best)
+            row["bwd_vs_best_sdpa"] = row["bwd_tflops"] / max(b["bwd_tflops"] for b in best)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    if len(sys.argv) > 1:
+        with open(sys.argv[1], "w") as f:
+            json.dump({"gpu": torch.cuda.get_device_name(0), "def": "causal FLOPs: fwd 2*s^2*h per sequence, bwd 2.5x; "
+                       "median of 20 CUDA-event timings per kernel, launched alone", "rows": rows}, f, indent=1)
 
 
 if __name__ == "__main__":

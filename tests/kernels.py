@@ -27,30 +27,21 @@ def gemm(A, B, C_, *, a_mn=False, b_mn=False, epi=0, C2=None, aux=None, accumula
                           _s()))
 
 
+def gemm_rownorm(A, B, C_, *, b_mn=False, epi=0, C2=None, aux=None, rs=None, ss_out=None, inv_n=0.0, eps=1e-5):
+    """gemm with the folded-RMSNorm hooks: row scale rsqrt(rs * inv_n + eps) / residual sum of squares."""
+    M, K = A.shape
+    N = B.shape[1] if b_mn else B.shape[0]
+    _lib.check(_lib.lib().pbt_gemm_rownorm(M, N, K, _p(A), A.stride(0), 0, _p(B), B.stride(0), int(b_mn), _p(C_),
+                                           C_.stride(0), _p(C2), _p(aux), aux.stride(0) if aux is not None else 0,
+                                           epi, _f(rs), C.c_float(inv_n), C.c_float(eps), _f(ss_out), _s()))
+
+
 def _f(t):
     return C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_float)) if t is not None else None
 
 
 def _i(t):
     return C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_int32))
-
-
-def attn_fwd(qkv, batch, seq, heads):
-    T = batch * seq
-    out = torch.empty(T, heads * 128, device="cuda", dtype=torch.bfloat16)
-    lse2 = torch.empty(heads, T, device="cuda", dtype=torch.float32)
-    _lib.check(_lib.lib().pbt_attn_fwd(_p(qkv), _p(out), _f(lse2), batch, seq, heads, _s()))
-    return out, lse2
-
-
-def attn_bwd(qkv, out, dout, lse2, batch, seq, heads):
-    T = batch * seq
-    dsum = torch.empty(heads, T, device="cuda", dtype=torch.float32)
-    dq = torch.empty(T, heads * 128, device="cuda", dtype=torch.float32)
-    dqkv = torch.empty_like(qkv)
-    _lib.check(_lib.lib().pbt_attn_bwd(_p(qkv), _p(out), _p(dout), _f(lse2), _f(dsum), _f(dq), _p(dqkv), batch, seq,
-                                       heads, _s()))
-    return dqkv
 
 
 def rmsnorm_fwd(x, g):
@@ -111,13 +102,5 @@ def set_pair_rows(rows: int) -> None:
     _lib.check(_lib.lib().pbt_gemm_set_pair_rows(rows))
 
 
-def set_tile_n(bn: int) -> None:
-    _lib.check(_lib.lib().pbt_gemm_set_tile_n(bn))
-
-
 def set_cta_group(cg: int) -> None:
     _lib.check(_lib.lib().pbt_gemm_set_cta_group(cg))
-
-
-def set_stream_k(on: int) -> None:
-    _lib.check(_lib.lib().pbt_gemm_set_stream_k(on))
