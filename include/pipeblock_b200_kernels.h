@@ -24,11 +24,13 @@ int pbt_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_
 int pbt_gemm_set_cta_group(int32_t cg);
 int pbt_gemm_set_pair_rows(int32_t rows); /* CTA-pair tile rows: 256, 512 (two A sub-tiles per CTA, M % 512 == 0), -1 = PB_GEMM_BM2 */
 /* pbt_gemm plus the folded-RMSNorm hooks: rs (may be NULL) = per-row sum of squares, the accumulator row
- * is scaled by rsqrt(rs[row] * rs_inv_n + rs_eps) (epi 0 / 1 / 3); ss_out (may be NULL, epi 2) += the
- * row's sum of squares of the stored bf16 outputs. */
+ * is scaled by rsqrt(rs[row] * rs_inv_n + rs_eps) (epi 0 / 1 / 3); ss_out (may be NULL, epi 2) = the
+ * row's sum of squares of the stored bf16 outputs (deterministic, bit-identical to pbt_row_sumsq). */
 int pbt_gemm_rownorm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn, const void* B,
                      int32_t ldb, int32_t b_mn, void* C, int32_t ldc, void* C2, const void* aux, int32_t ldaux,
                      int32_t epi, const float* rs, float rs_inv_n, float rs_eps, float* ss_out, void* stream);
+/* ss[t] = sum of squares of row t of x [T,h] bf16 (h % 128 == 0), in the GEMM epilogue's order */
+int pbt_row_sumsq(const void* x, float* ss, int32_t T, int32_t h, void* stream);
 /* causal attention, head_dim 128, tcgen05/TMEM (the executor's forward attention): qkv [T,3h] -> out [T,h],
  * lse2 [heads,T] (base-2 LSE of scaled scores); seq % 128 == 0 */
 int pbt_attn_fwd_tc(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);

@@ -44,7 +44,16 @@ extern "C" int pbt_gemm_rownorm(int32_t M, int32_t N, int32_t K, const void* A, 
         g.aux = static_cast<const __nv_bfloat16*>(aux), g.ldaux = ldaux;
         g.epi = epi;
         g.rs = rs, g.rs_inv_n = rs_inv_n, g.rs_eps = rs_eps, g.ss_out = ss_out;
-        pbk::gemm(g, static_cast<cudaStream_t>(stream));
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (ss_out) {  // the row-statistic workspace (the executor keeps one per device)
+            const size_t part = size_t(M) * (N / 128) * 4, cnt = size_t(M / 32 + 1) * 4;
+            if (cudaMallocAsync(reinterpret_cast<void**>(&g.ss_part), part + cnt, st) != cudaSuccess)
+                throw pbx::CudaError("ss workspace allocation failed");
+            g.ss_cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(g.ss_part) + part);
+            cudaMemsetAsync(g.ss_cnt, 0, cnt, st);
+        }
+        pbk::gemm(g, st);
+        if (ss_out) cudaFreeAsync(g.ss_part, st);
         cuda_check("pbt_gemm_rownorm");
     });
 }
@@ -52,6 +61,13 @@ extern "C" int pbt_gemm_rownorm(int32_t M, int32_t N, int32_t K, const void* A, 
 #define BF(p) static_cast<const __nv_bfloat16*>(p)
 #define BFM(p) static_cast<__nv_bfloat16*>(p)
 #define ST(s) static_cast<cudaStream_t>(s)
+
+extern "C" int pbt_row_sumsq(const void* x, float* ss, int32_t T, int32_t h, void* stream) {
+    return pbx::guard([&] {
+        pbk::row_sumsq(BF(x), ss, T, h, ST(stream));
+        cuda_check("pbt_row_sumsq");
+    });
+}
 
 extern "C" int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h,
                                void* stream) {

@@ -20,6 +20,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -111,7 +113,7 @@ void Exec::build_layout() {
             }
             y.lse = add(cur, size_t(H) * T * 4);
         }
-        if (fold) {  // one block of per-token sums of squares, zeroed at the start of every F pass
+        if (fold) {  // one block of per-token sums of squares, written by every F pass
             L.ss_bytes = size_t(2 * Lc + 1) * T * 4;
             L.ss = add(cur, L.ss_bytes);
             for (int l = 0; l < Lc; ++l) {
@@ -319,6 +321,10 @@ void Exec::init(int device) {
     scratch = static_cast<__nv_bfloat16*>(dmalloc(size_t(T) * h * 2, "scratch"));
     dsum = static_cast<float*>(dmalloc(size_t(H) * T * 4, "scratch"));
     dq_acc = static_cast<float*>(dmalloc(size_t(T) * h * 4, "scratch"));
+    // deterministic row sums of squares (folded RMSNorm): per-128-column partials + row-group counters
+    ss_part = static_cast<float*>(dmalloc(size_t(T) * (h / 128) * 4, "scratch"));
+    ss_cnt = static_cast<int*>(dmalloc(size_t(T / 32 + 1) * 4, "scratch"));
+    ck(cudaMemsetAsync(ss_cnt, 0, size_t(T / 32 + 1) * 4, cs), "memset");
     tokens = static_cast<int32_t*>(dmalloc(size_t(m) * T * 4, "inputs"));
     labels = static_cast<int32_t*>(dmalloc(size_t(m) * T * 4, "inputs"));
     loss_dev = static_cast<float*>(dmalloc(64, "loss"));
@@ -415,6 +421,14 @@ __nv_bfloat16* Exec::outbox_ptr(int k) const { return reinterpret_cast<__nv_bflo
 
 template <typename Fn>
 void Exec::timed(const char* label, Fn&& fn) {
+    static const bool sync_trace = std::getenv("PB_SYNC_TRACE") != nullptr;  // debugging: which launch hangs
+    if (sync_trace) {
+        std::fprintf(stderr, "[dev %d] launch %s\n", dev, label);
+        fn();
+        ck(cudaStreamSynchronize(cs), "sync trace");
+        std::fprintf(stderr, "[dev %d] done %s\n", dev, label);
+        return;
+    }
     if (!kernel_timing) {
         fn();
         return;
@@ -443,6 +457,7 @@ void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __
                 int epi, const __nv_bfloat16* aux, void* C2, int accumulate, const float* rs, float* ss_out) {
     pbk::GemmArgs g;
     g.rs = rs, g.rs_inv_n = 1.f / float(h), g.rs_eps = kNormEps, g.ss_out = ss_out;
+    if (ss_out) g.ss_part = ss_part, g.ss_cnt = ss_cnt;
     g.M = M, g.N = N, g.K = K;
     g.A = A, g.a_mn = a_mn, g.lda = a_mn ? M : K;
     g.B = B, g.b_mn = b_mn, g.ldb = b_mn ? N : K;
@@ -450,7 +465,10 @@ void Exec::gemm(int M, int N, int K, const __nv_bfloat16* A, bool a_mn, const __
     g.aux = aux, g.ldaux = N;
     g.epi = epi, g.accumulate = accumulate;
     const char* glabel = a_mn ? "gemm_W" : (b_mn ? "gemm_B" : "gemm_F");
-    if (kernel_timing) {
+    static const bool sync_trace = std::getenv("PB_SYNC_TRACE") != nullptr;
+    if (kernel_timing || sync_trace) {
+        if (sync_trace) std::fprintf(stderr, "[dev %d] gemm M%d N%d K%d epi%d amn%d bmn%d rs%d ss%d\n", dev, M, N, K, epi,
+                                     int(a_mn), int(b_mn), rs != nullptr, ss_out != nullptr);
         timed(glabel, [&] { pbk::gemm(g, cs); });
         gemm_flops_acc += 2.0 * double(M) * double(N) * double(K);
     } else if (gemm_timing) {
@@ -505,7 +523,8 @@ void Exec::build_w_groups() {
 }
 
 void Exec::run_gemm_timed(const char* label, double flops, const std::function<void()>& fn) {
-    if (kernel_timing) {
+    static const bool sync_trace = std::getenv("PB_SYNC_TRACE") != nullptr;
+    if (kernel_timing || sync_trace) {
         timed(label, fn);
         gemm_flops_acc += flops;
     } else if (gemm_timing) {
@@ -539,7 +558,8 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         // RMSNorm folded into the GEMMs around it (gamma is folded into the consuming weights, see
         // fold_weight): the residual epilogues accumulate each row's sum of squares, the consuming
         // projection scales its accumulator rows by rstd = rsqrt(ss / h + eps); x-hat is never stored.
-        ck(cudaMemsetAsync(f32(slot, L.ss), 0, L.ss_bytes, cs), "memset");
+        // Every statistic is written (not accumulated) and is bit-identical whether it comes from an
+        // epilogue or from row_sumsq, so results do not depend on where the stage boundaries fall.
         timed("row_sumsq", [&] { pbk::row_sumsq(x0, f32(slot, L.layer.empty() ? L.ssf : L.layer[0].ss1), T, h, cs); });
         ++launches;
     }
@@ -867,6 +887,25 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
 
 void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
     ck(cudaSetDevice(cuda), "cudaSetDevice");
+    if (const char* wd = std::getenv("PB_WATCHDOG_S"); wd && kernel_timing) {
+        // debugging: name the first launch of this device that has not completed after the deadline
+        const auto t0 = std::chrono::steady_clock::now();
+        while (cudaStreamQuery(cs) == cudaErrorNotReady) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::duration<double>(std::atof(wd))) {
+                for (size_t e = 0; e + 1 < kev_used; e += 2)
+                    if (cudaEventQuery(kev[e + 1]) == cudaErrorNotReady) {
+                        std::fprintf(stderr, "[dev %d] watchdog: launch %zu (%s) not complete, started: %d\n", dev,
+                                     e / 2, klabels[size_t(kev_label[e / 2])].c_str(),
+                                     int(cudaEventQuery(kev[e]) == cudaSuccess));
+                        break;
+                    }
+                std::fflush(stderr);
+                std::this_thread::sleep_for(std::chrono::seconds(2));  // let the peer devices report too
+                std::abort();
+            }
+            std::this_thread::sleep_for(std::chrono::milliseconds(5));
+        }
+    }
     ck(cudaStreamSynchronize(cs), "step");
     ck(cudaStreamSynchronize(xs), "step");
     pending = false;

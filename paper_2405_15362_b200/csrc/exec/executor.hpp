@@ -167,6 +167,8 @@ class Exec {
     uint32_t* flags = nullptr;
     __nv_bfloat16* scratch = nullptr;
     float *dsum = nullptr, *dq_acc = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
+    float* ss_part = nullptr;
+    int* ss_cnt = nullptr;
     int* id_err() { return reinterpret_cast<int*>(loss_dev + 1); }  // out-of-range token/label flag
     int32_t *tokens = nullptr, *labels = nullptr;
     std::vector<void*> allocations;

@@ -180,13 +180,15 @@ __global__ void __launch_bounds__(192, 1)
         mbar_init(o_full, 1);
         fence_barrier_init();
     }
+    // TMEM is allocated only once the previous kernel in the stream has finished: a CTA that
+    // launched early (PDL) never holds TMEM while it waits (see gemm_tc.cu)
+    pdl_wait();
+    pdl_launch();
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;  // cols [0,128) S0, [128,256) S1, [256,384) O, [384,448) P0, [448,512) P1
-    pdl_wait();
-    pdl_launch();
 
     if (warp == 0) {
         if (elect_one()) {
@@ -457,13 +459,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int i = 0; i < 18; ++i) mbar_init(&bars[i], (i == 12 || i == 14 || i == 16) ? 8 : 1);
         fence_barrier_init();
     }
+    // TMEM is allocated only once the previous kernel in the stream has finished: a CTA that
+    // launched early (PDL) never holds TMEM while it waits (see gemm_tc.cu)
+    pdl_wait();
+    pdl_launch();
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;  // [0,128) S^T -> P^T ; [128,256) dP^T -> dQ ; dV ; dK
-    pdl_wait();
-    pdl_launch();
 
     if (warp >= 10) {
         if (warp == 10 && lane_id() == 0) {
@@ -784,13 +788,15 @@ __global__ void __launch_bounds__(192, 2)
         for (int i = 0; i < 8; ++i) mbar_init(&bars[i], i == 6 ? 4 : 1);
         fence_barrier_init();
     }
+    // TMEM is allocated only once the previous kernel in the stream has finished: a CTA that
+    // launched early (PDL) never holds TMEM while it waits (see gemm_tc.cu)
+    pdl_wait();
+    pdl_launch();
     if (warp == 1) tmem_alloc<256>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_wait();
-    pdl_launch();
 
     if (warp == 0) {
         if (elect_one()) {

@@ -33,8 +33,13 @@ struct GemmArgs {
     // folded RMSNorm (STORE / GELU / DGELU): acc(row, :) *= rsqrt(rs[row] * rs_inv_n + rs_eps)
     const float* rs = nullptr;
     float rs_inv_n = 0.f, rs_eps = 0.f;
-    // RESID: ss_out[row] += sum of squares of the row's stored (bf16) outputs (atomic, per tile)
+    // RESID: ss_out[row] = sum of squares of the row's stored (bf16) outputs, deterministic: every
+    // tile writes one fp32 partial per 128 columns to ss_part ([N/128][M]); the last tile to finish a
+    // 32-row group (ss_cnt[row / 32], zero before the launch and reset by that tile) sums the partials
+    // in column order.  row_sumsq() (ops.hpp) computes the bit-identical value from a stored matrix.
     float* ss_out = nullptr;
+    float* ss_part = nullptr;
+    int* ss_cnt = nullptr;
 };
 
 void gemm(const GemmArgs& g, cudaStream_t s);

@@ -74,8 +74,11 @@ struct KParams {
     // rs = the row's sum of squares over the normalised width
     const float* rs;
     float rs_inv_n, rs_eps;
-    // EPI_RESID: ss_out[row] += sum over this tile's columns of bf16(out)^2 (the next RMSNorm's statistic)
+    // EPI_RESID: ss_out[row] = sum of bf16(out)^2 over the row (the next RMSNorm's statistic), from
+    // per-128-column partials (ss_part, [N/128][M]) summed in column order by the row group's last tile
     float* ss_out;
+    float* ss_part;
+    int* ss_cnt;
 };
 
 // Resolves tile t of the launch: its problem's descriptors, origin, K blocks, output.
@@ -148,14 +151,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_barrier_init();
     }
+    // TMEM is allocated after griddepcontrol.wait, and for a CTA pair only once both CTAs are
+    // resident: a CTA launched early by PDL must not hold (or block in) tcgen05.alloc while its
+    // peer or the previous kernel still owns the columns (observed: a pair hung in the prologue
+    // with one CTA at the cluster barrier and the other never leaving the allocation).
+    pdl_wait();
+    pdl_launch();
+    if constexpr (CG == 2) cluster_sync();
     if (warp == 1) tmem_alloc<C_::kTmemCols, CG>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     if constexpr (CG == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_wait();
-    pdl_launch();
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = row0 + s2 * kPairRows;
             const uint32_t tbase = tbase0 + s2 * 256;
             const float rsc = (p.rs && row < p.M) ? rsqrtf(p.rs[row] * p.rs_inv_n + p.rs_eps) : 1.f;
-            float ssq = 0.f;  // EPI_RESID with ss_out: sum of squares of this row's stored outputs
+            float ssq = 0.f;  // EPI_RESID with ss_out: sum of squares of this row's stored outputs per 128 columns
             uint4 aux_next[4];
             // (aux epilogues run only on full tiles: layer GEMMs have M = tokens, N = h or 4h)
             if constexpr (kAux) {
@@ -378,6 +386,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
+                    if constexpr (EPI == EPI_RESID) {
+                        if (p.ss_out && ((c + 32) & 127) == 0) {  // end of a 128-column chunk: its partial
+                            p.ss_part[size_t(col >> 7) * p.M + row] = ssq;
+                            ssq = 0.f;
+                        }
+                    }
                     if constexpr (EPI == EPI_GELU) {
                         // activation from the bf16-rounded pre-activation, as the backward sees it
                         uint4* g4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C2) + size_t(row) * p.ldc + col);
@@ -394,7 +408,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if constexpr (EPI == EPI_RESID) {
-                if (p.ss_out && row < p.M) atomicAdd(p.ss_out + row, ssq);
+                if (p.ss_out) {
+                    // deterministic row reduction: the last of the row group's N tiles sums the
+                    // partials in column order (threadfence reduction; the counter resets itself)
+                    __threadfence();
+                    __syncwarp();
+                    int last = 0;
+                    if (lane_id() == 0) last = atomicAdd(p.ss_cnt + (row >> 5), 1) == (p.N + BN - 1) / BN - 1;
+                    if (__shfl_sync(0xffffffffu, last, 0)) {
+                        __threadfence();
+                        if (row < p.M) {
+                            float sum = 0.f;
+                            for (int q = 0; q < (p.N >> 7); ++q) sum += __ldcg(p.ss_part + size_t(q) * p.M + row);
+                            p.ss_out[row] = sum;
+                        }
+                        if (lane_id() == 0) p.ss_cnt[row >> 5] = 0;
+                    }
+                }
             }
             }  // s2
             tc_fence_before();
@@ -504,7 +534,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
-               g.rs, g.rs_inv_n, g.rs_eps, g.ss_out};
+               g.rs, g.rs_inv_n, g.rs_eps, g.ss_out, g.ss_part, g.ss_cnt};
     const int tiles = ((g.M + BM * CG * BM2 - 1) / (BM * CG * BM2)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
     const int grid = (tiles < slots ? tiles : slots) * CG;
@@ -598,7 +628,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     }();
     (void)attr;
     KParams kp{0, 0, 0, nullptr, nullptr, nullptr, 0, 0, g.accumulate,
-               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, 0.f, 0.f, nullptr};
+               static_cast<const GroupProblem*>(g.table), g.n, g.total_tiles, nullptr, 0.f, 0.f, nullptr, nullptr, nullptr};
     const int slots = sm_count() / 2;
     const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
     CUtensorMap dummy{};
@@ -644,6 +674,8 @@ void gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.rs && (g.epi == EPI_RESID || g.epi == EPI_F32))
         throw std::invalid_argument("gemm: a row scale applies to the store / GELU / dGELU epilogues");
     if (g.ss_out && g.epi != EPI_RESID) throw std::invalid_argument("gemm: ss_out needs the residual epilogue");
+    if (g.ss_out && (!g.ss_part || !g.ss_cnt || g.N % 128))
+        throw std::invalid_argument("gemm: ss_out needs the ss_part / ss_cnt workspace and N % 128 == 0");
     if (cg == 2 && use_bm2(g))
         dispatch<256, 2, 2>(g, s);
     else if (cg == 2)

@@ -98,23 +98,39 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const _
 // materialises the normalised rows: the producer's residual epilogue accumulates ss = sum x^2, the
 // consumer GEMM scales its accumulator rows by rstd = rsqrt(ss / h + eps).  Only a stage's input
 // (pulled from the previous stage or embedded) needs this standalone statistic.
-// ss[row] = sum_c x[row, c]^2 ; one warp per row
+// ss[row] = sum_c x[row, c]^2, bit-identical to the residual GEMM epilogue's statistic (gemm_tc.cu):
+// one fp32 partial per 128 columns accumulated pair by pair in column order as
+// fmaf(lo, lo, fmaf(hi, hi, acc)), then the partials summed in column order.
+// Block = 4 rows x P threads (P = h / 128 <= 64), thread = one 128-column chunk.
 __global__ void __launch_bounds__(256) row_sumsq_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ ss,
                                                         int T, int h) {
     pdl_wait();
     pdl_launch();
-    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (row >= T) return;
-    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h);
-    float acc = 0.f;
-    for (int c = lane; c < (h >> 3); c += 32) {
-        float f[8];
-        unpack8(xr[c], f);
+    __shared__ float part[256];
+    const int P = h >> 7;
+    const int r = int(threadIdx.x) / P, q = int(threadIdx.x) % P;
+    const int row = blockIdx.x * 4 + r;
+    if (r < 4 && row < T) {
+        const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(row) * h + q * 128);
+        float acc = 0.f;
+#pragma unroll 4
+        for (int c = 0; c < 16; ++c) {
+            const uint4 v = xr[c];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc = fmaf(f[i], f[i], acc);
+            for (int e = 0; e < 4; ++e) {
+                const float lo = bf16_lo(w[e]), hi = bf16_hi(w[e]);
+                acc = fmaf(lo, lo, fmaf(hi, hi, acc));
+            }
+        }
+        part[threadIdx.x] = acc;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) ss[row] = acc;
+    __syncthreads();
+    if (r < 4 && q == 0 && row < T) {
+        float sum = 0.f;
+        for (int k = 0; k < P; ++k) sum += part[threadIdx.x + k];
+        ss[row] = sum;
+    }
 }
 
 // Backward of y = rstd * x (gamma folded away) given dy' = rstd * dy (the consuming projection's
@@ -451,8 +467,8 @@ void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfl
 }
 
 void row_sumsq(const __nv_bfloat16* x, float* ss, int T, int h, cudaStream_t s) {
-    if (h % 8) throw std::invalid_argument("row_sumsq: h % 8");
-    launch_k(row_sumsq_kernel, dim3((T + 7) / 8), dim3(256), 0, s, 1, x, ss, T, h);
+    if (h % 128 || h > 8192) throw std::invalid_argument("row_sumsq: h must be a multiple of 128 and <= 8192");
+    launch_k(row_sumsq_kernel, dim3((T + 3) / 4), dim3(4 * (h / 128)), 0, s, 1, x, ss, T, h);
 }
 
 void rmsnorm_bwd_x(const __nv_bfloat16* dyp, const __nv_bfloat16* x, const float* ss, const __nv_bfloat16* dres,

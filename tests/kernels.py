@@ -27,6 +27,11 @@ def gemm(A, B, C_, *, a_mn=False, b_mn=False, epi=0, C2=None, aux=None, accumula
                           _s()))
 
 
+def row_sumsq(x, ss):
+    T, h = x.shape
+    _lib.check(_lib.lib().pbt_row_sumsq(_p(x), _f(ss), T, h, _s()))
+
+
 def gemm_rownorm(A, B, C_, *, b_mn=False, epi=0, C2=None, aux=None, rs=None, ss_out=None, inv_n=0.0, eps=1e-5):
     """gemm with the folded-RMSNorm hooks: row scale rsqrt(rs * inv_n + eps) / residual sum of squares."""
     M, K = A.shape

@@ -109,11 +109,17 @@ def test_folded_rmsnorm_epilogues(cta_group, M, N, Kd):
     W = torch.randn(N, Kd, device="cuda", generator=g).bfloat16() * 0.05
     R = torch.randn(M, N, device="cuda", generator=g).bfloat16()
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ss = torch.full((M,), 0.5, device="cuda")  # accumulates onto what is there
+    ss = torch.full((M,), 0.5, device="cuda")  # overwritten
     K.gemm_rownorm(A, W, out, epi=2, aux=R, ss_out=ss)
+    ss2 = torch.full((M,), -1.0, device="cuda")
+    K.gemm_rownorm(A, W, out, epi=2, aux=R, ss_out=ss2)  # the row-group counters reset themselves
+    ss_k = torch.empty(M, device="cuda")
+    K.row_sumsq(out, ss_k)
     torch.cuda.synchronize()
     assert rel(out, A.float() @ W.float().t() + R.float()) < 4e-3
-    assert rel(ss, 0.5 + out.float().pow(2).sum(1)) < 1e-5
+    assert rel(ss, out.float().pow(2).sum(1)) < 1e-5
+    # deterministic, and bit-identical to the standalone statistic of a stage's input rows
+    assert torch.equal(ss, ss2) and torch.equal(ss, ss_k)
     # consumer: rows of X scaled by rstd(ss) through the epilogue == GEMM of the normalised rows
     X = out
     W2 = torch.randn(Kd, N, device="cuda", generator=g).bfloat16() * 0.05
