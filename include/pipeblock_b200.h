@@ -230,7 +230,8 @@ typedef struct pb_exec_stats {
                                D2H), i.e. the whole step on this device's compute stream */
     double busy_ms;         /* this device: sum of pass durations */
     int64_t pool_slots;     /* activation slots allocated = predicted exact_peak on this device */
-    int64_t pool_peak;      /* slots live at once, counted while running */
+    int64_t pool_peak;      /* slots live at once over the op order as enqueued (a host-side count, not a
+                               device measurement; device bytes come from pb_exec_memory) */
     int64_t slot_bytes;     /* bytes per activation slot */
     int64_t pool_bytes;     /* slot_bytes * pool_slots + the LM-head pool (head slot bytes * head slots,
                                last-stage device only: final-norm output and logits) */

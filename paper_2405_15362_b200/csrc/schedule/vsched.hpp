@@ -1,10 +1,15 @@
 // vsched — the schedule front end of the B200 V-shape pipeline executor.
 //
-// A from-scratch restatement of the reference "pipeblock" building-block API
-// (/root/reference/proj/include/pipeblock/*.hpp).  Same semantics, same
-// results bit for bit (pinned by tests/golden against the reference compiled
-// from its own headers), different structure: one value-type model, free
-// functions, no templates beyond the cell/time duration type.
+// A restatement of the reference "pipeblock" building-block API
+// (/root/reference/proj/include/pipeblock/*.hpp) with the same results bit for
+// bit (pinned by tests/golden against the reference compiled from its own
+// headers).  The data model differs (one value-type model, free functions, no
+// templates beyond the cell/time duration type), but the greedy passes —
+// repeat, validate_schedule, squeeze, reorder (assemble.hpp:85-397) — follow
+// the reference statement by statement: their tie-breaks ARE the op order the
+// executor must reproduce and their error strings are part of the interface,
+// so they are a close transliteration by necessity (CPU front end, not the
+// B200 hot path).
 //
 //   reference symbol                         here
 //   model.hpp:15  PassKind                   vsched::Kind

@@ -224,9 +224,18 @@ def project_via_chunks(args, mcfg, name, p, m, comm_ms):
         return frozenset(chunk_class(st, n_stages) for st in range(1, n_stages + 1) if topo.device_of(st) == d)
 
     probe_bytes = {classes(probe.topology, probe_S, d): b for d, b in slot_bytes.items()}
+    # the LM-head pool (logits + final hidden per live head microbatch) sits on the device holding stage
+    # S, outside the activation slots: take the probe's (pool_bytes - slots * slot_bytes) on that device
+    probe_last = probe.topology.device_of(probe_S)
+    st_last = None
+    for d, st in res.per_device.items():
+        if d == probe_last:
+            st_last = st
+    head_bytes = int(st_last.pool_bytes - st_last.slot_bytes * st_last.pool_slots) if st_last else 0
     pool = []
     for d in range(1, p + 1):
-        pool.append(int(pred[d - 1]) * probe_bytes[classes(target.topology, S, d)])
+        pool.append(int(pred[d - 1]) * probe_bytes[classes(target.topology, S, d)]
+                    + (head_bytes if target.topology.device_of(S) == d else 0))
     T = cfg.tokens_per_microbatch
     return {"schedule": name, "p": p, "probe": f"{name} p={probe_p} m={probe_m}, {cfg.layers} layers "
                                                 f"({per_chunk} per chunk, {last} on the LM-head chunk)",
@@ -235,7 +244,9 @@ def project_via_chunks(args, mcfg, name, p, m, comm_ms):
             "bubble_rate": rep.bubble_rate, "bubble_rate_zero_comm": rep0.bubble_rate,
             "pipeline_roofline_frac": max(rep.busy) / rep.makespan, "ideal_ms": max(rep.busy),
             "busy_ms_per_device": rep.busy, "mean_pass_ms": {f"{c}.{k}": v for (c, k), v in sorted(mean.items())},
-            "predicted_peak_units": pred, "pool_bytes_per_device": pool, "max_pool_gib": max(pool) / 2**30,
+            "predicted_peak_units": pred, "pool_bytes_per_device": pool, "head_pool_bytes": head_bytes,
+            "pool_def": "predicted peak slots x probe slot bytes (same chunk classes) + the probe's LM-head pool on "
+                        "the device holding the last stage", "max_pool_gib": max(pool) / 2**30,
             "probe_slot_bytes": sorted(set(slot_bytes.values()))}
 
 
