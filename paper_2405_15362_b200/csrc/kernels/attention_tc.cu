@@ -742,6 +742,349 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ backward v5 (half-tile pipeline)
+// Same math and CTA decomposition as v4 (CTA per 128-key tile kb, loop over the query rows >= kb),
+// but the query loop runs in 64-row HALF tiles j with two TMEM buffers, so the tensor pipe computes
+// S^T / dP^T of half tile j+1 while the compute warps form P^T / dS^T of half tile j:
+//   buffer b = j & 1:  [b*128, +64)  S^T_j  (128 keys x 64 queries) -> P^T_j bf16 pairs in [+0, +32)
+//                      [b*128+64, +64) dP^T_j -> dQ^T_j (fp32, 128 d lanes x 64 queries)
+//   [256,384) dV, [384,512) dK accumulators (as v4).
+// dS^T_j goes to shared memory only ([key][q], one 128B-swizzled atom): it is the B operand
+// (MN-major) of dQ^T_j = K^T dS^T_j and the A operand (K-major) of dK_j.
+// MMA issue order (one thread, in-order pipe):  S_0 dP_0 S_1 dP_1 | per j: [ds_full_j] dQ^T_j dK_j dV_j
+// S_{j+2} [dq_free_j] dP_{j+2}: dQ^T_j first, over the consumed dP^T_j columns, so it can be drained
+// while dK_j / dV_j run; S_{j+2} overwrites P^T_j after dV_j read it.
+// Compute warps (thread = TMEM lane, column half hf of the 64 queries), per j: E_j (S, dP -> P, dS;
+// lse2 / D as smem float4 broadcasts) -> ds_full_j -> read dQ^T_{j-1} (thread = d lane) ->
+// dq_free_{j-1} -> stage it fp32 (128B-swizzled [64 q][32 d] chunks, a warp writes one 128 B row per
+// store) -> dq_staged -> the reducer warp issues the TMA bulk reduce-add.  Per 64-row half tile the
+// MMAs are 5 x 128x64x128-equivalent (~1.3k cycles at full rate); phase stamps
+// (tests/trace_attn_bwd.py) put the period at ~2.9k cycles, bounded by the dP_{j+2} -> dQ^T_j drain
+// dependency and the per-SM TMA reduce of 32 KB (~1.6k cycles to read out under full-chip load).
+constexpr int BQH = 64;
+constexpr int kHalf = BQH * D * 2;  // 16 KB: two 128B-swizzled atoms of [64 rows][64]
+struct Bwd5Smem {
+    static constexpr int k = 0;                 // [128 keys][128 d]: two atoms of 16 KB
+    static constexpr int v = k + kTile;
+    static constexpr int q = v + kTile;         // [3] half tiles
+    static constexpr int dO = q + 3 * kHalf;    // [3]
+    static constexpr int ds = dO + 3 * kHalf;   // [2] dS^T_j: [128 keys][64 q] bf16, one atom
+    static constexpr int stg = ds + 2 * 16384;  // dQ staging: 4 chunks [64 q][32 d] fp32, 8 KB each
+    static constexpr int lse = stg + 32768;     // [2][128] floats: lse2[64] | D[64]
+    static constexpr int bars = lse + 1024;
+    static constexpr int total = bars + 256 + 512;  // 512 B alignment slack (as BwdSmem)
+};
+static_assert(Bwd5Smem::total <= 232448, "attn bwd v5: shared memory over the sm_100 opt-in limit");
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_tc5_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                        const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
+                        const float* __restrict__ lse2, const float* __restrict__ dsum,
+                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale,
+                        const float* __restrict__ rs, float rs_inv_n, float rs_eps) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd5Smem::bars);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* q_full = bars + 1;      // [3]
+    uint64_t* q_empty = bars + 4;     // [3] MMA commit after dK_j
+    uint64_t* do_full = bars + 7;     // [3]
+    uint64_t* do_empty = bars + 10;   // [3] MMA commit after dV_j
+    uint64_t* s_full = bars + 13;     // [2]
+    uint64_t* dp_full = bars + 15;    // [2]
+    uint64_t* ds_full = bars + 17;    // [2] 8 compute warps
+    uint64_t* dq_full = bars + 19;    // [2]
+    uint64_t* dq_free = bars + 21;    // [2] 8 compute warps
+    uint64_t* stg_free = bars + 23;   // reducer: staging read out
+    uint64_t* dq_staged = bars + 24;  // 8 compute warps
+    uint64_t* dkv_full = bars + 25;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+    float* sL = reinterpret_cast<float*>(sm + Bwd5Smem::lse);
+
+    const uint32_t warp = warp_id();
+    const int nqb = seq / BQ;
+    const int hb = int(blockIdx.x) % (H * (T / seq));
+    const int kb = int(blockIdx.x) / (H * (T / seq));
+    const int head = hb % H, b = hb / H;
+    const int tok0 = b * seq;
+    const int n = 2 * (nqb - kb);               // half tiles
+    const int qrow0 = tok0 + kb * BQ;           // token row of half tile 0
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&tm_kv);
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_do);
+        tma_prefetch(&tm_dq);
+        for (int i = 0; i < 26; ++i) {
+            const bool eight = (i >= 17 && i < 19) || (i >= 21 && i < 23) || i == 24;
+            mbar_init(&bars[i], eight ? 8 : 1);
+        }
+        fence_barrier_init();
+    }
+    pdl_wait();
+    pdl_launch();
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp >= 10) {
+        if (warp == 10 && lane_id() == 0) {
+            // dQ reducer: four 8 KB TMA bulk reduce-adds per half tile
+            for (int u = 0; u < n; ++u) {
+                mbar_wait(dq_staged, u & 1);
+                ATRACE(u, 6);
+                const int row = qrow0 + u * BQH;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tm_dq)),
+                        "r"(smem_u32(sm + Bwd5Smem::stg + c * 8192)), "r"(head * D + c * 32), "r"(row)
+                        : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                ATRACE(u, 7);
+                mbar_arrive(stg_free);
+            }
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        if (warp == 11 && lane_id() == 0) {
+            for (int j = 0; j < n; ++j) {
+                const int st = j % 3;
+                if (j >= 3) mbar_wait(&do_empty[st], ((j / 3) - 1) & 1);
+                uint8_t* dst = sm + Bwd5Smem::dO + st * kHalf;
+                mbar_expect_tx(&do_full[st], kHalf);
+                tma_load_2d(dst, &tm_do, &do_full[st], head * D, qrow0 + j * BQH);
+                tma_load_2d(dst + 8192, &tm_do, &do_full[st], head * D + 64, qrow0 + j * BQH);
+            }
+        }
+    } else if (warp == 0) {
+        if (lane_id() == 0) {
+            const int ck = H * D + head * D, cv = 2 * H * D + head * D;
+            const int kr = tok0 + kb * BK;
+            mbar_expect_tx(kv_full, 2 * kTile);
+            tma_load_2d(sm + Bwd5Smem::k, &tm_kv, kv_full, ck, kr);
+            tma_load_2d(sm + Bwd5Smem::k + 16384, &tm_kv, kv_full, ck + 64, kr);
+            tma_load_2d(sm + Bwd5Smem::v, &tm_kv, kv_full, cv, kr);
+            tma_load_2d(sm + Bwd5Smem::v + 16384, &tm_kv, kv_full, cv + 64, kr);
+            for (int j = 0; j < n; ++j) {
+                const int st = j % 3;
+                if (j >= 3) mbar_wait(&q_empty[st], ((j / 3) - 1) & 1);
+                ATRACE(j, 11);
+                uint8_t* dst = sm + Bwd5Smem::q + st * kHalf;
+                mbar_expect_tx(&q_full[st], kHalf);
+                tma_load_2d(dst, &tm_q, &q_full[st], head * D, qrow0 + j * BQH);
+                tma_load_2d(dst + 8192, &tm_q, &q_full[st], head * D + 64, qrow0 + j * BQH);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id_sd = idesc_bf16(128, 64, false, false);   // S^T, dP^T: K-major x K-major
+        constexpr uint32_t id_kv = idesc_bf16(128, 128, false, true);   // dK, dV: A from TMEM, B MN-major
+        constexpr uint32_t id_dq = idesc_bf16(128, 64, true, true);     // dQ^T = K^T dS^T: both MN-major
+        const uint32_t sk = smem_u32(sm + Bwd5Smem::k), sv = smem_u32(sm + Bwd5Smem::v);
+        auto issue_sd = [&](int j, bool dp) {  // S^T_j = K Q_j^T or dP^T_j = V dO_j^T
+            const int st = j % 3;
+            uint64_t* full = dp ? &do_full[st] : &q_full[st];
+            const uint32_t sb = smem_u32(sm + (dp ? Bwd5Smem::dO : Bwd5Smem::q) + st * kHalf);
+            const uint32_t sa = dp ? sv : sk;
+            mbar_wait(full, (j / 3) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma(tmem + (j & 1) * 128 + (dp ? 64 : 0), sdesc(sa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                           sdesc(sb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_sd, kk != 0);
+                tc_commit(dp ? &dp_full[j & 1] : &s_full[j & 1]);
+            }
+            __syncwarp();
+        };
+        mbar_wait(kv_full, 0);
+        issue_sd(0, false);
+        issue_sd(0, true);
+        issue_sd(1, false);
+        issue_sd(1, true);
+        for (int j = 0; j < n; ++j) {
+            const int bb = j & 1, st = j % 3;
+            const uint32_t sq = smem_u32(sm + Bwd5Smem::q + st * kHalf);
+            const uint32_t sdo = smem_u32(sm + Bwd5Smem::dO + st * kHalf);
+            const uint32_t sds = smem_u32(sm + Bwd5Smem::ds + bb * 16384);
+            mbar_wait(&ds_full[bb], (j >> 1) & 1);
+            tc_fence_after();
+            if (lane_id() == 0) ATRACE(j, 8);
+            if (elect_one()) {
+                // dQ^T_j = K^T dS^T_j over the consumed dP^T_j columns: first, so the compute warps can
+                // drain it while dK_j / dV_j run
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma(tmem + bb * 128 + 64, sdesc(sk + kk * 2048, 16384, 1024), sdesc(sds + kk * 2048, 8192, 1024),
+                           id_dq, kk != 0);
+                tc_commit(&dq_full[bb]);
+                // dK += dS^T_j Q_j (A = the same dS^T smem tile read K-major; K = 64 queries)
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    tc_mma(tmem + 384, sdesc(sds + kk * 32, 16, 1024), sdesc(sq + kk * 2048, 8192, 1024), id_kv,
+                           (j | kk) != 0);
+                tc_commit(&q_empty[st]);
+                // dV += P^T_j dO_j (A = P^T bf16 pairs in TMEM)
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    tc_mma_ts(tmem + 256, tmem + bb * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
+                              sdesc(sdo + kk * 2048, 8192, 1024), id_kv, (j | kk) != 0);
+                tc_commit(&do_empty[st]);
+            }
+            __syncwarp();
+            if (j + 2 < n) {
+                issue_sd(j + 2, false);                // over P^T_j, after dV_j read it (in-order pipe)
+                mbar_wait(&dq_free[bb], (j >> 1) & 1);  // dQ^T_j read out of TMEM
+                tc_fence_after();
+                if (lane_id() == 0) ATRACE(j, 10);
+                issue_sd(j + 2, true);
+            }
+        }
+        if (elect_one()) tc_commit(dkv_full);
+        __syncwarp();
+    } else {
+        const uint32_t q4 = warp & 3;
+        const int hf = int(warp - 2) >> 2;  // query column half (32 of the 64) handled by this warp
+        const int r = int(q4 * 32 + lane_id());
+        const uint32_t lane_base = (q4 * 32) << 16;
+        const float sl2 = scale * kLog2e;
+        const int key = r;  // key row relative to the tile (queries relative to qrow0 below)
+        auto lse_of = [&](int j) {  // staged value of this thread (r < 64): lse2 (hf 0) or D (hf 1)
+            const size_t idx = size_t(head) * T + qrow0 + j * BQH + (r & 63);
+            return hf == 0 ? lse2[idx] : dsum[idx];
+        };
+        if (r < 64) sL[hf * 64 + r] = lse_of(0);
+        bar_sync_compute();
+        auto drain_dq = [&](int u) {  // dQ^T_u: TMEM -> registers -> release -> fp32 staging
+            const int pb = u & 1;
+            mbar_wait(&dq_full[pb], (u >> 1) & 1);
+            tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(u, 3);
+            float v[32];
+            tmem_ld32(tmem + lane_base + pb * 128 + 64 + hf * 32, v);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&dq_free[pb]);
+            if (u >= 1) mbar_wait(stg_free, (u - 1) & 1);
+            if (threadIdx.x == 64) ATRACE(u, 4);
+            // thread = d row r (chunk q4 = r / 32, lane = r % 32), 32 query rows hf*32 + c
+            uint8_t* chunk = sm + Bwd5Smem::stg + q4 * 8192;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int qq = hf * 32 + c;
+                *reinterpret_cast<float*>(chunk + qq * 128 + (((lane_id() >> 2) ^ (qq & 7)) << 4) + (lane_id() & 3) * 4) = v[c];
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(dq_staged);
+            if (threadIdx.x == 64) ATRACE(u, 5);
+        };
+        for (int j = 0; j < n; ++j) {
+            const int bb = j & 1;
+            const float* Lb = sL + bb * 128;
+            const float lnext = (j + 1 < n && r < 64) ? lse_of(j + 1) : 0.f;
+            if (threadIdx.x == 64) ATRACE(j, 0);
+            mbar_wait(&s_full[bb], (j >> 1) & 1);
+            if (threadIdx.x == 64) ATRACE(j, 12);
+            mbar_wait(&dp_full[bb], (j >> 1) & 1);
+            tc_fence_after();
+            if (threadIdx.x == 64) ATRACE(j, 1);
+            const int c0 = hf * 32;
+            {
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + bb * 128 + c0, sv);
+                tmem_ld32(tmem + lane_base + bb * 128 + 64 + c0, dp);
+                tmem_ld_wait();
+                if (threadIdx.x == 64) ATRACE(j, 13);
+                if (__builtin_expect(j < 2, 0)) {  // causal mask: the two half tiles of the diagonal block
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (key > j * BQH + c0 + e) sv[e] = -INFINITY;
+                }
+                // lse2 / D of this half's 32 query columns: the same for every lane (smem broadcast),
+                // loaded as float4 so the 32 independent exp2 chains issue back to back
+                const float4* l4 = reinterpret_cast<const float4*>(Lb + c0);
+                const float4* d4 = reinterpret_cast<const float4*>(Lb + 64 + c0);
+                uint32_t pk[16], dk[16];
+#pragma unroll
+                for (int e4 = 0; e4 < 8; ++e4) {
+                    const float4 lq = l4[e4], dq = d4[e4];
+                    const float lz[4] = {lq.x, lq.y, lq.z, lq.w}, dz[4] = {dq.x, dq.y, dq.z, dq.w};
+                    float pv[4], dsv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        pv[u] = fast_exp2(fmaf(sv[4 * e4 + u], sl2, -lz[u]));
+                        dsv[u] = pv[u] * (dp[4 * e4 + u] - dz[u]);
+                    }
+                    pk[2 * e4] = pack_bf16(pv[0], pv[1]);
+                    pk[2 * e4 + 1] = pack_bf16(pv[2], pv[3]);
+                    dk[2 * e4] = pack_bf16(dsv[0], dsv[1]);
+                    dk[2 * e4 + 1] = pack_bf16(dsv[2], dsv[3]);
+                }
+                if (threadIdx.x == 64) ATRACE(j, 14);
+                tmem_st16u(tmem + lane_base + bb * 128 + c0, pk);
+                // dS^T_j to smem ([key][q], 128B-swizzled, one atom): B operand (MN-major) of dQ^T_j and
+                // A operand (K-major) of dK_j.  Its last readers, dQ^T_{j-2} and dK_{j-2}, precede S_j in
+                // the MMA pipe, so s_full_j (waited above) covers them.
+                uint8_t* sds = sm + Bwd5Smem::ds + bb * 16384;
+#pragma unroll
+                for (int e8 = 0; e8 < 4; ++e8)
+                    *reinterpret_cast<uint4*>(sds + r * 128 + ((((c0 >> 3) + e8) ^ (r & 7)) << 4)) =
+                        make_uint4(dk[4 * e8], dk[4 * e8 + 1], dk[4 * e8 + 2], dk[4 * e8 + 3]);
+            }
+            tmem_st_wait();
+            if (threadIdx.x == 64) ATRACE(j, 15);
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&ds_full[bb]);
+            if (threadIdx.x == 64) ATRACE(j, 2);
+            if (j >= 1) drain_dq(j - 1);
+            if (j + 1 < n) {
+                if (r < 64) sL[((j + 1) & 1) * 128 + hf * 64 + r] = lnext;  // buffer last read by E_{j-1}
+                bar_sync_compute();
+            }
+        }
+        drain_dq(n - 1);
+        // dV, dK rows (thread = key row, column half hf), as v4
+        mbar_wait(dkv_full, 0);
+        tc_fence_after();
+        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
+        const float fv = rs ? rsqrtf(rs[tok0 + kb * BK + r] * rs_inv_n + rs_eps) : 1.f;
+        const float fk = fv * scale;
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = hf * 2 + cc;
+            float v[32], k[32];
+            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
+            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
+            tmem_ld_wait();
+            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
+            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                dv[e] = make_uint4(pack_bf16(v[8 * e] * fv, v[8 * e + 1] * fv), pack_bf16(v[8 * e + 2] * fv, v[8 * e + 3] * fv),
+                                   pack_bf16(v[8 * e + 4] * fv, v[8 * e + 5] * fv), pack_bf16(v[8 * e + 6] * fv, v[8 * e + 7] * fv));
+                dk[e] = make_uint4(pack_bf16(k[8 * e] * fk, k[8 * e + 1] * fk),
+                                   pack_bf16(k[8 * e + 2] * fk, k[8 * e + 3] * fk),
+                                   pack_bf16(k[8 * e + 4] * fk, k[8 * e + 5] * fk),
+                                   pack_bf16(k[8 * e + 6] * fk, k[8 * e + 7] * fk));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free<512>(tmem);
+    }
+}
+
 // ------------------------------------------------------------------ forward v3 (two CTAs per SM)
 // Single-buffered per CTA so that TWO CTAs fit on an SM (96 KB smem: Q, K, V; 256 TMEM columns:
 // S / P at [0,128), O at [128,256)): while one CTA runs its softmax the other CTA's S / PV MMAs
@@ -996,17 +1339,33 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     attn_bwd_pre(dout, out, dsum, dq_acc, heads, batch * seq, s);
     static bool once = [] {
         cudaFuncSetAttribute(attn_bwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::total);
+        cudaFuncSetAttribute(attn_bwd_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd5Smem::total);
         return true;
     }();
     (void)once;
+    static const int bver = [] {  // PB_ATTN_BWD=4 selects the full-tile kernel
+        const char* e = std::getenv("PB_ATTN_BWD");
+        return e && e[0] == '4' ? 4 : 5;
+    }();
     const int T = batch * seq;
     const CUtensorMap tq = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
-    const CUtensorMap td = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 128);
-    const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
-                                       uint64_t(heads) * D, 32, 128);
     static unsigned long long* trace = trace_buffer("PB_ATTN_TRACE");
-    launch_k(attn_bwd_tc4_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), BwdSmem::total, s, 1, tq, td, tdq,
-             lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs, rs_inv_n, rs_eps);
+    if (bver == 5) {
+        const CUtensorMap tq64 = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 64);
+        const CUtensorMap td64 = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 64);
+        const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D,
+                                           uint64_t(T), uint64_t(heads) * D, 32, 64);
+        launch_k(attn_bwd_tc5_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), Bwd5Smem::total, s, 1, tq,
+                 tq64, td64, tdq, lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs,
+                 rs_inv_n, rs_eps);
+    } else {
+        const CUtensorMap td = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 128);
+        const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D,
+                                           uint64_t(T), uint64_t(heads) * D, 32, 128);
+        launch_k(attn_bwd_tc4_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), BwdSmem::total, s, 1, tq,
+                 td, tdq, lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs,
+                 rs_inv_n, rs_eps);
+    }
     trace_dump(trace, "attn_bwd", s);
     attn_dq_store(dq_acc, dqkv, heads, T, s, rs, rs_inv_n, rs_eps);
 }

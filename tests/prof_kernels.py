@@ -16,6 +16,14 @@ W2t = torch.randn(h, 4 * h, device="cuda").bfloat16()
 K.gemm(dY, W2t, U, b_mn=True, epi=3, aux=U)                     # B: dgl * gelu'
 dW = torch.zeros(h, 4 * h, device="cuda")
 K.gemm(dY, G, dW, a_mn=True, b_mn=True, epi=4, accumulate=1)   # W: dW2 += dY^T gelu(u)
+# folded RMSNorm (the executor's default F pass): FC1+GELU with the rstd row scale, FC2 + residual
+# emitting the next norm's per-row sum of squares, and the stand-alone statistic of a stage input
+ss = (torch.rand(T, device="cuda") + 0.5) * h
+K.gemm_rownorm(A, W1, U, epi=1, C2=G, rs=ss, inv_n=1.0 / h)    # F: fc1 + GELU, rows scaled by rstd
+W2 = torch.randn(h, 4 * h, device="cuda").bfloat16()
+X1 = torch.empty(T, h, device="cuda", dtype=torch.bfloat16)
+K.gemm_rownorm(G, W2, X1, epi=2, aux=A, ss_out=ss)              # F: fc2 + residual + sum of squares
+K.row_sumsq(X1, ss)
 qkv = torch.randn(T, 3 * h, device="cuda").bfloat16()
 out, lse2 = K.attn_fwd_tc(qkv, B_, S_, H)
 dout = torch.randn_like(out)
