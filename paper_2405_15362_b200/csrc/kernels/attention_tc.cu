@@ -746,11 +746,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // Same math and CTA decomposition as v4 (CTA per 128-key tile kb, loop over the query rows >= kb),
 // but the query loop runs in 64-row HALF tiles j with two TMEM buffers, so the tensor pipe computes
 // S^T / dP^T of half tile j+1 while the compute warps form P^T / dS^T of half tile j:
-//   buffer b = j & 1:  [b*128, +64)  S^T_j  (128 keys x 64 queries) -> P^T_j bf16 pairs in [+0, +32)
+//   buffer b = j & 1:  [b*128, +64)  S^T_j  (128 keys x 64 queries); after the elementwise phase each
+//                      32-query half h holds P^T bf16 pairs in [32h, 32h+16) and dS^T pairs in [32h+16, 32h+32)
+//                      (the TMEM A operands of dV_j and dK_j)
 //                      [b*128+64, +64) dP^T_j -> dQ^T_j (fp32, 128 d lanes x 64 queries)
 //   [256,384) dV, [384,512) dK accumulators (as v4).
-// dS^T_j goes to shared memory only ([key][q], one 128B-swizzled atom): it is the B operand
-// (MN-major) of dQ^T_j = K^T dS^T_j and the A operand (K-major) of dK_j.
+// dS^T_j also goes to shared memory ([key][q], one 128B-swizzled atom) as the B operand (MN-major)
+// of dQ^T_j = K^T dS^T_j.  A operands come from TMEM wherever the layout allows: the kernel is bound
+// by shared-memory bandwidth (128 B/clk/SM: SS MMAs with N = 64 read 6 KB per 32-cycle K step, plus
+// the TMA fills, the dS^T tile and the fp32 dQ staging written and read back by the reduce).
 // MMA issue order (one thread, in-order pipe):  S_0 dP_0 S_1 dP_1 | per j: [ds_full_j] dQ^T_j dK_j dV_j
 // S_{j+2} [dq_free_j] dP_{j+2}: dQ^T_j first, over the consumed dP^T_j columns, so it can be drained
 // while dK_j / dV_j run; S_{j+2} overwrites P^T_j after dV_j read it.
@@ -922,11 +926,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     tc_mma(tmem + bb * 128 + 64, sdesc(sk + kk * 2048, 16384, 1024), sdesc(sds + kk * 2048, 8192, 1024),
                            id_dq, kk != 0);
                 tc_commit(&dq_full[bb]);
-                // dK += dS^T_j Q_j (A = the same dS^T smem tile read K-major; K = 64 queries)
+                // dK += dS^T_j Q_j (A = dS^T bf16 pairs in the S^T_j columns [16,32) / [48,64); K = 64 queries)
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    tc_mma(tmem + 384, sdesc(sds + kk * 32, 16, 1024), sdesc(sq + kk * 2048, 8192, 1024), id_kv,
-                           (j | kk) != 0);
+                    tc_mma_ts(tmem + 384, tmem + bb * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
+                              sdesc(sq + kk * 2048, 8192, 1024), id_kv, (j | kk) != 0);
                 tc_commit(&q_empty[st]);
                 // dV += P^T_j dO_j (A = P^T bf16 pairs in TMEM)
 #pragma unroll
@@ -1028,6 +1032,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 }
                 if (threadIdx.x == 64) ATRACE(j, 14);
                 tmem_st16u(tmem + lane_base + bb * 128 + c0, pk);
+                tmem_st16u(tmem + lane_base + bb * 128 + c0 + 16, dk);
                 // dS^T_j to smem ([key][q], 128B-swizzled, one atom): B operand (MN-major) of dQ^T_j and
                 // A operand (K-major) of dK_j.  Its last readers, dQ^T_{j-2} and dK_{j-2}, precede S_j in
                 // the MMA pipe, so s_full_j (waited above) covers them.
