@@ -1019,16 +1019,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 for (int e4 = 0; e4 < 8; ++e4) {
                     const float4 lq = l4[e4], dq = d4[e4];
                     const float lz[4] = {lq.x, lq.y, lq.z, lq.w}, dz[4] = {dq.x, dq.y, dq.z, dq.w};
-                    float pv[4], dsv[4];
+                    // packed f32x2 FMA / ADD / MUL (FFMA2 & co. on sm_100): half the issue slots
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        pv[u] = fast_exp2(fmaf(sv[4 * e4 + u], sl2, -lz[u]));
-                        dsv[u] = pv[u] * (dp[4 * e4 + u] - dz[u]);
+                    for (int u = 0; u < 4; u += 2) {
+                        const float2 x = __ffma2_rn(make_float2(sv[4 * e4 + u], sv[4 * e4 + u + 1]), make_float2(sl2, sl2),
+                                                    make_float2(-lz[u], -lz[u + 1]));
+                        const float2 pv = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                        const float2 dd = __fadd2_rn(make_float2(dp[4 * e4 + u], dp[4 * e4 + u + 1]),
+                                                     make_float2(-dz[u], -dz[u + 1]));
+                        const float2 dsv = __fmul2_rn(pv, dd);
+                        pk[2 * e4 + (u >> 1)] = pack_bf16(pv.x, pv.y);
+                        dk[2 * e4 + (u >> 1)] = pack_bf16(dsv.x, dsv.y);
                     }
-                    pk[2 * e4] = pack_bf16(pv[0], pv[1]);
-                    pk[2 * e4 + 1] = pack_bf16(pv[2], pv[3]);
-                    dk[2 * e4] = pack_bf16(dsv[0], dsv[1]);
-                    dk[2 * e4 + 1] = pack_bf16(dsv[2], dsv[3]);
                 }
                 if (threadIdx.x == 64) ATRACE(j, 14);
                 tmem_st16u(tmem + lane_base + bb * 128 + c0, pk);
@@ -1246,7 +1248,7 @@ __global__ void __launch_bounds__(192, 2)
             }
             if (j == 0) m_used = m_new;
             // pass 2: P = exp2(S*c - m) -> bf16 pairs over the consumed S columns [0,64)
-            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
             float s[4][32];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + c * 32, s[c]);
@@ -1260,16 +1262,16 @@ __global__ void __launch_bounds__(192, 2)
                 }
                 uint32_t pk[16];
 #pragma unroll
-                for (int e2 = 0; e2 < 16; ++e2) {
-                    const float p0 = fast_exp2(fmaf(s[c][2 * e2], sl2, -m_used));
-                    const float p1 = fast_exp2(fmaf(s[c][2 * e2 + 1], sl2, -m_used));
-                    rs8[(2 * e2) & 7] += p0;
-                    rs8[(2 * e2 + 1) & 7] += p1;
-                    pk[e2] = pack_bf16(p0, p1);
+                for (int e2 = 0; e2 < 16; ++e2) {  // packed f32x2 FMA / ADD (FFMA2, FADD2)
+                    const float2 x = __ffma2_rn(make_float2(s[c][2 * e2], s[c][2 * e2 + 1]), make_float2(sl2, sl2),
+                                                make_float2(-m_used, -m_used));
+                    const float2 pv = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                    rs4[e2 & 3] = __fadd2_rn(rs4[e2 & 3], pv);
+                    pk[e2] = pack_bf16(pv.x, pv.y);
                 }
                 tmem_st16u(tmem + lane_base + c * 16, pk);
             }
-            l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+            l += ((rs4[0].x + rs4[1].x) + (rs4[2].x + rs4[3].x)) + ((rs4[0].y + rs4[1].y) + (rs4[2].y + rs4[3].y));
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
