@@ -374,376 +374,14 @@ __global__ void __launch_bounds__(192, 1)
 
 
 // ------------------------------------------------------------------ backward
-// One CTA per (128-key tile kb, head, sequence), looping over query tiles qb >= kb:
-//   S^T  = K Q^T,  dP^T = V dO^T                       -> TMEM [0,128), [128,256)
-//   8 compute warps (2 per SM sub-partition, column halves; thread = key row):
-//        P^T = exp2(S^T*c - lse2[q]),  dS^T = P^T (dP^T - D[q])
-//   dV += P^T dO,  dK += dS^T Q                          -> TMEM [256,384), [384,512)
-//   dQ_tile = dS K                                       -> fp32 smem -> TMA bulk reduce-add into dq_acc
-// Shared memory: K, V, double-buffered Q / dO tiles, the dS^T tile and the lse / D rows.
-struct BwdSmem {
-    static constexpr int k = 0;
-    static constexpr int v = k + kTile;
-    static constexpr int q = v + kTile;       // [2]
-    static constexpr int dO = q + 2 * kTile;  // [2]
-    static constexpr int dst = dO + 2 * kTile;
-    static constexpr int lse = dst + kTile;   // [2][256] floats: lse2 | D
-    static constexpr int bars = lse + 2048;
-    // 512 B of alignment slack (the 227 KB opt-in limit leaves no room for 1 KB; the dynamic
-    // window starts 1 KB-aligned when the kernel has no static shared memory)
-    static constexpr int total = bars + 256 + 512;
-};
-static_assert(BwdSmem::total <= 232448, "attn bwd: shared memory over the sm_100 opt-in limit");
+// (round 1's full-tile kernel v4 is superseded by v5 below: 6-9 % slower at every measured shape,
+// profiles/r2_attn_vs_cudnn.json and DESIGN §4.)
 constexpr int kBwdThreads = 384;
 
 __device__ __forceinline__ void bar_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-// ------------------------------------------------------------------ backward kernel
-// MMA order chosen so that the dQ drain, its reduce and the
-// lse / D loads leave the tensor pipe's critical path:
-//   * dQ(i) = dS K goes into the consumed dP^T columns [128,256) and is issued FIRST after dS^T
-//     lands; the compute warps read it out (registers), release the columns, then stage it (fp32)
-//     in the consumed dO(i) buffer (d columns 0-63) and the consumed dS^T buffer (64-127) for the
-//     TMA bulk reduce-add, while the tensor pipe runs dV(i), dK(i) and S^T(i+1);
-//   * Q and dO have separate full / empty barriers: Q(i) is refilled as soon as dK(i) retires, dO(i)
-//     once the reduce has read the staging; the dS^T buffer is handed back to the compute warps
-//     (ds_buf) once the reduce has read its half, before they store dS^T(i+1);
-//   * dP^T(i+1) follows once dQ(i) has left TMEM, S^T(i+1) right after dV(i) read P^T (in-order pipe);
-//   * lse / D of query tile i+1 are loaded into registers while tile i is processed.
-// MMA issue order per tile: dK(i) dQ(i) dV(i) S^T(i+1) | dP^T(i+1); P^T and dS^T are A operands
-// straight from TMEM (bf16 pairs over their consumed fp32 columns), which keeps dK off shared memory.
-// 384 threads: warp 0 K/V + Q loads, warp 1 MMA, warps 2-9 compute, warp 10 dQ reducer, warp 11 dO
-// loads (each blocking wait on its own warp: a divergent lane's wait_group stalls its whole warp).
-// Measured dead ends: staging dQ in both Q(i) and dO(i) (as v3) stalls S^T(i+1) on the Q reload
-// behind the reduce; splitting the elementwise phase to run P^T under the MMAs, and draining dQ
-// with red.global.add from registers (L2 atomics issue-bound, ~2.7k cycles per tile), were slower.
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    attn_bwd_tc4_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
-                        const float* __restrict__ dsum,
-                        __nv_bfloat16* __restrict__ dqkv, int seq, int H, int T, float scale,
-                        const float* __restrict__ rs, float rs_inv_n, float rs_eps) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
-    if ((smem_u32(smem_raw) & 1023u) > 512u) __trap();  // alignment slack is 512 B (BwdSmem::total)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BwdSmem::bars);
-    uint64_t* kv_full = bars + 0;
-    uint64_t* q_full = bars + 1;     // [2]
-    uint64_t* do_full = bars + 3;    // [2]
-    uint64_t* q_empty = bars + 5;    // [2] MMA commit after dK(i): Q(i) no longer read
-    uint64_t* do_empty = bars + 7;   // [2] reducer: dQ(i) staging in dO(i) read out
-    uint64_t* s_full = bars + 9;     // MMA: S^T(i) in [0,128)
-    uint64_t* qdo_used = bars + 10;  // MMA commit after dK(i): dO(i), dS^T(i) no longer read
-    uint64_t* dp_full = bars + 11;   // MMA: dP^T(i) in [128,256)
-    uint64_t* ds_full = bars + 12;   // 8 compute warps: dS^T(i) in smem, P^T(i) in TMEM, S^T / dP^T consumed
-    uint64_t* dq_full = bars + 13;   // MMA: dQ(i) in [128,256)
-    uint64_t* dq_free = bars + 14;   // 8 compute warps: dQ(i) read out of TMEM
-    uint64_t* dkv_full = bars + 15;
-    uint64_t* dq_staged = bars + 16;  // 8 compute warps: dQ(i) staged (fp32) in dO(i) / dS^T buffers
-    uint64_t* ds_buf = bars + 17;     // reducer: the dS^T-buffer half of the staging read out
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
-    float* sL = reinterpret_cast<float*>(sm + BwdSmem::lse);
-
-    const uint32_t warp = warp_id();
-    const int nqb = seq / BQ;
-    const int hb = int(blockIdx.x) % (H * (T / seq));
-    const int kb = int(blockIdx.x) / (H * (T / seq));
-    const int head = hb % H, b = hb / H;
-    const int tok0 = b * seq;
-    const int nq = nqb - kb;
-
-    if (warp == 0 && elect_one()) {
-        tma_prefetch(&tm_qkv);
-        tma_prefetch(&tm_do);
-        tma_prefetch(&tm_dq);
-        for (int i = 0; i < 18; ++i) mbar_init(&bars[i], (i == 12 || i == 14 || i == 16) ? 8 : 1);
-        fence_barrier_init();
-    }
-    // TMEM is allocated only once the previous kernel in the stream has finished: a CTA that
-    // launched early (PDL) never holds TMEM while it waits (see gemm_tc.cu)
-    pdl_wait();
-    pdl_launch();
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;  // [0,128) S^T -> P^T ; [128,256) dP^T -> dQ ; dV ; dK
-
-    if (warp >= 10) {
-        if (warp == 10 && lane_id() == 0) {
-            // dQ reducer: one TMA bulk reduce-add per 16 KB chunk; the dS^T-buffer half first, so the
-            // compute warps get that buffer back early
-            for (int i = 0; i < nq; ++i) {
-                mbar_wait(dq_staged, i & 1);
-                const int row = tok0 + (kb + i) * BQ;
-                uint8_t* stage_d = sm + BwdSmem::dO + (i & 1) * kTile;
-                uint8_t* stage_s = sm + BwdSmem::dst;
-#pragma unroll
-                for (int c = 3; c >= 0; --c) {
-                    asm volatile(
-                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tm_dq)),
-                        "r"(smem_u32((c < 2 ? stage_d : stage_s) + (c & 1) * 16384)), "r"(head * D + c * 32), "r"(row)
-                        : "memory");
-                    if (c == 2) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                mbar_arrive(ds_buf);
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                mbar_arrive(&do_empty[i & 1]);
-            }
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        if (warp == 11 && lane_id() == 0) {
-            for (int i = 0; i < nq; ++i) {
-                const int st = i & 1;
-                if (i >= 2) mbar_wait(&do_empty[st], ((i - 2) >> 1) & 1);
-                uint8_t* ds = sm + BwdSmem::dO + st * kTile;
-                const int qr = tok0 + (kb + i) * BQ;
-                mbar_expect_tx(&do_full[st], kTile);
-                tma_load_2d(ds, &tm_do, &do_full[st], head * D, qr);
-                tma_load_2d(ds + 16384, &tm_do, &do_full[st], head * D + 64, qr);
-            }
-        }
-    } else if (warp == 0) {
-        const int cq = head * D;
-        if (lane_id() == 0) {
-            const int ck = H * D + head * D, cv = 2 * H * D + head * D;
-            const int kr = tok0 + kb * BK;
-            mbar_expect_tx(kv_full, 2 * kTile);
-            tma_load_2d(sm + BwdSmem::k, &tm_qkv, kv_full, ck, kr);
-            tma_load_2d(sm + BwdSmem::k + 16384, &tm_qkv, kv_full, ck + 64, kr);
-            tma_load_2d(sm + BwdSmem::v, &tm_qkv, kv_full, cv, kr);
-            tma_load_2d(sm + BwdSmem::v + 16384, &tm_qkv, kv_full, cv + 64, kr);
-            for (int i = 0; i < nq; ++i) {
-                const int st = i & 1;
-                if (i >= 2) mbar_wait(&q_empty[st], ((i - 2) >> 1) & 1);
-                uint8_t* qs = sm + BwdSmem::q + st * kTile;
-                const int qr = tok0 + (kb + i) * BQ;
-                mbar_expect_tx(&q_full[st], kTile);
-                tma_load_2d(qs, &tm_qkv, &q_full[st], cq, qr);
-                tma_load_2d(qs + 16384, &tm_qkv, &q_full[st], cq + 64, qr);
-            }
-        }
-    } else if (warp == 1) {
-        constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);
-        constexpr uint32_t id_kmn = idesc_bf16(128, 128, false, true);
-        constexpr uint32_t id_mnmn = idesc_bf16(128, 128, true, true);
-        const uint32_t sk = smem_u32(sm + BwdSmem::k), sv = smem_u32(sm + BwdSmem::v);
-        const uint32_t sdst = smem_u32(sm + BwdSmem::dst);
-        auto issue_s = [&](int i) {  // S^T(i) = K Q(i)^T -> [0,128)
-            const uint32_t sq = smem_u32(sm + BwdSmem::q + (i & 1) * kTile);
-            mbar_wait(&q_full[i & 1], (i >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 0, sdesc(sk + o, 16, 1024), sdesc(sq + o, 16, 1024), id_kk, kk != 0);
-                }
-                tc_commit(s_full);
-            }
-            __syncwarp();
-        };
-        auto issue_dp = [&](int i) {  // dP^T(i) = V dO(i)^T -> [128,256)
-            const uint32_t sdo = smem_u32(sm + BwdSmem::dO + (i & 1) * kTile);
-            mbar_wait(&do_full[i & 1], (i >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    tc_mma(tmem + 128, sdesc(sv + o, 16, 1024), sdesc(sdo + o, 16, 1024), id_kk, kk != 0);
-                }
-                tc_commit(dp_full);
-            }
-            __syncwarp();
-        };
-        mbar_wait(kv_full, 0);
-        issue_s(0);
-        issue_dp(0);
-        for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
-            const uint32_t sq = smem_u32(sm + BwdSmem::q + st * kTile);
-            const uint32_t sdo = smem_u32(sm + BwdSmem::dO + st * kTile);
-            mbar_wait(ds_full, i & 1);
-            tc_fence_after();
-            if (lane_id() == 0) ATRACE(i, 8);
-            if (elect_one()) {
-                // dK += dS^T Q : A = dS^T (bf16 pairs over the consumed dP^T columns) from TMEM
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 384, tmem + 128 + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
-                              sdesc(sq + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
-                // dQ = dS K -> [128,256), after dK has read dS^T there (in-order pipe)
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma(tmem + 128, sdesc(sdst + kk * 2048, 16384, 1024), sdesc(sk + kk * 2048, 16384, 1024),
-                           id_mnmn, kk != 0);
-                tc_commit(dq_full);
-                // dV += P^T dO : A = P^T from TMEM (8 bf16-pair columns per K=16 step; queries 0-63 in
-                // columns [0,32), 64-127 in [64,96))
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 256, tmem + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
-                              sdesc(sdo + kk * 2048, 16384, 1024), id_kmn, (i | kk) != 0);
-                tc_commit(qdo_used);  // dO(i), dS^T(i) no longer read
-                tc_commit(&q_empty[st]);  // (Q(i) was last read by dK(i))
-            }
-            __syncwarp();
-            if (i + 1 < nq) {
-                // S^T(i+1) overwrites [0,128) after dV(i) has read P^T there (the MMA pipe runs in issue order)
-                issue_s(i + 1);
-                if (lane_id() == 0) ATRACE(i, 10);
-                mbar_wait(dq_free, i & 1);
-                tc_fence_after();
-                if (lane_id() == 0) ATRACE(i, 9);
-                issue_dp(i + 1);
-            }
-        }
-        if (elect_one()) tc_commit(dkv_full);
-        __syncwarp();
-    } else {
-        const uint32_t q4 = warp & 3;
-        const int hf = int(warp - 2) >> 2;  // query half (columns of S^T) handled by this warp
-        const int r = int(q4 * 32 + lane_id());
-        const uint32_t lane_base = (q4 * 32) << 16;
-        const float sl2 = scale * kLog2e;
-        uint8_t* sdst = sm + BwdSmem::dst;
-        const int key = kb * BK + r;
-        auto lse_of = [&](int qb) {  // this thread's staged value: lse2 (half 0) or D (half 1) of query row r
-            return hf == 0 ? lse2[size_t(head) * T + tok0 + qb * BQ + r] : dsum[size_t(head) * T + tok0 + qb * BQ + r];
-        };
-        sL[hf * 128 + r] = lse_of(kb);
-        bar_sync_compute();
-        for (int i = 0; i < nq; ++i) {
-            const int qb = kb + i;
-            const float* Lb = sL + (i & 1) * 256;
-            const float lnext = i + 1 < nq ? lse_of(qb + 1) : 0.f;  // in flight during this tile
-            if (threadIdx.x == 64) ATRACE(i, 0);
-            mbar_wait(s_full, i & 1);
-            mbar_wait(dp_full, i & 1);
-            tc_fence_after();
-            if (threadIdx.x == 64) ATRACE(i, 1);
-            const bool diag = (qb == kb);
-            // per 32-column chunk of this half: S^T / dP^T -> P^T and dS^T (bf16 pairs) written back over
-            // the chunk's own consumed columns (P^T: half 0 -> [0,32), half 1 -> [64,96); dS^T at +128),
-            // and dS^T to smem (the dQ MMA reads it MN-major)
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                const int c0 = hf * 64 + cc * 32;
-                float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + c0, sv);
-                tmem_ld32(tmem + lane_base + 128 + c0, dp);
-                tmem_ld_wait();
-                if (__builtin_expect(diag, 0)) {  // causal mask on the diagonal tile only
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (key > qb * BQ + c0 + e) sv[e] = -INFINITY;
-                }
-                uint32_t pk[16], dk[16];
-#pragma unroll
-                for (int e2 = 0; e2 < 16; ++e2) {
-                    float pv[2], dsv[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int e = 2 * e2 + u;
-                        const float v = fast_exp2(fmaf(sv[e], sl2, -Lb[c0 + e]));
-                        pv[u] = v;
-                        dsv[u] = v * (dp[e] - Lb[128 + c0 + e]);
-                    }
-                    pk[e2] = pack_bf16(pv[0], pv[1]);
-                    dk[e2] = pack_bf16(dsv[0], dsv[1]);
-                }
-                tmem_st16u(tmem + lane_base + hf * 64 + cc * 16, pk);
-                tmem_st16u(tmem + lane_base + 128 + hf * 64 + cc * 16, dk);
-                if (cc == 0 && i > 0) mbar_wait(ds_buf, (i - 1) & 1);  // dQ(i-1) staging there read out
-#pragma unroll
-                for (int e8 = 0; e8 < 4; ++e8) {
-                    const int col = c0 + e8 * 8;
-                    *reinterpret_cast<uint4*>(sdst + sw128(r, col)) =
-                        make_uint4(dk[4 * e8], dk[4 * e8 + 1], dk[4 * e8 + 2], dk[4 * e8 + 3]);
-                }
-            }
-            tmem_st_wait();
-            fence_async_smem();
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(ds_full);
-            if (threadIdx.x == 64) ATRACE(i, 2);
-            // ---- dQ(i) (thread = query row r, d columns of half hf): TMEM -> registers -> release the
-            // columns -> fp32 smem staged in the tile's consumed Q / dO buffers -> TMA bulk reduce-add
-            mbar_wait(dq_full, i & 1);
-            tc_fence_after();
-            if (threadIdx.x == 64) ATRACE(i, 3);
-            {
-                float v[64];
-                tmem_ld32(tmem + lane_base + 128 + hf * 64, *reinterpret_cast<float(*)[32]>(&v[0]));
-                tmem_ld32(tmem + lane_base + 128 + hf * 64 + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
-                tmem_ld_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane_id() == 0) mbar_arrive(dq_free);  // [128,256) free for dP^T(i+1)
-                if (threadIdx.x == 64) ATRACE(i, 5);
-                mbar_wait(qdo_used, i & 1);               // dK(i) retired: dO(i) / dS^T may be overwritten
-                uint8_t* stage = hf == 0 ? sm + BwdSmem::dO + (i & 1) * kTile : sm + BwdSmem::dst;
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    uint8_t* chunk = stage + cc * 16384 + r * 128;
-#pragma unroll
-                    for (int g = 0; g < 8; ++g)
-                        *reinterpret_cast<float4*>(chunk + ((g ^ (r & 7)) << 4)) =
-                            make_float4(v[cc * 32 + 4 * g], v[cc * 32 + 4 * g + 1], v[cc * 32 + 4 * g + 2],
-                                        v[cc * 32 + 4 * g + 3]);
-                }
-            }
-            fence_async_smem();  // staging writes visible to the TMA reduce
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(dq_staged);
-            if (threadIdx.x == 64) ATRACE(i, 4);
-            if (i + 1 < nq) {
-                sL[((i + 1) & 1) * 256 + hf * 128 + r] = lnext;  // buffer last read by tile i-1
-                bar_sync_compute();
-            }
-        }
-        // dV, dK rows (thread = key row, column half hf)
-        mbar_wait(dkv_full, 0);
-        tc_fence_after();
-        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
-        // folded RMSNorm of the QKV input: dqkv' = rstd1(row) * dqkv (executor.cpp, fold mode)
-        const float fv = rs ? rsqrtf(rs[tok0 + kb * BK + r] * rs_inv_n + rs_eps) : 1.f;
-        const float fk = fv * scale;
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c = hf * 2 + cc;
-            float v[32], k[32];
-            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
-            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
-            tmem_ld_wait();
-            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
-            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                dv[e] = make_uint4(pack_bf16(v[8 * e] * fv, v[8 * e + 1] * fv), pack_bf16(v[8 * e + 2] * fv, v[8 * e + 3] * fv),
-                                   pack_bf16(v[8 * e + 4] * fv, v[8 * e + 5] * fv), pack_bf16(v[8 * e + 6] * fv, v[8 * e + 7] * fv));
-                dk[e] = make_uint4(pack_bf16(k[8 * e] * fk, k[8 * e + 1] * fk),
-                                   pack_bf16(k[8 * e + 2] * fk, k[8 * e + 3] * fk),
-                                   pack_bf16(k[8 * e + 4] * fk, k[8 * e + 5] * fk),
-                                   pack_bf16(k[8 * e + 6] * fk, k[8 * e + 7] * fk));
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_free<512>(tmem);
-    }
-}
-
 // ------------------------------------------------------------------ backward v5 (half-tile pipeline)
-// Same math and CTA decomposition as v4 (CTA per 128-key tile kb, loop over the query rows >= kb),
+// One CTA per (128-key tile kb, head, sequence), looping over the query rows >= kb (as round 1's v4),
 // but the query loop runs in 64-row HALF tiles j with two TMEM buffers, so the tensor pipe computes
 // S^T / dP^T of half tile j+1 while the compute warps form P^T / dS^T of half tile j:
 //   buffer b = j & 1:  [b*128, +64)  S^T_j  (128 keys x 64 queries); after the elementwise phase each
@@ -776,7 +414,9 @@ struct Bwd5Smem {
     static constexpr int stg = ds + 2 * 16384;  // dQ staging: 4 chunks [64 q][32 d] fp32, 8 KB each
     static constexpr int lse = stg + 32768;     // [2][128] floats: lse2[64] | D[64]
     static constexpr int bars = lse + 1024;
-    static constexpr int total = bars + 256 + 512;  // 512 B alignment slack (as BwdSmem)
+    // 512 B of alignment slack: the 227 KB opt-in limit leaves no room for 1 KB; the dynamic window
+    // starts 1 KB-aligned when the kernel has no static shared memory (checked at run time)
+    static constexpr int total = bars + 256 + 512;
 };
 static_assert(Bwd5Smem::total <= 232448, "attn bwd v5: shared memory over the sm_100 opt-in limit");
 
@@ -1345,34 +985,20 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     if (seq % 128) throw std::invalid_argument("attention: seq must be a multiple of 128");
     attn_bwd_pre(dout, out, dsum, dq_acc, heads, batch * seq, s);
     static bool once = [] {
-        cudaFuncSetAttribute(attn_bwd_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::total);
         cudaFuncSetAttribute(attn_bwd_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd5Smem::total);
         return true;
     }();
     (void)once;
-    static const int bver = [] {  // PB_ATTN_BWD=4 selects the full-tile kernel
-        const char* e = std::getenv("PB_ATTN_BWD");
-        return e && e[0] == '4' ? 4 : 5;
-    }();
     const int T = batch * seq;
     const CUtensorMap tq = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 128);
+    const CUtensorMap tq64 = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 64);
+    const CUtensorMap td64 = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 64);
+    const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
+                                       uint64_t(heads) * D, 32, 64);
     static unsigned long long* trace = trace_buffer("PB_ATTN_TRACE");
-    if (bver == 5) {
-        const CUtensorMap tq64 = make_map(qkv, uint64_t(3) * heads * D, uint64_t(T), uint64_t(3) * heads * D, 64, 64);
-        const CUtensorMap td64 = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 64);
-        const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D,
-                                           uint64_t(T), uint64_t(heads) * D, 32, 64);
-        launch_k(attn_bwd_tc5_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), Bwd5Smem::total, s, 1, tq,
-                 tq64, td64, tdq, lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs,
-                 rs_inv_n, rs_eps);
-    } else {
-        const CUtensorMap td = make_map(dout, uint64_t(heads) * D, uint64_t(T), uint64_t(heads) * D, 64, 128);
-        const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D,
-                                           uint64_t(T), uint64_t(heads) * D, 32, 128);
-        launch_k(attn_bwd_tc4_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), BwdSmem::total, s, 1, tq,
-                 td, tdq, lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs,
-                 rs_inv_n, rs_eps);
-    }
+    launch_k(attn_bwd_tc5_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), Bwd5Smem::total, s, 1, tq, tq64,
+             td64, tdq, lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs, rs_inv_n,
+             rs_eps);
     trace_dump(trace, "attn_bwd", s);
     attn_dq_store(dq_acc, dqkv, heads, T, s, rs, rs_inv_n, rs_eps);
 }
