@@ -97,14 +97,32 @@ def main():
     ap.add_argument("--latency-us", type=float, default=8.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--svg-prefix", default=None)
+    ap.add_argument("--layers", type=int, default=None,
+                    help="override the layer count; the LM-head stage takes the remainder (ceil split), e.g. 31 = "
+                         "2 per V stage + 1 on the LM-head stage at p=8")
+    ap.add_argument("--balance", action="store_true", help="balanced_stage_layers: fewer layers on the LM-head stage")
     args = ap.parse_args()
 
     import torch
 
     from paper_2405_15362_b200 import pipeblock as pb
-    from paper_2405_15362_b200.executor import ModelConfig, synthetic_batch
+    from paper_2405_15362_b200.executor import ModelConfig, balanced_stage_layers, synthetic_batch
 
-    cfg = ModelConfig(**CONFIGS[args.model], micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    mcfg = dict(CONFIGS[args.model])
+    if args.layers:
+        mcfg["layers"] = args.layers
+    cfg0 = ModelConfig(**mcfg, micro_batch=args.micro_batch, optimizer=True, timeline=True)
+    cfg = cfg0
+
+    def split_for(topology):
+        """Stage layers for this schedule's topology: balanced, the ceil split of --layers, or even."""
+        S = topology.num_stages
+        if args.balance:
+            return tuple(balanced_stage_layers(cfg0, topology))
+        if args.layers and args.layers % S:
+            per = -(-args.layers // S)
+            return tuple([per] * (S - 1) + [args.layers - per * (S - 1)])
+        return None
     m, p, T = args.microbatches, args.p, cfg.tokens_per_microbatch
     tokens, labels = synthetic_batch(cfg, m)
     tok, lab = torch.from_numpy(tokens).cuda(), torch.from_numpy(labels).cuda()
@@ -114,8 +132,12 @@ def main():
            "method": "PB_FLAG_SOLO device probes of every pipeline device (tools/device_probe.py), per-pass "
                      "CUDA-event durations replayed with pb_replay", "schedules": {}, "growth": [], "search": []}
     profiles = {}
+    out["layers"] = cfg0.layers
+    out["stage_layers"] = {}
     for name in args.schedules:
         sched = pb.assemble(pb.build_entry(name, p), m)
+        cfg = dataclasses.replace(cfg0, stage_layers=split_for(sched.topology))
+        out["stage_layers"][name] = list(cfg.stage_layers) if cfg.stage_layers else None
         run = probe_schedule(cfg, sched, name, list(range(1, p + 1)), tok, lab, 1, comm_ms)
         if "durations" not in run:
             out["schedules"][name] = {"all_fit": False, "devices": [{k: v for k, v in r.items() if k != "passes"}
@@ -161,6 +183,7 @@ def main():
                 ent.update({"best": r.best.str(), "predicted_bubble_eval_n": r.bubble_rate,
                             "exact_peak_m": r.exact_peak})
                 sched = pb.search_assemble(p, r.best, m)
+                cfg = dataclasses.replace(cfg0, stage_layers=split_for(sched.topology))
                 run = probe_schedule(cfg, sched, "search", list(range(1, p + 1)), tok, lab, 1, comm_ms)
                 if "durations" in run:
                     ent.update({k: run[k] for k in ("projected_tokens_per_s", "bubble_rate", "max_activation_gib",
