@@ -6,6 +6,7 @@ bf16-valued weights and tokens.
   * GPT-1.5B slice: h=2048, 16 heads, s=2048, V=50304, mbs=2, 4 layers, V-Half p=2
   * GPT-6B slice:   h=4096, 32 heads, s=4096, V=50304, mbs=1, 4 layers, V-ZB p=2 (and 1F1B p=2)
   * GPT-14B slice:  h=6144, 48 heads, s=6144, V=50304, mbs=1, 5 layers split (2,1,1,1), V-Min p=2
+  * round 2: 14B V-Half p=2; 6B ZB-H1 p=2 with an uneven (3, 2) split; 1.5B interleaved-1F1B p=2 (looped)
 
 The big slices run the oracle's fp32 restatement on the GPU (oracle.numerics.reference_step,
 device="cuda", TF32 off): the same arithmetic, minutes faster than host cores.  Tolerances are
@@ -38,6 +39,13 @@ SLICES = {
                             optimizer=False), "1f1b", 2, 3, "cuda"),
     "14b": (ModelConfig(layers=5, hidden=6144, heads=48, seq=6144, vocab=50304, micro_batch=1, optimizer=False,
                         stage_layers=(2, 1, 1, 1)), "v-min", 2, 3, "cuda"),
+    # round 2: the other schedule families at real layer shapes
+    "14b-v-half": (ModelConfig(layers=4, hidden=6144, heads=48, seq=6144, vocab=50304, micro_batch=1,
+                               optimizer=False), "v-half", 2, 4, "cuda"),
+    "6b-zb-h1-uneven": (ModelConfig(layers=5, hidden=4096, heads=32, seq=4096, vocab=50304, micro_batch=1,
+                                    optimizer=False, stage_layers=(3, 2)), "zb-h1", 2, 4, "cuda"),
+    "1.5b-interleaved": (ModelConfig(layers=4, hidden=2048, heads=16, seq=2048, vocab=50304, micro_batch=2,
+                                     optimizer=False), "interleaved-1f1b", 2, 4, "cuda"),
 }
 
 
