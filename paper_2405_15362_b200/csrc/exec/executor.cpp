@@ -122,7 +122,7 @@ void Exec::build_layout() {
             }
             L.ssf = L.ss + size_t(2 * Lc) * T * 4;
         }
-        if (s == S) {  // LM-head buffers live in their own lifespan pool (head slots, see constructor)
+        if (is_last(s)) {  // LM-head buffers live in their own lifespan pool (head slots, see constructor)
             size_t hc = 0;
             if (!fold) {
                 L.hf = add(hc, Th * 2);
@@ -149,7 +149,7 @@ void Exec::build_params() {
     const float std_in = 0.02f, std_out = 0.02f / std::sqrt(2.f * cfg.layers);
     for (int s : stages) {
         StageParams sp;
-        if (s == 1) sp.emb = add("s1.emb", size_t(V) * h, 1, std_in, 0.f);
+        if (is_first(s)) sp.emb = add("s" + std::to_string(s) + ".emb", size_t(V) * h, 1, std_in, 0.f);
         for (int l = 0; l < stage_L[s]; ++l) {
             const int gl = stage_first[s] + l;
             const std::string pre = "s" + std::to_string(s) + ".l" + std::to_string(l) + ".";
@@ -162,7 +162,7 @@ void Exec::build_params() {
             lp.w2 = add(pre + "w2", size_t(4) * h * h, 16 + gl * 8 + 5, std_out, 0.f);
             sp.layers.push_back(lp);
         }
-        if (s == S) {
+        if (is_last(s)) {
             sp.gf = add("s" + std::to_string(s) + ".norm", h, 2, 0.f, 1.f);
             sp.head = add("s" + std::to_string(s) + ".head", size_t(V) * h, 3, std_in, 0.f);
         }
@@ -184,22 +184,30 @@ Exec::Exec(const pb_model_cfg& c, const vsched::Grid& grid, int device, int cuda
 void Exec::init(int device) {
     if (device < 1 || device > plan.topo.devices) throw std::invalid_argument("device out of range");
     S = plan.topo.num_stages;
+    twin = !plan.topo.default_routes();  // make_plan admits only the gems / chimera twin besides
+    Sm = twin ? S / 2 : S;
     stage_L.assign(size_t(S) + 1, 0);
     stage_first.assign(size_t(S) + 2, 0);
+    std::vector<int> model_L(size_t(Sm) + 1, 0), model_first(size_t(Sm) + 2, 0);
     if (cfg.stage_layers) {
+        if (twin) throw std::invalid_argument("stage_layers: not supported with replicated-weight (twin) schedules");
         int sum = 0;
         for (int s = 1; s <= S; ++s) {
-            stage_L[s] = cfg.stage_layers[s - 1];
-            if (stage_L[s] < 1) throw std::invalid_argument("stage_layers: every stage needs >= 1 layer");
-            sum += stage_L[s];
+            model_L[s] = cfg.stage_layers[s - 1];
+            if (model_L[s] < 1) throw std::invalid_argument("stage_layers: every stage needs >= 1 layer");
+            sum += model_L[s];
         }
         if (sum != cfg.layers) throw std::invalid_argument("stage_layers must sum to layers");
         cfg.stage_layers = nullptr;  // copied
     } else {
-        if (cfg.layers % S) throw std::invalid_argument("layers must be a multiple of the stage count");
-        for (int s = 1; s <= S; ++s) stage_L[s] = cfg.layers / S;
+        if (cfg.layers % Sm) throw std::invalid_argument("layers must be a multiple of the stage count");
+        for (int s = 1; s <= Sm; ++s) model_L[s] = cfg.layers / Sm;
     }
-    for (int s = 1; s <= S; ++s) stage_first[s + 1] = stage_first[s] + stage_L[s];
+    for (int s = 1; s <= Sm; ++s) model_first[s + 1] = model_first[s] + model_L[s];
+    for (int s = 1; s <= S; ++s) {  // a replica stage holds its model stage's layers (same init ids)
+        stage_L[s] = model_L[model_stage(s)];
+        stage_first[s] = model_first[model_stage(s)];
+    }
     h = cfg.hidden;
     H = cfg.heads;
     V = cfg.vocab;
@@ -258,6 +266,11 @@ void Exec::init(int device) {
     grads = static_cast<float*>(dmalloc(n_params * 4, "grads"));
     adam_m = static_cast<float*>(dmalloc(n_params * 4, "adam"));
     adam_v = static_cast<float*>(dmalloc(n_params * 4, "adam"));
+    if (twin) {  // receive buffer for the replica device's gradient arena (same size: same model stages)
+        rtmp = static_cast<float*>(dmalloc(n_params * 4, "replica grads"));
+        const int s0 = stages.front();
+        replica_dev = plan.topo.device_of(s0 > Sm ? s0 - Sm : s0 + Sm);
+    }
     ck(cudaMemsetAsync(grads, 0, n_params * 4, cs), "memset");
     ck(cudaMemsetAsync(adam_m, 0, n_params * 4, cs), "memset");
     ck(cudaMemsetAsync(adam_v, 0, n_params * 4, cs), "memset");
@@ -275,7 +288,7 @@ void Exec::init(int device) {
                 folds.push_back({lp.w1, lp.g2, 4 * h, h, off});
                 off += align_up(size_t(4) * h * h, 64);
             }
-            if (s == S) {
+            if (is_last(s)) {
                 folds.push_back({P.head, P.gf, V, h, off});
                 off += align_up(size_t(V) * h, 64);
             }
@@ -293,11 +306,11 @@ void Exec::init(int device) {
     // coloured like the main pool but over stage S alone — a V device holding stages 1 and 2p
     // does not pay the logits in every one of its slots
     head_slot_mb.assign(size_t(m), -1);
-    if (std::find(stages.begin(), stages.end(), S) != stages.end()) {
+    if (std::any_of(stages.begin(), stages.end(), [&](int st) { return is_last(st); })) {
         std::vector<bool> busy;
         for (int i : plan.dev_ops[dev]) {
             const auto& o = plan.ops[size_t(i)].op;
-            if (o.stage != S) continue;
+            if (!is_last(o.stage)) continue;
             if (o.kind == vsched::Kind::F) {
                 int k = 0;
                 while (k < int(busy.size()) && busy[k]) ++k;
@@ -550,7 +563,7 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
     const StageLayout& L = layout.at(s);
     const StageParams& P = sparams.at(s);
     __nv_bfloat16* x0 = bf(slot, L.x[0]);
-    if (s == 1) {
+    if (is_first(s)) {
         timed("embed_fwd", [&] { pbk::embed_fwd(tokens + size_t(mb) * T, wts + ptensors[P.emb].off, x0, T, h, V, id_err(), cs); });
         ++launches;
     }
@@ -567,9 +580,9 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         const auto& y = L.layer[l];
         const auto& w = P.layers[l];
         __nv_bfloat16* x = bf(slot, L.x[l]);
-        __nv_bfloat16* xo = (l == Lc - 1 && s < S) ? out : bf(slot, L.x[l + 1]);
+        __nv_bfloat16* xo = (l == Lc - 1 && !is_last(s)) ? out : bf(slot, L.x[l + 1]);
         if (fold) {
-            float* ss_next = l + 1 < Lc ? f32(slot, L.layer[l + 1].ss1) : (s == S ? f32(slot, L.ssf) : nullptr);
+            float* ss_next = l + 1 < Lc ? f32(slot, L.layer[l + 1].ss1) : (is_last(s) ? f32(slot, L.ssf) : nullptr);
             gemm(T, 3 * h, h, x, false, W(w.wqkv), false, bf(slot, y.qkv), pbk::EPI_STORE, nullptr, nullptr, 0,
                  f32(slot, y.ss1));
             timed("attn_fwd", [&] { pbk::attn_fwd_tc(bf(slot, y.qkv), bf(slot, y.o), f32(slot, y.lse), mbs, seq, H, cs); });
@@ -592,7 +605,7 @@ void Exec::pass_forward(int s, int mb, int slot, __nv_bfloat16* out) {
         gemm(T, h, 4 * h, bf(slot, y.gl), false, W(w.w2), false, xo, pbk::EPI_RESID, bf(slot, y.x1));
         launches += 3;
     }
-    if (s == S) {
+    if (is_last(s)) {
         const float scale = 1.f / float(size_t(m) * T);
         if (fold) {
             gemm(T, V, h, bf(slot, L.x[Lc]), false, W(P.head), false, HB(mb, L.logits), pbk::EPI_STORE, nullptr,
@@ -620,7 +633,7 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         // Fold mode runs every normalised projection's backward on row-scaled output gradients
         // (dY' = rstd * dY: the CE kernel, the dGELU epilogue and the attention backward apply it), so
         // the dX GEMMs yield rstd * dX-hat and the weight GEMMs use the stored x: dW' = dY'^T x.
-        if (s == S) {
+        if (is_last(s)) {
             gemm(T, h, V, HB(mb, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
             timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd_x(scratch, bf(slot, L.x[Lc]), f32(slot, L.ssf), nullptr, bf(slot, L.dx[Lc]), T, h, kNormEps, cs); });
             ++launches;
@@ -629,7 +642,7 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
             const auto& y = L.layer[l];
             const auto& w = P.layers[l];
             __nv_bfloat16* dy = bf(slot, L.dx[l + 1]);
-            __nv_bfloat16* dxo = (l == 0 && s > 1) ? out : bf(slot, L.dx[l]);
+            __nv_bfloat16* dxo = (l == 0 && !is_first(s)) ? out : bf(slot, L.dx[l]);
             // du' = rstd2 * (dy . W2) * gelu'(u), written over u
             gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u), nullptr, 0,
                  f32(slot, y.ss2));
@@ -646,7 +659,7 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         }
         return;
     }
-    if (s == S) {
+    if (is_last(s)) {
         // dhf = dlogits . Whead ; dx_L = rmsnorm_bwd(dhf)
         gemm(T, h, V, HB(mb, L.logits), false, W(P.head), true, scratch, pbk::EPI_STORE);
         timed("rmsnorm_bwd", [&] { pbk::rmsnorm_bwd(scratch, bf(slot, L.x[Lc]), W(P.gf), HF(mb, L.rstdf), nullptr, bf(slot, L.dx[Lc]), T, h,
@@ -658,7 +671,7 @@ void Exec::pass_backward(int s, int mb, int slot, __nv_bfloat16* out) {
         const auto& y = L.layer[l];
         const auto& w = P.layers[l];
         __nv_bfloat16* dy = bf(slot, L.dx[l + 1]);
-        __nv_bfloat16* dxo = (l == 0 && s > 1) ? out : bf(slot, L.dx[l]);
+        __nv_bfloat16* dxo = (l == 0 && !is_first(s)) ? out : bf(slot, L.dx[l]);
         // du = (dy . W2) * gelu'(u), written over u
         gemm(T, 4 * h, h, dy, false, W(w.w2), true, bf(slot, y.u), pbk::EPI_DGELU, bf(slot, y.u));
         gemm(T, h, 4 * h, bf(slot, y.u), false, W(w.w1), true, scratch, pbk::EPI_STORE);
@@ -690,10 +703,10 @@ void Exec::pass_weight(int s, int mb, int slot) {
         gemm(h, h, T, bf(slot, y.dx1), true, bf(slot, y.o), true, G(w.wo), pbk::EPI_F32, nullptr, nullptr, 1);
         gemm(3 * h, h, T, bf(slot, y.dqkv), true, bf(slot, fold ? L.x[l] : y.a), true, GW(w.wqkv), pbk::EPI_F32, nullptr, nullptr, 1);
     }
-    if (s == S)
+    if (is_last(s))
         gemm(V, h, T, HB(mb, L.logits), true, fold ? bf(slot, L.x[Lc]) : HB(mb, L.hf), true, GW(P.head), pbk::EPI_F32,
              nullptr, nullptr, 1);
-    if (s == 1) {
+    if (is_first(s)) {
         timed("embed_bwd", [&] { pbk::embed_bwd(tokens + size_t(mb) * T, bf(slot, L.dx[0]), G(P.emb), T, h, V, id_err(), cs); });
         ++launches;
     }
@@ -734,8 +747,8 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     // step's last users (W passes read dx.back(), F-input slots whose first use has free_op < 0) may
     // still be reading on the compute stream — start the copy stream after everything enqueued so far
     ck(cudaStreamWaitEvent(xs, ev_step0, 0), "wait");
-    const bool has_first = std::find(stages.begin(), stages.end(), 1) != stages.end();
-    const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
+    const bool has_first = std::any_of(stages.begin(), stages.end(), [&](int st) { return is_first(st); });
+    const bool has_last = std::any_of(stages.begin(), stages.end(), [&](int st) { return is_last(st); });
     if (on_host) {  // ids index the embedding / logits: reject out-of-range ids before anything is enqueued
         auto check = [&](const int32_t* ids, const char* what) {
             for (size_t i = 0; i < size_t(m) * T; ++i)
@@ -868,6 +881,7 @@ void Exec::enqueue(const int32_t* tok, const int32_t* lab, bool on_host) {
     if (isolate && group)  // keep the optimizer off the isolated pass window
         group->wait([&] { return group->iso_step == t && group->iso_done == int64_t(plan.ops.size()); });
     if (fold) timed("fold_grad", [&] { fold_grads(); });
+    if (twin && !solo) sync_replicas(t);  // data-parallel replicas: every copy gets the summed gradient
     if (cfg.optimizer) {
         ++adam_step;
         timed("adamw", [&] {
@@ -913,7 +927,7 @@ void Exec::finish(pb_timed_pass* tl, size_t tl_n, pb_exec_stats* st) {
     if (reinterpret_cast<const int32_t*>(loss_host)[1])
         throw std::invalid_argument("token or label id outside [0, " + std::to_string(V) + ") in the step's device inputs");
     const auto& ops = plan.dev_ops[dev];
-    const bool has_last = std::find(stages.begin(), stages.end(), S) != stages.end();
+    const bool has_last = std::any_of(stages.begin(), stages.end(), [&](int st) { return is_last(st); });
     double busy = 0;
     if (timeline) {
         if (tl && tl_n < ops.size()) throw Space("timeline buffer too small");
@@ -981,6 +995,10 @@ LocalGroup::~LocalGroup() {
     for (int b = 0; b < 2; ++b) {
         for (auto e : ready_ev[b]) cudaEventDestroy(e);
         for (auto e : ack_ev[b]) cudaEventDestroy(e);
+        for (auto e : gdone_ev[b])
+            if (e) cudaEventDestroy(e);
+        for (auto e : gcopied_ev[b])
+            if (e) cudaEventDestroy(e);
     }
 }
 
@@ -1007,6 +1025,21 @@ std::shared_ptr<LocalGroup> make_group(const std::vector<Exec*>& all) {
     g->ack_step.assign(n, -1);
     g->enqueued.assign(size_t(p.topo.devices) + 1, 0);
     for (Exec* e : all) g->enqueued[e->dev] = e->steps_done;
+    g->execs.assign(size_t(p.topo.devices) + 1, nullptr);
+    for (Exec* e : all) g->execs[size_t(e->dev)] = e;
+    if (all.front()->twin) {
+        for (int b = 0; b < 2; ++b) {
+            g->gdone_ev[b].assign(size_t(p.topo.devices) + 1, nullptr);
+            g->gcopied_ev[b].assign(size_t(p.topo.devices) + 1, nullptr);
+            for (Exec* e : all) {
+                ck(cudaSetDevice(e->cuda), "cudaSetDevice");
+                ck(cudaEventCreateWithFlags(&g->gdone_ev[b][size_t(e->dev)], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&g->gcopied_ev[b][size_t(e->dev)], cudaEventDisableTiming), "event");
+            }
+        }
+        g->gdone_step.assign(size_t(p.topo.devices) + 1, -1);
+        g->gcopied_step.assign(size_t(p.topo.devices) + 1, -1);
+    }
     return g;
 }
 
@@ -1028,7 +1061,51 @@ void Exec::connect_local(const std::vector<Exec*>& all, std::shared_ptr<LocalGro
             cudaGetLastError();
         }
     }
+    if (twin) {  // pair every local tensor "s<s>.<rest>" with "s<partner>.<rest>" on the replica device
+        const Exec* peer = nullptr;
+        for (Exec* e : all)
+            if (e->dev == replica_dev) peer = e;
+        if (!peer) throw std::invalid_argument("connect: replica device missing");
+        std::map<std::string, const PTensor*> by_name;
+        for (const auto& q : peer->ptensors) by_name[q.name] = &q;
+        replica_map.clear();
+        for (const auto& q : ptensors) {
+            const size_t dot = q.name.find('.');
+            const int s = std::stoi(q.name.substr(1, dot - 1));
+            const int ps = s > Sm ? s - Sm : s + Sm;
+            auto it = by_name.find("s" + std::to_string(ps) + q.name.substr(dot));
+            if (it == by_name.end() || it->second->numel != q.numel)
+                throw std::invalid_argument("connect: replica of " + q.name + " not found");
+            replica_map.push_back({q.off, it->second->off, q.numel});
+        }
+    }
     connected = true;
+}
+
+// Twin topologies: the two copies of every model stage sum their gradients before the optimizer
+// (gems / chimera train two weight replicas data-parallel).  Host-ordered like the message events:
+// record "gradients final" -> pull the replica device's arena -> record "pulled" -> wait until the
+// replica device has pulled ours -> add its arena into ours, tensor by tensor.
+void Exec::sync_replicas(int64_t t) {
+    if (!group) throw StateError("replicated-weight schedules need an in-process pipeline (connect_local)");
+    const size_t b = size_t(t & 1), me = size_t(dev), pd = size_t(replica_dev);
+    const Exec* peer = group->execs[pd];
+    ck(cudaEventRecord(group->gdone_ev[b][me], cs), "event");
+    group->set(group->gdone_step, me, t);
+    group->wait([&] { return group->gdone_step[pd] >= t; });
+    ck(cudaStreamWaitEvent(cs, group->gdone_ev[b][pd], 0), "wait");
+    if (peer->cuda == cuda)
+        ck(cudaMemcpyAsync(rtmp, peer->grads, n_params * 4, cudaMemcpyDeviceToDevice, cs), "replica copy");
+    else
+        ck(cudaMemcpyPeerAsync(rtmp, cuda, peer->grads, peer->cuda, n_params * 4, cs), "replica copy");
+    ck(cudaEventRecord(group->gcopied_ev[b][me], cs), "event");
+    group->set(group->gcopied_step, me, t);
+    group->wait([&] { return group->gcopied_step[pd] >= t; });
+    ck(cudaStreamWaitEvent(cs, group->gcopied_ev[b][pd], 0), "wait");
+    timed("replica_sync", [&] {
+        for (const auto& r : replica_map) pbk::grad_add(grads + r[0], rtmp + r[1], r[2], cs);
+    });
+    launches += int64_t(replica_map.size());
 }
 
 struct IpcBlob {
@@ -1065,6 +1142,9 @@ size_t Exec::export_blob(void* buf, size_t cap) {
 
 void Exec::connect_ipc(const std::vector<std::pair<const void*, size_t>>& blobs) {
     if (connected) throw StateError("connect_ipc: already connected");
+    if (twin)
+        throw std::invalid_argument(
+            "connect_ipc: replicated-weight (twin: gems / chimera) schedules run with in-process pipelines only");
     if (int(blobs.size()) != plan.topo.devices) throw std::invalid_argument("connect_ipc: need one blob per device");
     ck(cudaSetDevice(cuda), "cudaSetDevice");
     // validate everything before mapping anything: each device 1..D exactly once, same plan

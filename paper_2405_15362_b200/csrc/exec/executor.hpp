@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <condition_variable>
 #include <functional>
 #include <map>
@@ -57,6 +58,8 @@ struct Peer {
     bool ipc = false;
 };
 
+class Exec;
+
 // In-process peer group: message hand-off through CUDA events whose records are
 // host-ordered before any wait on them (double-buffered by step parity), so no
 // stream ever waits on work that is not yet submitted.
@@ -66,6 +69,10 @@ struct LocalGroup {
     std::vector<cudaEvent_t> ready_ev[2], ack_ev[2];  // per message
     std::vector<int64_t> ready_step, ack_step;        // last step whose record is enqueued
     std::vector<int64_t> enqueued;                    // per device: steps fully enqueued
+    // twin topologies (gems / chimera): replica-gradient exchange at the end of a step, per device
+    std::vector<Exec*> execs;                         // [device]
+    std::vector<cudaEvent_t> gdone_ev[2], gcopied_ev[2];
+    std::vector<int64_t> gdone_step, gcopied_step;
     // PB_FLAG_ISOLATE: one pass at a time on the whole group (GPU token), passes done this step
     std::mutex iso_mu;
     int64_t iso_step = -1, iso_done = 0;
@@ -101,6 +108,20 @@ class Exec {
     int dev, cuda;
     int S = 0, T = 0, h = 0, H = 0, V = 0, seq = 0, mbs = 0, m = 0;
     std::vector<int> stage_L, stage_first;  // [stage] layers held, global index of its first layer
+    // twin topology (gems / chimera): stages d+k replicate model stage k (weights, init, names' layers);
+    // the first / last stage of each route carries the embedding / LM head
+    bool twin = false;
+    int Sm = 0;  // model stages (S, or d for twin)
+    int model_stage(int s) const { return twin && s > Sm ? s - Sm : s; }
+    bool is_first(int s) const { return model_stage(s) == 1; }
+    bool is_last(int s) const { return model_stage(s) == Sm; }
+    // replica gradients: the device holding the replicas of this device's stages, the (dst, src, n)
+    // element ranges that pair each local tensor with its replica in that device's arena, and a
+    // receive buffer for the replica's gradient arena
+    int replica_dev = 0;
+    std::vector<std::array<size_t, 3>> replica_map;
+    float* rtmp = nullptr;
+    void sync_replicas(int64_t t);
     std::vector<int> stages;
     std::vector<PTensor> ptensors;
     float *master = nullptr, *grads = nullptr, *adam_m = nullptr, *adam_v = nullptr;

@@ -14,7 +14,12 @@ ExecPlan make_plan(const vsched::Grid& g) {
     p.topo = g.topo;
     p.microbatches = g.microbatches;
     const int D = g.topo.devices, S = g.topo.num_stages;
-    if (!g.topo.default_routes()) throw std::invalid_argument("executor: only single-route topologies are supported");
+    // single-route topologies (straight, V, looped) and the two-route twin of gems / chimera
+    // (model.hpp:93-107: route 0 = stages 1..d, route 1 = stages d+1..2d over replicated weights)
+    const bool twin = g.topo.routes.size() == 2 && g.topo.routes[0] == vsched::Topology::iota(1, S / 2) &&
+                      g.topo.routes[1] == vsched::Topology::iota(S / 2 + 1, S);
+    if (!g.topo.default_routes() && !twin)
+        throw std::invalid_argument("executor: only single-route and twin (gems / chimera) topologies are supported");
     for (int s = 1; s <= S; ++s)
         if (g.topo.mem_of(s) != 1.0) throw std::invalid_argument("executor: stage_mem must be 1.0 for every stage");
 
@@ -63,7 +68,11 @@ ExecPlan make_plan(const vsched::Grid& g) {
         p.slots[d] = int(busy.size());
     }
 
-    // messages: F(s)->F(s+1) and B(s)->B(s-1); consumer found by identity
+    // messages: F(s)->F(next stage on the microbatch's route) and B(s)->B(previous); consumer found by identity
+    auto route_end = [&](int stage, int mb, bool want_last) {
+        const auto& r = g.topo.route_for(mb);
+        return want_last ? stage == r.back() : stage == r.front();
+    };
     auto find = [&](int stage, int cls, int mb) {
         auto it = at.find({stage, cls, mb});
         if (it == at.end()) throw std::invalid_argument("executor: schedule misses a pass on the route");
@@ -78,8 +87,9 @@ ExecPlan make_plan(const vsched::Grid& g) {
         for (int i : p.dev_ops[d]) {
             const auto& o = g.ops[i];
             int cons = -1;
-            if (o.kind == Kind::F && o.stage < S) cons = find(o.stage + 1, 0, o.mb);
-            if ((o.kind == Kind::B || o.kind == Kind::BW) && o.stage > 1) cons = find(o.stage - 1, 1, o.mb);
+            if (o.kind == Kind::F && !route_end(o.stage, o.mb, true)) cons = find(o.stage + 1, 0, o.mb);
+            if ((o.kind == Kind::B || o.kind == Kind::BW) && !route_end(o.stage, o.mb, false))
+                cons = find(o.stage - 1, 1, o.mb);
             if (cons < 0) continue;
             int k = 0;
             while (k < int(busy_until.size()) && busy_until[k] > o.start) ++k;

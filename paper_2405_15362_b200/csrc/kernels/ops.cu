@@ -466,6 +466,26 @@ void rmsnorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfl
     launch_k(rmsnorm_bwd_kernel, dim3(T), dim3(h / 8), 0, s, 1, dy, x, g, rstd, dres, dx, T, h);
 }
 
+// dst[i] += src[i] (fp32, both 16-byte aligned): replica gradients of the twin topologies
+__global__ void grad_add_kernel(float* __restrict__ dst, const float* __restrict__ src, size_t n4) {
+    pdl_wait();
+    pdl_launch();
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) {
+        float4 a = reinterpret_cast<float4*>(dst)[i];
+        const float4 b = reinterpret_cast<const float4*>(src)[i];
+        a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+        reinterpret_cast<float4*>(dst)[i] = a;
+    }
+}
+
+void grad_add(float* dst, const float* src, size_t n, cudaStream_t s) {
+    if (n % 4 || (reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) % 16)
+        throw std::invalid_argument("grad_add: 16-byte aligned float4 ranges expected");
+    const size_t n4 = n / 4;
+    const unsigned blocks = unsigned(std::min<size_t>((n4 + 255) / 256, 148 * 8));
+    launch_k(grad_add_kernel, dim3(blocks), dim3(256), 0, s, 1, dst, src, n4);
+}
+
 void row_sumsq(const __nv_bfloat16* x, float* ss, int T, int h, cudaStream_t s) {
     if (h % 128 || h > 8192) throw std::invalid_argument("row_sumsq: h must be a multiple of 128 and <= 8192");
     launch_k(row_sumsq_kernel, dim3((T + 3) / 4), dim3(4 * (h / 128)), 0, s, 1, x, ss, T, h);

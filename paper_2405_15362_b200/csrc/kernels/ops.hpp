@@ -45,6 +45,8 @@ void cross_entropy(__nv_bfloat16* logits, const int32_t* labels, float* loss, in
                    cudaStream_t s, const float* rs = nullptr, float rs_inv_n = 0.f, float rs_eps = 0.f);
 // folded RMSNorm (executor fold mode): ss[row] = sum_c x^2 ; and the backward
 // dx = dyp - x * rstd^2 * mean(dyp * x) + dres (dres may be null), rstd = rsqrt(ss / h + eps)
+// dst[0, n) += src[0, n) (fp32; n % 4 == 0, 16-byte aligned)
+void grad_add(float* dst, const float* src, size_t n, cudaStream_t s);
 void row_sumsq(const __nv_bfloat16* x, float* ss, int T, int h, cudaStream_t s);
 void rmsnorm_bwd_x(const __nv_bfloat16* dyp, const __nv_bfloat16* x, const float* ss, const __nv_bfloat16* dres,
                    __nv_bfloat16* dx, int T, int h, float eps, cudaStream_t s);

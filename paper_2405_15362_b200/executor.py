@@ -286,7 +286,10 @@ class PipelineExecutor:
         tl = [p for dv in sorted(results) for p in results[dv][0]]
         stats = {dv: results[dv][1] for dv in results}
         sim = pb.account(self.schedule.topology, tl) if tl else None
-        return PipelineResult(stats[self.last.device].loss, tl, stats, sim)
+        # every device holding a route's last stage reports its microbatches' share of the mean loss
+        # (one device for single-route schedules, two for the gems / chimera twin)
+        losses = [st.loss for st in stats.values() if st.loss == st.loss]
+        return PipelineResult(float(sum(losses)) if losses else float("nan"), tl, stats, sim)
 
     def set_flags(self, **kw) -> None:
         for x in self.devices:

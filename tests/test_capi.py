@@ -52,14 +52,24 @@ def test_no_gpu_executor_fails_loudly():
     lib.pb_schedule_destroy(h)
 
 
-def test_executor_rejects_replicated_weight_blocks():
-    """gems / chimera route microbatches over two weight replicas (twin topology, gallery.hpp:252-326):
-    generated and analysed bit-exactly, but the executor runs single-route models only."""
+def test_twin_plans_follow_routes():
+    """gems / chimera route microbatches over two weight replicas (twin topology, gallery.hpp:252-326,
+    model.hpp:93-107): the execution plan sends F / B messages along each microbatch's route only —
+    nothing crosses from the end of route 0 (stage d) into route 1 (stage d+1) or back."""
+    from tests.test_multirank_cpu import device_plan
     from paper_2405_15362_b200 import pipeblock as pb
-    from paper_2405_15362_b200._lib import ScheduleError
-    from paper_2405_15362_b200.executor import DeviceExecutor, ModelConfig
-    cfg = ModelConfig(layers=8, hidden=256, heads=2, seq=256, vocab=1024)
-    for e in ("gems", "chimera"):
-        sched = pb.assemble(pb.build_entry(e, 2), 4)
-        with pytest.raises(ScheduleError, match="single-route"):
-            DeviceExecutor(cfg, sched, 1, 0)
+    for e, d in (("gems", 2), ("chimera", 2), ("chimera", 4)):
+        sched = pb.assemble(pb.build_entry(e, d), 4)
+        topo = sched.topology
+        for dev in range(1, d + 1):
+            ops, slots, _ = device_plan(sched, dev)
+            for o in ops:
+                route = list(range(1, d + 1)) if o["mb"] % 2 == 0 else list(range(d + 1, 2 * d + 1))
+                assert o["stage"] in route, (e, o)
+                pos = route.index(o["stage"])
+                if o["kind"] == "F":  # to the next stage of the route, none from the route's last stage
+                    nxt = route[pos + 1] if pos + 1 < d else None
+                    assert o["send_to"] == (topo.device_of(nxt) if nxt else 0), (e, o)
+                if o["kind"] in ("B", "BW"):  # back to the previous stage, none from the route's first
+                    prv = route[pos - 1] if pos > 0 else None
+                    assert o["send_to"] == (topo.device_of(prv) if prv else 0), (e, o)

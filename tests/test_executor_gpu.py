@@ -321,3 +321,61 @@ def test_search_winner_from_measured_profile_matches_oracle():
     peaks = pb.exact_peak(sched)
     for d, st in res.per_device.items():
         assert st.pool_slots == int(peaks[d - 1])
+
+
+@pytest.mark.parametrize("entry,p,m", [("gems", 2, 4), ("chimera", 2, 4), ("chimera", 4, 8), ("gems", 3, 6)])
+def test_twin_schedules_match_oracle(entry, p, m):
+    """gems / chimera (twin topology: two routes over two weight replicas, gallery.hpp:252-326): every
+    microbatch runs its route's stages; at the end of the step the replicas exchange gradients, so both
+    copies of every model stage carry the gradient of the whole batch.  Reference: the same model with
+    d stages trained on all m microbatches (oracle.numerics.reference_step)."""
+    sched = pb.assemble(pb.build_entry(entry, p), m)
+    S = sched.topology.num_stages
+    Sm = S // 2
+    cfg = ModelConfig(layers=2 * Sm, hidden=256, heads=2, seq=256, vocab=1024, micro_batch=1, optimizer=False)
+    ex = PipelineExecutor(cfg, sched)
+    tokens, labels = synthetic_batch(cfg, m)
+    res = ex.step(tokens, labels)
+
+    def model_name(n):
+        s, rest = n.split(".", 1)
+        k = int(s[1:])
+        return f"s{k - Sm if k > Sm else k}.{rest}"
+
+    names = list(ex.params())
+    shp = N.shapes(cfg, Sm)
+    assert sorted({model_name(n) for n in names}) == sorted(shp)
+    w = {model_name(n): torch.from_numpy(ex.get(n, "weight").reshape(shp[model_name(n)])) for n in names
+         if int(n.split(".")[0][1:]) <= Sm}
+    for n in names:  # replicas start identical (init ids follow the model layer)
+        assert np.array_equal(ex.get(n, "weight"), w[model_name(n)].numpy().ravel()), n
+    loss_ref, grads_ref = N.reference_step(w, tokens, labels, cfg, Sm)
+    assert abs(res.loss - loss_ref) <= LOSS_RTOL * abs(loss_ref), (res.loss, loss_ref)
+    for n in names:
+        g, r = ex.get(n, "grad"), grads_ref[model_name(n)].numpy().ravel()
+        assert N.rel_l2(g, r) < GRAD_REL_L2, (n, N.rel_l2(g, r))
+    for n in names:  # both copies hold the same summed gradient
+        k = int(n.split(".")[0][1:])
+        if k <= Sm:
+            twin_n = f"s{k + Sm}." + n.split(".", 1)[1]
+            assert np.array_equal(ex.get(n, "grad"), ex.get(twin_n, "grad")), n
+    peaks = pb.exact_peak(sched)
+    for d, st in res.per_device.items():
+        assert st.pool_slots == int(peaks[d - 1])
+
+
+def test_twin_optimizer_keeps_replicas_identical():
+    """Two AdamW steps on a chimera pipeline: the replicas see the same summed gradient, so their
+    weights stay bit-identical and the loss goes down."""
+    sched = pb.assemble(pb.build_entry("chimera", 2), 4)
+    cfg = ModelConfig(layers=4, hidden=256, heads=2, seq=256, vocab=1024, micro_batch=1, optimizer=True, lr=1e-3)
+    ex = PipelineExecutor(cfg, sched)
+    tokens, labels = synthetic_batch(cfg, 4)
+    l0 = ex.step(tokens, labels).loss
+    ex.step(tokens, labels)
+    l2 = ex.step(tokens, labels).loss
+    assert l2 < l0, (l0, l2)
+    for n in ex.params():
+        k = int(n.split(".")[0][1:])
+        if k <= 2:
+            assert np.array_equal(ex.get(n, "weight"), ex.get(f"s{k + 2}." + n.split(".", 1)[1], "weight")), n
