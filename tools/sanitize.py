@@ -1,6 +1,6 @@
 """compute-sanitizer evidence: one toy pipeline step (two pipeline devices sharing cuda:0,
 V-Half p=2 m=4, every kernel the executor launches incl. folded-RMSNorm epilogues, attention fwd/bwd,
-grouped dW, CE, AdamW) and the stand-alone GEMM / attention entry points, run under
+grouped dW, CE, AdamW), a chimera step (twin routes + replica-gradient exchange) and the stand-alone GEMM / attention entry points, run under
     compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize.py
 Small shapes: the sanitizer serialises and instruments every access."""
 import os
@@ -23,6 +23,10 @@ tokens, labels = synthetic_batch(cfg, 4)
 res = ex.step(tokens, labels)
 res = ex.step(tokens, labels)
 print("step loss", res.loss)
+# twin topology (chimera: two routes, replica-gradient exchange before AdamW)
+sched2 = pb.assemble(pb.build_entry("chimera", 2), 4)
+ex2 = PipelineExecutor(cfg, sched2, cuda_devices=[0, 0])
+print("chimera loss", ex2.step(tokens, labels).loss)
 # stand-alone GEMM (CTA pair, 512-row pair tiles) and attention at a multi-tile shape
 g = torch.Generator(device="cuda").manual_seed(0)
 A = torch.randn(512, 8192, device="cuda", generator=g).bfloat16()
