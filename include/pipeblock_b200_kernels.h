@@ -34,7 +34,8 @@ int pbt_row_sumsq(const void* x, float* ss, int32_t T, int32_t h, void* stream);
 /* causal attention, head_dim 128, tcgen05/TMEM (the executor's forward attention): qkv [T,3h] -> out [T,h],
  * lse2 [heads,T] (base-2 LSE of scaled scores); seq % 128 == 0 */
 int pbt_attn_fwd_tc(const void* qkv, void* out, float* lse2, int32_t batch, int32_t seq, int32_t heads, void* stream);
-/* backward on tcgen05/TMEM (the executor's): dqkv [T,3h]; dsum [heads,T], dq_acc [T,h] fp32 scratch */
+/* backward on tcgen05/TMEM (the executor's): dqkv [T,3h]; dsum [heads*T + 64] (the row terms, then the
+ * persistent kernel's work counter), dq_acc [T,h] fp32 scratch */
 int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse2, float* dsum, float* dq_acc,
                     void* dqkv, int32_t batch, int32_t seq, int32_t heads, void* stream);
 int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h, void* stream);

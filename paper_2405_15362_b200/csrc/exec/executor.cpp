@@ -332,7 +332,7 @@ void Exec::init(int device) {
     flags = static_cast<uint32_t*>(dmalloc(nflags * 4, "flags"));
     ck(cudaMemsetAsync(flags, 0, nflags * 4, cs), "memset");
     scratch = static_cast<__nv_bfloat16*>(dmalloc(size_t(T) * h * 2, "scratch"));
-    dsum = static_cast<float*>(dmalloc(size_t(H) * T * 4, "scratch"));
+    dsum = static_cast<float*>(dmalloc(size_t(H) * T * 4 + 256, "scratch"));  // + the attention bwd work counter
     dq_acc = static_cast<float*>(dmalloc(size_t(T) * h * 4, "scratch"));
     // deterministic row sums of squares (folded RMSNorm): per-128-column partials + row-group counters
     ss_part = static_cast<float*>(dmalloc(size_t(T) * (h / 128) * 4, "scratch"));

@@ -70,6 +70,7 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dout, cons
         if (lane == 0) dsum[size_t(head) * T + t] = s;
         *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (t == 0 && threadIdx.x == 0) reinterpret_cast<int*>(dsum + size_t(H) * T)[0] = 0;  // bwd work counter
 }
 
 // dQ (bf16, into the q columns of dqkv) = scale * dq_acc, times the row's folded-RMSNorm factor
@@ -413,10 +414,10 @@ struct Bwd5Smem {
     static constexpr int ds = dO + 3 * kHalf;   // [2] dS^T_j: [128 keys][64 q] bf16, one atom
     static constexpr int stg = ds + 2 * 16384;  // dQ staging: 4 chunks [64 q][32 d] fp32, 8 KB each
     static constexpr int lse = stg + 32768;     // [2][128] floats: lse2[64] | D[64]
-    static constexpr int bars = lse + 1024;
+    static constexpr int bars = lse + 1024;  // 36 barriers, the TMEM slot, a 4-entry item ring
     // 512 B of alignment slack: the 227 KB opt-in limit leaves no room for 1 KB; the dynamic window
     // starts 1 KB-aligned when the kernel has no static shared memory (checked at run time)
-    static constexpr int total = bars + 256 + 512;
+    static constexpr int total = bars + 384 + 512;
 };
 static_assert(Bwd5Smem::total <= 232448, "attn bwd v5: shared memory over the sm_100 opt-in limit");
 
@@ -432,9 +433,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Bwd5Smem::bars);
     uint64_t* kv_full = bars + 0;
     uint64_t* q_full = bars + 1;      // [3]
-    uint64_t* q_empty = bars + 4;     // [3] MMA commit after dK_j
+    uint64_t* q_empty = bars + 4;     // [3] MMA commit after dK_g
     uint64_t* do_full = bars + 7;     // [3]
-    uint64_t* do_empty = bars + 10;   // [3] MMA commit after dV_j
+    uint64_t* do_empty = bars + 10;   // [3] MMA commit after dV_g
     uint64_t* s_full = bars + 13;     // [2]
     uint64_t* dp_full = bars + 15;    // [2]
     uint64_t* ds_full = bars + 17;    // [2] 8 compute warps
@@ -442,27 +443,40 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* dq_free = bars + 21;    // [2] 8 compute warps
     uint64_t* stg_free = bars + 23;   // reducer: staging read out
     uint64_t* dq_staged = bars + 24;  // 8 compute warps
-    uint64_t* dkv_full = bars + 25;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+    uint64_t* dkv_full = bars + 25;   // MMA commit after an item's last dV
+    uint64_t* kv_empty = bars + 26;   // (same commit) the item's K / V no longer read
+    uint64_t* dkv_free = bars + 27;   // 8 compute warps: the item's dK / dV read out of TMEM
+    uint64_t* item_full = bars + 28;  // [4] loader: the item index of ring slot k is published
+    uint64_t* item_empty = bars + 32; // [4] the 11 consumer warps have read it
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
+    int* item_ring = reinterpret_cast<int*>(bars + 37);  // [4]
     float* sL = reinterpret_cast<float*>(sm + Bwd5Smem::lse);
 
     const uint32_t warp = warp_id();
     const int nqb = seq / BQ;
-    const int hb = int(blockIdx.x) % (H * (T / seq));
-    const int kb = int(blockIdx.x) / (H * (T / seq));
-    const int head = hb % H, b = hb / H;
-    const int tok0 = b * seq;
-    const int n = 2 * (nqb - kb);               // half tiles
-    const int qrow0 = tok0 + kb * BQ;           // token row of half tile 0
+    const int HB = H * (T / seq);     // (head, sequence) pairs
+    const int NI = nqb * HB;          // items: (128-key tile kb, head, sequence), heaviest kb first
+    // Persistent CTAs with dynamic (greedy, heaviest-first) items: the loader warp takes the next item
+    // index from a global counter (attn_bwd_pre zeroes it; the first item is blockIdx.x) and publishes it
+    // in a 4-entry shared ring; every other warp reads the ring in the same order.  Half tiles are
+    // numbered globally (g) across a CTA's items: ring slots, TMEM buffers and barrier phases follow g.
+    int* work = reinterpret_cast<int*>(const_cast<float*>(dsum) + size_t(H) * T);
+    auto next_item = [&](int k, bool whole_warp) {  // consumer warps: one arrival per warp
+        mbar_wait(&item_full[k & 3], (k >> 2) & 1);
+        const int idx = *reinterpret_cast<volatile int*>(&item_ring[k & 3]);
+        if (whole_warp) __syncwarp();
+        if (!whole_warp || lane_id() == 0) mbar_arrive(&item_empty[k & 3]);
+        return idx;
+    };
 
     if (warp == 0 && elect_one()) {
         tma_prefetch(&tm_kv);
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
         tma_prefetch(&tm_dq);
-        for (int i = 0; i < 26; ++i) {
-            const bool eight = (i >= 17 && i < 19) || (i >= 21 && i < 23) || i == 24;
-            mbar_init(&bars[i], eight ? 8 : 1);
+        for (int i = 0; i < 36; ++i) {
+            const bool eight = (i >= 17 && i < 19) || (i >= 21 && i < 23) || i == 24 || i == 27;
+            mbar_init(&bars[i], i >= 32 ? 11 : (eight ? 8 : 1));
         }
         fence_barrier_init();
     }
@@ -477,51 +491,76 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (warp >= 10) {
         if (warp == 10 && lane_id() == 0) {
             // dQ reducer: four 8 KB TMA bulk reduce-adds per half tile
-            for (int u = 0; u < n; ++u) {
-                mbar_wait(dq_staged, u & 1);
-                ATRACE(u, 6);
-                const int row = qrow0 + u * BQH;
+            int u = 0;
+            for (int r = 0;; ++r) {
+                const int idx = next_item(r, false);
+                if (idx >= NI) break;
+                const int kb = idx / HB, hb = idx % HB, head = hb % H;
+                const int qrow0 = (hb / H) * seq + kb * BQ, n = 2 * (nqb - kb);
+                for (int j = 0; j < n; ++j, ++u) {
+                    mbar_wait(dq_staged, u & 1);
+                    ATRACE(u, 6);
+                    const int row = qrow0 + j * BQH;
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    asm volatile(
-                        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tm_dq)),
-                        "r"(smem_u32(sm + Bwd5Smem::stg + c * 8192)), "r"(head * D + c * 32), "r"(row)
-                        : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                ATRACE(u, 7);
-                mbar_arrive(stg_free);
+                    for (int cc = 0; cc < 4; ++cc)
+                        asm volatile(
+                            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&tm_dq)),
+                            "r"(smem_u32(sm + Bwd5Smem::stg + cc * 8192)), "r"(head * D + cc * 32), "r"(row)
+                            : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    ATRACE(u, 7);
+                    mbar_arrive(stg_free);
+                }
             }
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
         if (warp == 11 && lane_id() == 0) {
-            for (int j = 0; j < n; ++j) {
-                const int st = j % 3;
-                if (j >= 3) mbar_wait(&do_empty[st], ((j / 3) - 1) & 1);
-                uint8_t* dst = sm + Bwd5Smem::dO + st * kHalf;
-                mbar_expect_tx(&do_full[st], kHalf);
-                tma_load_2d(dst, &tm_do, &do_full[st], head * D, qrow0 + j * BQH);
-                tma_load_2d(dst + 8192, &tm_do, &do_full[st], head * D + 64, qrow0 + j * BQH);
+            int g = 0;
+            for (int r = 0;; ++r) {
+                const int idx = next_item(r, false);
+                if (idx >= NI) break;
+                const int kb = idx / HB, hb = idx % HB, head = hb % H;
+                const int qrow0 = (hb / H) * seq + kb * BQ, n = 2 * (nqb - kb);
+                for (int j = 0; j < n; ++j, ++g) {
+                    const int st = g % 3;
+                    if (g >= 3) mbar_wait(&do_empty[st], ((g / 3) - 1) & 1);
+                    uint8_t* dst = sm + Bwd5Smem::dO + st * kHalf;
+                    mbar_expect_tx(&do_full[st], kHalf);
+                    tma_load_2d(dst, &tm_do, &do_full[st], head * D, qrow0 + j * BQH);
+                    tma_load_2d(dst + 8192, &tm_do, &do_full[st], head * D + 64, qrow0 + j * BQH);
+                }
             }
         }
     } else if (warp == 0) {
         if (lane_id() == 0) {
-            const int ck = H * D + head * D, cv = 2 * H * D + head * D;
-            const int kr = tok0 + kb * BK;
-            mbar_expect_tx(kv_full, 2 * kTile);
-            tma_load_2d(sm + Bwd5Smem::k, &tm_kv, kv_full, ck, kr);
-            tma_load_2d(sm + Bwd5Smem::k + 16384, &tm_kv, kv_full, ck + 64, kr);
-            tma_load_2d(sm + Bwd5Smem::v, &tm_kv, kv_full, cv, kr);
-            tma_load_2d(sm + Bwd5Smem::v + 16384, &tm_kv, kv_full, cv + 64, kr);
-            for (int j = 0; j < n; ++j) {
-                const int st = j % 3;
-                if (j >= 3) mbar_wait(&q_empty[st], ((j / 3) - 1) & 1);
-                ATRACE(j, 11);
-                uint8_t* dst = sm + Bwd5Smem::q + st * kHalf;
-                mbar_expect_tx(&q_full[st], kHalf);
-                tma_load_2d(dst, &tm_q, &q_full[st], head * D, qrow0 + j * BQH);
-                tma_load_2d(dst + 8192, &tm_q, &q_full[st], head * D + 64, qrow0 + j * BQH);
+            int g = 0;
+            for (int r = 0;; ++r) {
+                const int idx = r == 0 ? int(blockIdx.x) : int(gridDim.x) + atomicAdd(work, 1);
+                if (r >= 4) mbar_wait(&item_empty[r & 3], ((r >> 2) - 1) & 1);
+                item_ring[r & 3] = idx < NI ? idx : NI;  // NI: no more work
+                mbar_arrive(&item_full[r & 3]);
+                if (idx >= NI) break;
+                const int kb = idx / HB, hb = idx % HB, head = hb % H;
+                const int tok0 = (hb / H) * seq, qrow0 = tok0 + kb * BQ, n = 2 * (nqb - kb);
+                const int ck = H * D + head * D, cv = 2 * H * D + head * D;
+                const int kr = tok0 + kb * BK;
+                if (r > 0) mbar_wait(kv_empty, (r - 1) & 1);  // the previous item's MMAs are done with K / V
+                mbar_expect_tx(kv_full, 2 * kTile);
+                tma_load_2d(sm + Bwd5Smem::k, &tm_kv, kv_full, ck, kr);
+                tma_load_2d(sm + Bwd5Smem::k + 16384, &tm_kv, kv_full, ck + 64, kr);
+                tma_load_2d(sm + Bwd5Smem::v, &tm_kv, kv_full, cv, kr);
+                tma_load_2d(sm + Bwd5Smem::v + 16384, &tm_kv, kv_full, cv + 64, kr);
+                for (int j = 0; j < n; ++j, ++g) {
+                    const int st = g % 3;
+                    if (g >= 3) mbar_wait(&q_empty[st], ((g / 3) - 1) & 1);
+                    ATRACE(g, 11);
+                    uint8_t* dst = sm + Bwd5Smem::q + st * kHalf;
+                    mbar_expect_tx(&q_full[st], kHalf);
+                    tma_load_2d(dst, &tm_q, &q_full[st], head * D, qrow0 + j * BQH);
+                    tma_load_2d(dst + 8192, &tm_q, &q_full[st], head * D + 64, qrow0 + j * BQH);
+                }
             }
         }
     } else if (warp == 1) {
@@ -529,67 +568,79 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         constexpr uint32_t id_kv = idesc_bf16(128, 128, false, true);   // dK, dV: A from TMEM, B MN-major
         constexpr uint32_t id_dq = idesc_bf16(128, 64, true, true);     // dQ^T = K^T dS^T: both MN-major
         const uint32_t sk = smem_u32(sm + Bwd5Smem::k), sv = smem_u32(sm + Bwd5Smem::v);
-        auto issue_sd = [&](int j, bool dp) {  // S^T_j = K Q_j^T or dP^T_j = V dO_j^T
-            const int st = j % 3;
+        auto issue_sd = [&](int g, bool dp) {  // S^T_g = K Q_g^T or dP^T_g = V dO_g^T
+            const int st = g % 3;
             uint64_t* full = dp ? &do_full[st] : &q_full[st];
             const uint32_t sb = smem_u32(sm + (dp ? Bwd5Smem::dO : Bwd5Smem::q) + st * kHalf);
             const uint32_t sa = dp ? sv : sk;
-            mbar_wait(full, (j / 3) & 1);
+            if (dp && g >= 2) {  // dP^T_g lands over dQ^T_{g-2}: wait until it is read out of TMEM
+                mbar_wait(&dq_free[g & 1], ((g - 2) >> 1) & 1);
+                if (lane_id() == 0) ATRACE(g - 2, 10);
+            }
+            mbar_wait(full, (g / 3) & 1);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    tc_mma(tmem + (j & 1) * 128 + (dp ? 64 : 0), sdesc(sa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    tc_mma(tmem + (g & 1) * 128 + (dp ? 64 : 0), sdesc(sa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                            sdesc(sb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_sd, kk != 0);
-                tc_commit(dp ? &dp_full[j & 1] : &s_full[j & 1]);
+                tc_commit(dp ? &dp_full[g & 1] : &s_full[g & 1]);
             }
             __syncwarp();
         };
-        mbar_wait(kv_full, 0);
-        issue_sd(0, false);
-        issue_sd(0, true);
-        issue_sd(1, false);
-        issue_sd(1, true);
-        for (int j = 0; j < n; ++j) {
-            const int bb = j & 1, st = j % 3;
-            const uint32_t sq = smem_u32(sm + Bwd5Smem::q + st * kHalf);
-            const uint32_t sdo = smem_u32(sm + Bwd5Smem::dO + st * kHalf);
-            const uint32_t sds = smem_u32(sm + Bwd5Smem::ds + bb * 16384);
-            mbar_wait(&ds_full[bb], (j >> 1) & 1);
+        int g = 0;
+        for (int r = 0;; ++r) {
+            const int idx = next_item(r, true);
+            if (idx >= NI) break;
+            const int kb = idx / HB, n = 2 * (nqb - kb);
+            mbar_wait(kv_full, r & 1);
             tc_fence_after();
-            if (lane_id() == 0) ATRACE(j, 8);
-            if (elect_one()) {
-                // dQ^T_j = K^T dS^T_j over the consumed dP^T_j columns: first, so the compute warps can
-                // drain it while dK_j / dV_j run
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma(tmem + bb * 128 + 64, sdesc(sk + kk * 2048, 16384, 1024), sdesc(sds + kk * 2048, 8192, 1024),
-                           id_dq, kk != 0);
-                tc_commit(&dq_full[bb]);
-                // dK += dS^T_j Q_j (A = dS^T bf16 pairs in the S^T_j columns [16,32) / [48,64); K = 64 queries)
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    tc_mma_ts(tmem + 384, tmem + bb * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
-                              sdesc(sq + kk * 2048, 8192, 1024), id_kv, (j | kk) != 0);
-                tc_commit(&q_empty[st]);
-                // dV += P^T_j dO_j (A = P^T bf16 pairs in TMEM)
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    tc_mma_ts(tmem + 256, tmem + bb * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
-                              sdesc(sdo + kk * 2048, 8192, 1024), id_kv, (j | kk) != 0);
-                tc_commit(&do_empty[st]);
-            }
-            __syncwarp();
-            if (j + 2 < n) {
-                issue_sd(j + 2, false);                // over P^T_j, after dV_j read it (in-order pipe)
-                mbar_wait(&dq_free[bb], (j >> 1) & 1);  // dQ^T_j read out of TMEM
+            issue_sd(g, false);
+            issue_sd(g, true);
+            issue_sd(g + 1, false);
+            issue_sd(g + 1, true);
+            for (int j = 0; j < n; ++j) {
+                const int gg = g + j, bb = gg & 1, st = gg % 3;
+                const uint32_t sq = smem_u32(sm + Bwd5Smem::q + st * kHalf);
+                const uint32_t sdo = smem_u32(sm + Bwd5Smem::dO + st * kHalf);
+                const uint32_t sds = smem_u32(sm + Bwd5Smem::ds + bb * 16384);
+                mbar_wait(&ds_full[bb], (gg >> 1) & 1);
+                if (j == 0 && r > 0) mbar_wait(dkv_free, (r - 1) & 1);  // previous item's dK / dV read out
                 tc_fence_after();
-                if (lane_id() == 0) ATRACE(j, 10);
-                issue_sd(j + 2, true);
+                if (lane_id() == 0) ATRACE(gg, 8);
+                if (elect_one()) {
+                    // dQ^T_g = K^T dS^T_g over the consumed dP^T_g columns: first, so the compute warps can
+                    // drain it while dK_g / dV_g run
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        tc_mma(tmem + bb * 128 + 64, sdesc(sk + kk * 2048, 16384, 1024),
+                               sdesc(sds + kk * 2048, 8192, 1024), id_dq, kk != 0);
+                    tc_commit(&dq_full[bb]);
+                    // dK += dS^T_g Q_g (A = dS^T bf16 pairs in the S^T_g columns [16,32) / [48,64); K = 64)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        tc_mma_ts(tmem + 384, tmem + bb * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
+                                  sdesc(sq + kk * 2048, 8192, 1024), id_kv, (j | kk) != 0);
+                    tc_commit(&q_empty[st]);
+                    // dV += P^T_g dO_g (A = P^T bf16 pairs in TMEM)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        tc_mma_ts(tmem + 256, tmem + bb * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
+                                  sdesc(sdo + kk * 2048, 8192, 1024), id_kv, (j | kk) != 0);
+                    tc_commit(&do_empty[st]);
+                    if (j == n - 1) {
+                        tc_commit(dkv_full);
+                        tc_commit(kv_empty);
+                    }
+                }
+                __syncwarp();
+                if (j + 2 < n) {
+                    issue_sd(gg + 2, false);  // over P^T_g, after dV_g read it (in-order pipe)
+                    issue_sd(gg + 2, true);
+                }
             }
+            g += n;
         }
-        if (elect_one()) tc_commit(dkv_full);
-        __syncwarp();
     } else {
         const uint32_t q4 = warp & 3;
         const int hf = int(warp - 2) >> 2;  // query column half (32 of the 64) handled by this warp
@@ -597,12 +648,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t lane_base = (q4 * 32) << 16;
         const float sl2 = scale * kLog2e;
         const int key = r;  // key row relative to the tile (queries relative to qrow0 below)
-        auto lse_of = [&](int j) {  // staged value of this thread (r < 64): lse2 (hf 0) or D (hf 1)
-            const size_t idx = size_t(head) * T + qrow0 + j * BQH + (r & 63);
-            return hf == 0 ? lse2[idx] : dsum[idx];
-        };
-        if (r < 64) sL[hf * 64 + r] = lse_of(0);
-        bar_sync_compute();
         auto drain_dq = [&](int u) {  // dQ^T_u: TMEM -> registers -> release -> fp32 staging
             const int pb = u & 1;
             mbar_wait(&dq_full[pb], (u >> 1) & 1);
@@ -619,109 +664,127 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // thread = d row r (chunk q4 = r / 32, lane = r % 32), 32 query rows hf*32 + c
             uint8_t* chunk = sm + Bwd5Smem::stg + q4 * 8192;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int qq = hf * 32 + c;
-                *reinterpret_cast<float*>(chunk + qq * 128 + (((lane_id() >> 2) ^ (qq & 7)) << 4) + (lane_id() & 3) * 4) = v[c];
+            for (int cc = 0; cc < 32; ++cc) {
+                const int qq = hf * 32 + cc;
+                *reinterpret_cast<float*>(chunk + qq * 128 + (((lane_id() >> 2) ^ (qq & 7)) << 4) + (lane_id() & 3) * 4) = v[cc];
             }
             fence_async_smem();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(dq_staged);
             if (threadIdx.x == 64) ATRACE(u, 5);
         };
-        for (int j = 0; j < n; ++j) {
-            const int bb = j & 1;
-            const float* Lb = sL + bb * 128;
-            const float lnext = (j + 1 < n && r < 64) ? lse_of(j + 1) : 0.f;
-            if (threadIdx.x == 64) ATRACE(j, 0);
-            mbar_wait(&s_full[bb], (j >> 1) & 1);
-            if (threadIdx.x == 64) ATRACE(j, 12);
-            mbar_wait(&dp_full[bb], (j >> 1) & 1);
-            tc_fence_after();
-            if (threadIdx.x == 64) ATRACE(j, 1);
-            const int c0 = hf * 32;
-            {
-                float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + bb * 128 + c0, sv);
-                tmem_ld32(tmem + lane_base + bb * 128 + 64 + c0, dp);
-                tmem_ld_wait();
-                if (threadIdx.x == 64) ATRACE(j, 13);
-                if (__builtin_expect(j < 2, 0)) {  // causal mask: the two half tiles of the diagonal block
+        int g = 0;
+        for (int ri = 0;; ++ri) {
+            const int idx = next_item(ri, true);
+            if (idx >= NI) break;
+            const int kb = idx / HB, hb = idx % HB, head = hb % H;
+            const int tok0 = (hb / H) * seq, qrow0 = tok0 + kb * BQ, n = 2 * (nqb - kb);
+            auto lse_of = [&](int j) {  // staged value of this thread (r < 64): lse2 (hf 0) or D (hf 1)
+                const size_t i2 = size_t(head) * T + qrow0 + j * BQH + (r & 63);
+                return hf == 0 ? lse2[i2] : dsum[i2];
+            };
+            if (r < 64) sL[(g & 1) * 128 + hf * 64 + r] = lse_of(0);
+            bar_sync_compute();
+            for (int j = 0; j < n; ++j) {
+                const int gg = g + j, bb = gg & 1;
+                const float* Lb = sL + bb * 128;
+                const float lnext = (j + 1 < n && r < 64) ? lse_of(j + 1) : 0.f;
+                if (threadIdx.x == 64) ATRACE(gg, 0);
+                mbar_wait(&s_full[bb], (gg >> 1) & 1);
+                if (threadIdx.x == 64) ATRACE(gg, 12);
+                mbar_wait(&dp_full[bb], (gg >> 1) & 1);
+                tc_fence_after();
+                if (threadIdx.x == 64) ATRACE(gg, 1);
+                const int c0 = hf * 32;
+                {
+                    float sv[32], dp[32];
+                    tmem_ld32(tmem + lane_base + bb * 128 + c0, sv);
+                    tmem_ld32(tmem + lane_base + bb * 128 + 64 + c0, dp);
+                    tmem_ld_wait();
+                    if (threadIdx.x == 64) ATRACE(gg, 13);
+                    if (__builtin_expect(j < 2, 0)) {  // causal mask: the two half tiles of the diagonal block
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (key > j * BQH + c0 + e) sv[e] = -INFINITY;
-                }
-                // lse2 / D of this half's 32 query columns: the same for every lane (smem broadcast),
-                // loaded as float4 so the 32 independent exp2 chains issue back to back
-                const float4* l4 = reinterpret_cast<const float4*>(Lb + c0);
-                const float4* d4 = reinterpret_cast<const float4*>(Lb + 64 + c0);
-                uint32_t pk[16], dk[16];
-#pragma unroll
-                for (int e4 = 0; e4 < 8; ++e4) {
-                    const float4 lq = l4[e4], dq = d4[e4];
-                    const float lz[4] = {lq.x, lq.y, lq.z, lq.w}, dz[4] = {dq.x, dq.y, dq.z, dq.w};
-                    // packed f32x2 FMA / ADD / MUL (FFMA2 & co. on sm_100): half the issue slots
-#pragma unroll
-                    for (int u = 0; u < 4; u += 2) {
-                        const float2 x = __ffma2_rn(make_float2(sv[4 * e4 + u], sv[4 * e4 + u + 1]), make_float2(sl2, sl2),
-                                                    make_float2(-lz[u], -lz[u + 1]));
-                        const float2 pv = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-                        const float2 dd = __fadd2_rn(make_float2(dp[4 * e4 + u], dp[4 * e4 + u + 1]),
-                                                     make_float2(-dz[u], -dz[u + 1]));
-                        const float2 dsv = __fmul2_rn(pv, dd);
-                        pk[2 * e4 + (u >> 1)] = pack_bf16(pv.x, pv.y);
-                        dk[2 * e4 + (u >> 1)] = pack_bf16(dsv.x, dsv.y);
+                        for (int e = 0; e < 32; ++e)
+                            if (key > j * BQH + c0 + e) sv[e] = -INFINITY;
                     }
-                }
-                if (threadIdx.x == 64) ATRACE(j, 14);
-                tmem_st16u(tmem + lane_base + bb * 128 + c0, pk);
-                tmem_st16u(tmem + lane_base + bb * 128 + c0 + 16, dk);
-                // dS^T_j to smem ([key][q], 128B-swizzled, one atom): B operand (MN-major) of dQ^T_j and
-                // A operand (K-major) of dK_j.  Its last readers, dQ^T_{j-2} and dK_{j-2}, precede S_j in
-                // the MMA pipe, so s_full_j (waited above) covers them.
-                uint8_t* sds = sm + Bwd5Smem::ds + bb * 16384;
+                    // lse2 / D of this half's 32 query columns: the same for every lane (smem broadcast),
+                    // loaded as float4 so the 32 independent exp2 chains issue back to back
+                    const float4* l4 = reinterpret_cast<const float4*>(Lb + c0);
+                    const float4* d4 = reinterpret_cast<const float4*>(Lb + 64 + c0);
+                    uint32_t pk[16], dk[16];
 #pragma unroll
-                for (int e8 = 0; e8 < 4; ++e8)
-                    *reinterpret_cast<uint4*>(sds + r * 128 + ((((c0 >> 3) + e8) ^ (r & 7)) << 4)) =
-                        make_uint4(dk[4 * e8], dk[4 * e8 + 1], dk[4 * e8 + 2], dk[4 * e8 + 3]);
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const float4 lq = l4[e4], dq = d4[e4];
+                        const float lz[4] = {lq.x, lq.y, lq.z, lq.w}, dz[4] = {dq.x, dq.y, dq.z, dq.w};
+                        // packed f32x2 FMA / ADD / MUL (FFMA2 & co. on sm_100): half the issue slots
+#pragma unroll
+                        for (int u = 0; u < 4; u += 2) {
+                            const float2 x = __ffma2_rn(make_float2(sv[4 * e4 + u], sv[4 * e4 + u + 1]),
+                                                        make_float2(sl2, sl2), make_float2(-lz[u], -lz[u + 1]));
+                            const float2 pv = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                            const float2 dd = __fadd2_rn(make_float2(dp[4 * e4 + u], dp[4 * e4 + u + 1]),
+                                                         make_float2(-dz[u], -dz[u + 1]));
+                            const float2 dsv = __fmul2_rn(pv, dd);
+                            pk[2 * e4 + (u >> 1)] = pack_bf16(pv.x, pv.y);
+                            dk[2 * e4 + (u >> 1)] = pack_bf16(dsv.x, dsv.y);
+                        }
+                    }
+                    if (threadIdx.x == 64) ATRACE(gg, 14);
+                    tmem_st16u(tmem + lane_base + bb * 128 + c0, pk);
+                    tmem_st16u(tmem + lane_base + bb * 128 + c0 + 16, dk);
+                    // dS^T_g to smem ([key][q], 128B-swizzled, one atom): B operand (MN-major) of dQ^T_g.
+                    // Its last readers, dQ^T_{g-2} and dK_{g-2}, precede S_g in the MMA pipe, so s_full_g
+                    // (waited above) covers them.
+                    uint8_t* sds = sm + Bwd5Smem::ds + bb * 16384;
+#pragma unroll
+                    for (int e8 = 0; e8 < 4; ++e8)
+                        *reinterpret_cast<uint4*>(sds + r * 128 + ((((c0 >> 3) + e8) ^ (r & 7)) << 4)) =
+                            make_uint4(dk[4 * e8], dk[4 * e8 + 1], dk[4 * e8 + 2], dk[4 * e8 + 3]);
+                }
+                tmem_st_wait();
+                if (threadIdx.x == 64) ATRACE(gg, 15);
+                fence_async_smem();
+                tc_fence_before();
+                __syncwarp();
+                if (lane_id() == 0) mbar_arrive(&ds_full[bb]);
+                if (threadIdx.x == 64) ATRACE(gg, 2);
+                if (j >= 1) drain_dq(gg - 1);
+                if (j + 1 < n) {
+                    if (r < 64) sL[((gg + 1) & 1) * 128 + hf * 64 + r] = lnext;  // buffer last read by E_{g-1}
+                    bar_sync_compute();
+                }
             }
-            tmem_st_wait();
-            if (threadIdx.x == 64) ATRACE(j, 15);
-            fence_async_smem();
+            drain_dq(g + n - 1);
+            // dV, dK rows (thread = key row, column half hf); then the columns go to the next item
+            mbar_wait(dkv_full, ri & 1);
+            tc_fence_after();
+            const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
+            // folded RMSNorm of the QKV input: dqkv' = rstd1(row) * dqkv (executor.cpp, fold mode)
+            const float fv = rs ? rsqrtf(rs[tok0 + kb * BK + r] * rs_inv_n + rs_eps) : 1.f;
+            const float fk = fv * scale;
+#pragma unroll 1
+            for (int cc = 0; cc < 2; ++cc) {
+                const int cq = hf * 2 + cc;
+                float v[32], k[32];
+                tmem_ld32(tmem + lane_base + 256 + cq * 32, v);
+                tmem_ld32(tmem + lane_base + 384 + cq * 32, k);
+                tmem_ld_wait();
+                uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + cq * 32);
+                uint4* dkp = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + cq * 32);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    dv[e] = make_uint4(pack_bf16(v[8 * e] * fv, v[8 * e + 1] * fv), pack_bf16(v[8 * e + 2] * fv, v[8 * e + 3] * fv),
+                                       pack_bf16(v[8 * e + 4] * fv, v[8 * e + 5] * fv), pack_bf16(v[8 * e + 6] * fv, v[8 * e + 7] * fv));
+                    dkp[e] = make_uint4(pack_bf16(k[8 * e] * fk, k[8 * e + 1] * fk),
+                                        pack_bf16(k[8 * e + 2] * fk, k[8 * e + 3] * fk),
+                                        pack_bf16(k[8 * e + 4] * fk, k[8 * e + 5] * fk),
+                                        pack_bf16(k[8 * e + 6] * fk, k[8 * e + 7] * fk));
+                }
+            }
             tc_fence_before();
             __syncwarp();
-            if (lane_id() == 0) mbar_arrive(&ds_full[bb]);
-            if (threadIdx.x == 64) ATRACE(j, 2);
-            if (j >= 1) drain_dq(j - 1);
-            if (j + 1 < n) {
-                if (r < 64) sL[((j + 1) & 1) * 128 + hf * 64 + r] = lnext;  // buffer last read by E_{j-1}
-                bar_sync_compute();
-            }
-        }
-        drain_dq(n - 1);
-        // dV, dK rows (thread = key row, column half hf), as v4
-        mbar_wait(dkv_full, 0);
-        tc_fence_after();
-        const size_t rowoff = size_t(tok0 + kb * BK + r) * (3 * H * D);
-        const float fv = rs ? rsqrtf(rs[tok0 + kb * BK + r] * rs_inv_n + rs_eps) : 1.f;
-        const float fk = fv * scale;
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c = hf * 2 + cc;
-            float v[32], k[32];
-            tmem_ld32(tmem + lane_base + 256 + c * 32, v);
-            tmem_ld32(tmem + lane_base + 384 + c * 32, k);
-            tmem_ld_wait();
-            uint4* dv = reinterpret_cast<uint4*>(dqkv + rowoff + 2 * H * D + head * D + c * 32);
-            uint4* dk = reinterpret_cast<uint4*>(dqkv + rowoff + H * D + head * D + c * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                dv[e] = make_uint4(pack_bf16(v[8 * e] * fv, v[8 * e + 1] * fv), pack_bf16(v[8 * e + 2] * fv, v[8 * e + 3] * fv),
-                                   pack_bf16(v[8 * e + 4] * fv, v[8 * e + 5] * fv), pack_bf16(v[8 * e + 6] * fv, v[8 * e + 7] * fv));
-                dk[e] = make_uint4(pack_bf16(k[8 * e] * fk, k[8 * e + 1] * fk),
-                                   pack_bf16(k[8 * e + 2] * fk, k[8 * e + 3] * fk),
-                                   pack_bf16(k[8 * e + 4] * fk, k[8 * e + 5] * fk),
-                                   pack_bf16(k[8 * e + 6] * fk, k[8 * e + 7] * fk));
-            }
+            if (lane_id() == 0) mbar_arrive(dkv_free);
+            g += n;
         }
     }
     tc_fence_before();
@@ -996,7 +1059,9 @@ void attn_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_
     const CUtensorMap tdq = make_map_t(dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(heads) * D, uint64_t(T),
                                        uint64_t(heads) * D, 32, 64);
     static unsigned long long* trace = trace_buffer("PB_ATTN_TRACE");
-    launch_k(attn_bwd_tc5_kernel, dim3(seq / BK * heads * batch), dim3(kBwdThreads), Bwd5Smem::total, s, 1, tq, tq64,
+    const int items = seq / BK * heads * batch;  // persistent: one CTA per SM walks the items
+    launch_k(attn_bwd_tc5_kernel, dim3(items < num_sms() ? items : num_sms()), dim3(kBwdThreads), Bwd5Smem::total, s, 1,
+             tq, tq64,
              td64, tdq, lse2, static_cast<const float*>(dsum), dqkv, seq, heads, T, 0.08838834764831845f, rs, rs_inv_n,
              rs_eps);
     trace_dump(trace, "attn_bwd", s);

@@ -95,7 +95,7 @@ def attn_fwd_tc(qkv, batch, seq, heads):
 
 def attn_bwd_tc(qkv, out, dout, lse2, batch, seq, heads):
     T = batch * seq
-    dsum = torch.empty(heads, T, device="cuda", dtype=torch.float32)
+    dsum = torch.empty(heads * T + 64, device="cuda", dtype=torch.float32)  # + the work counter
     dq = torch.empty(T, heads * 128, device="cuda", dtype=torch.float32)
     dqkv = torch.empty_like(qkv)
     _lib.check(_lib.lib().pbt_attn_bwd_tc(_p(qkv), _p(out), _p(dout), _f(lse2), _f(dsum), _f(dq), _p(dqkv), batch,
