@@ -34,6 +34,9 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+// EPI_F32 epilogue staging: 4 epilogue warps x 2 buffers x [32 rows][32 fp32] (128B-swizzled), drained
+// by TMA bulk reduce-adds (accumulate) or stores
+constexpr int kEpiStage = 4 * 2 * 4096;
 #ifndef PB_GEMM_SMEM_KB
 #define PB_GEMM_SMEM_KB 200  // operand ring budget (KB): 6 stages of 32 KB for the CTA-pair 256-wide tiles
 #endif
@@ -53,10 +56,13 @@ struct Cfg {
     static constexpr int kTmemCols = 2 * kAccStride;           // (power of 2)
     static_assert(BM2 == 1 || (BN == 256 && CG == 2), "BM2 = 2 is a CTA-pair 512 x 256 tile");
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    // EPI_F32: the barriers take a 1 KB slot, then the epilogue warps' fp32 staging for TMA
+    static constexpr int kSmemF32 = kStages * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ + kEpiStage;
+    static_assert(kSmemF32 <= 232448, "gemm: EPI_F32 staging over the opt-in shared memory limit");
 };
 
 struct alignas(128) GroupProblem {
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, tc;  // tc: fp32 C, box 32 x 32 (EPI_F32 epilogue)
     void* C;
     int M, N, K, ldc, tile0, ntiles, num_m, pad;
 };
@@ -85,20 +91,21 @@ struct KParams {
 struct TileRef {
     const CUtensorMap* ta;
     const CUtensorMap* tb;
+    const CUtensorMap* tc;
     void* C;
     int m_blk, n_blk, num_k, ldc;
 };
 template <int BN, int CG, int BM2 = 1>
-__device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensorMap* ta, const CUtensorMap* tb, int t,
-                                                int& cursor) {
+__device__ __forceinline__ TileRef resolve_tile(const KParams& p, const CUtensorMap* ta, const CUtensorMap* tb,
+                                                const CUtensorMap* tc, int t, int& cursor) {
     if (p.group == nullptr) {
         const int num_m = (p.M + BM * CG * BM2 - 1) / (BM * CG * BM2);  // the last M / N tile may be half empty
-        return TileRef{ta, tb, p.C, t % num_m, t / num_m, p.K / BK, p.ldc};
+        return TileRef{ta, tb, tc, p.C, t % num_m, t / num_m, p.K / BK, p.ldc};
     }
     while (t >= p.group[cursor].tile0 + p.group[cursor].ntiles) ++cursor;  // tiles visited in increasing order
     const GroupProblem& g = p.group[cursor];
     const int lt = t - g.tile0;
-    return TileRef{&g.ta, &g.tb, g.C, lt % g.num_m, lt / g.num_m, g.K / BK, g.ldc};
+    return TileRef{&g.ta, &g.tb, &g.tc, g.C, lt % g.num_m, lt / g.num_m, g.K / BK, g.ldc};
 }
 
 // Whole tiles round-robin over the persistent CTAs (pairs).
@@ -118,7 +125,8 @@ struct TileIter {
 // leader issues tcgen05.mma.cta_group::2 (M=256) and commits to both CTAs.
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, KParams p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                const __grid_constant__ CUtensorMap tma_c, KParams p) {
     using C_ = Cfg<BN, CG, BM2>;
     constexpr int kPairRows = BM * CG;  // rows of one MMA (both CTAs of a pair)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -128,6 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + C_::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // EPI_F32 staging (1 KB-aligned, after the barriers' 1 KB slot): [epilogue warp][2][32 rows][128 B]
+    uint8_t* epi_stage = smem + C_::kStages * C_::kStageBytes + 1024;
 
     const uint32_t warp = warp_id();
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             TileIter it(num_tiles, cid, ncl);
             int t;
             while (it.next(t)) {
-                const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor);
+                const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, &tma_c, t, cursor);
                 const CUtensorMap* pa = tr.ta;
                 const CUtensorMap* pb = tr.tb;
                 const int num_k = tr.num_k;
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             TileIter it(num_tiles, cid, ncl);
             int t;
             while (it.next(t)) {
-                const int num_k = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor).num_k;
+                const int num_k = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, &tma_c, t, cursor).num_k;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * C_::kAccStride;  // (BM2 = 2: sub-tile s2 at + s2 * 256)
@@ -283,13 +293,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ epilogue
         const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
         const int row_in_tile = int(q * 32 + lane_id());
+        int epi_chunk = 0;  // EPI_F32: staged blocks issued by this warp (staging buffer parity)
         int acc = 0;
         uint32_t acc_phase = 0;
         int cursor = 0;
         TileIter it(num_tiles, cid, ncl);
         int t;
         while (it.next(t)) {
-            const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, t, cursor);
+            const TileRef tr = resolve_tile<BN, CG, BM2>(p, &tma_a, &tma_b, &tma_c, t, cursor);
             const int m0 = tr.m_blk * kPairRows * BM2 + int(rank) * BM, n0 = tr.n_blk * BN;
             void* const Cout = tr.C;
             const int ldc = tr.ldc;
@@ -336,20 +347,38 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // partial last tile (M or N = 128 mod 256): nothing to store outside the matrix
                 if (!(p.group || (row < p.M && col < p.N))) continue;
                 if constexpr (EPI == EPI_F32) {
-                    float* dst = reinterpret_cast<float*>(Cout) + size_t(row) * ldc + col;
-                    float4* d4 = reinterpret_cast<float4*>(dst);
-                    if (p.accumulate) {
-                        // C += acc reduced in L2: no read round trip; one update per element per launch,
-                        // so the result is deterministic
+                    // C (+)= acc through shared memory and the TMA: the warp's 32 rows x 32 columns go to a
+                    // 128B-swizzled staging buffer (a thread writes its row: conflict-free), then one
+                    // bulk tensor reduce-add (accumulate; one update per element per launch, so the result
+                    // is deterministic) or store covers the whole 4 KB block in full 128 B lines
+                    (void)Cout;
+                    (void)ldc;
+                    uint8_t* buf = epi_stage + (q * 2 + (epi_chunk & 1)) * 4096;
+                    if (lane_id() == 0 && epi_chunk >= 2)  // this buffer's previous block has been read out
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + 4 * j),
-                                         "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<float4*>(buf + lane_id() * 128 + ((j ^ (lane_id() & 7)) << 4)) =
+                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane_id() == 0) {
+                        const int rowb = row - int(lane_id());  // the warp's first row
+                        if (p.accumulate)
+                            asm volatile(
+                                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                    reinterpret_cast<uint64_t>(tr.tc)),
+                                "r"(smem_u32(buf)), "r"(col), "r"(rowb)
+                                : "memory");
+                        else
+                            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                             reinterpret_cast<uint64_t>(tr.tc)),
+                                         "r"(smem_u32(buf)), "r"(col), "r"(rowb)
                                          : "memory");
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
+                    ++epi_chunk;
                 } else {
                     if constexpr (kAux) {
 #pragma unroll
@@ -436,6 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_arrive_cluster(map_peer(smem_u32(&tempty[acc]), 0));
             }
             if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
+        }
+        if constexpr (EPI == EPI_F32) {
+            if (lane_id() == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // staging stays valid
         }
     }
     tc_fence_before();
@@ -525,20 +557,24 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2 = 1>
 void launch(const GemmArgs& g, cudaStream_t s) {
     using C_ = Cfg<BN, CG, BM2>;
     auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, CG, BM2>;
+    constexpr int smem = EPI == EPI_F32 ? C_::kSmemF32 : C_::kSmem;
     static bool attr = [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         return true;
     }();
     (void)attr;
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, 64) : make_map(g.A, g.K, g.M, g.lda, 64, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, 64) : make_map(g.B, g.K, g.N, g.ldb, 64, C_::kBRows);
+    CUtensorMap tc{};
+    if constexpr (EPI == EPI_F32)
+        tc = make_map_t(g.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 32, 32);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
                g.rs, g.rs_inv_n, g.rs_eps, g.ss_out, g.ss_part, g.ss_cnt};
     const int tiles = ((g.M + BM * CG * BM2 - 1) / (BM * CG * BM2)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
     const int grid = (tiles < slots ? tiles : slots) * CG;
-    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, CG, ta, tb, kp);
+    launch_k(kern, dim3(grid), dim3(kThreads), smem, s, CG, ta, tb, tc, kp);
 }
 
 template <int BN, int CG, int BM2 = 1>
@@ -600,6 +636,7 @@ GemmGroup gemm_group_create(const GemmArgs* probs, int n) {
         GroupProblem& q = t[i];
         q.ta = make_map(g.A, g.M, g.K, g.lda, 64, 64);
         q.tb = make_map(g.B, g.N, g.K, g.ldb, 64, 64);
+        q.tc = make_map_t(g.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 32, 32);
         q.C = g.C;
         q.M = g.M, q.N = g.N, q.K = g.K, q.ldc = g.ldc;
         q.num_m = g.M / 256;
@@ -623,7 +660,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     using C_ = Cfg<256, 2, 1>;
     auto kern = gemm_kernel<256, true, true, EPI_F32, 2, 1>;
     static bool attr = [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemF32);
         return true;
     }();
     (void)attr;
@@ -632,7 +669,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     const int slots = sm_count() / 2;
     const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
     CUtensorMap dummy{};
-    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmem, s, 2, dummy, dummy, kp);
+    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmemF32, s, 2, dummy, dummy, dummy, kp);
 }
 
 void gemm_group_destroy(GemmGroup& g) {
