@@ -398,12 +398,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
+                    // single-output epilogues stage the bf16 block in shared memory ([32 rows][64 cols], 128B-
+                    // swizzled: two 32-column chunks) and write it with one TMA tensor store per 64 columns
+                    constexpr bool kStaged = EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU;
                     uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + size_t(row) * p.ldc + col);
+                    const int half = (c >> 5) & 1;
+                    uint8_t* sbuf = epi_stage + (q * 2 + (epi_chunk & 1)) * 4096;
+                    if constexpr (kStaged) {
+                        if (half == 0) {
+                            if (lane_id() == 0 && epi_chunk >= 2)  // this buffer's previous block has been read out
+                                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                            __syncwarp();
+                        }
+                    }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const uint4 o = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
                                                    pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
-                        d4[j] = o;
+                        if constexpr (kStaged)
+                            *reinterpret_cast<uint4*>(sbuf + lane_id() * 128 + (((half * 4 + j) ^ (lane_id() & 7)) << 4)) = o;
+                        else
+                            d4[j] = o;
                         if constexpr (EPI == EPI_RESID) {
                             if (p.ss_out) {
                                 const uint32_t w4[4] = {o.x, o.y, o.z, o.w};
@@ -413,6 +428,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     ssq = fmaf(lo, lo, fmaf(hi, hi, ssq));
                                 }
                             }
+                        }
+                    }
+                    if constexpr (kStaged) {
+                        if (half == 1) {  // the 64-column block is complete: one TMA store
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            __syncwarp();
+                            if (lane_id() == 0) {
+                                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                                 reinterpret_cast<uint64_t>(tr.tc)),
+                                             "r"(smem_u32(sbuf)), "r"(col - 32), "r"(row - int(lane_id()))
+                                             : "memory");
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
+                            ++epi_chunk;
                         }
                     }
                     if constexpr (EPI == EPI_RESID) {
@@ -466,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
         }
-        if constexpr (EPI == EPI_F32) {
+        if constexpr (EPI == EPI_F32 || EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU) {
             if (lane_id() == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // staging stays valid
         }
     }
@@ -557,7 +586,8 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2 = 1>
 void launch(const GemmArgs& g, cudaStream_t s) {
     using C_ = Cfg<BN, CG, BM2>;
     auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, CG, BM2>;
-    constexpr int smem = EPI == EPI_F32 ? C_::kSmemF32 : C_::kSmem;
+    constexpr bool staged = EPI == EPI_F32 || EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU;
+    constexpr int smem = staged ? C_::kSmemF32 : C_::kSmem;
     static bool attr = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
@@ -569,6 +599,8 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     CUtensorMap tc{};
     if constexpr (EPI == EPI_F32)
         tc = make_map_t(g.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 32, 32);
+    else if constexpr (staged)
+        tc = make_map(g.C, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 64, 32);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
                g.rs, g.rs_inv_n, g.rs_eps, g.ss_out, g.ss_part, g.ss_cnt};
     const int tiles = ((g.M + BM * CG * BM2 - 1) / (BM * CG * BM2)) * ((g.N + BN - 1) / BN);
