@@ -126,7 +126,7 @@ struct TileIter {
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                const __grid_constant__ CUtensorMap tma_c, KParams p) {
+                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_c2, KParams p) {
     using C_ = Cfg<BN, CG, BM2>;
     constexpr int kPairRows = BM * CG;  // rows of one MMA (both CTAs of a pair)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -403,11 +403,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     constexpr bool kStaged = EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU;
                     uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + size_t(row) * p.ldc + col);
                     const int half = (c >> 5) & 1;
-                    uint8_t* sbuf = epi_stage + (q * 2 + (epi_chunk & 1)) * 4096;
-                    if constexpr (kStaged) {
+                    // GELU (two outputs): u and gelu(u) blocks single-buffered in the warp's two slots
+                    uint8_t* sbuf = epi_stage + (q * 2 + (EPI == EPI_GELU ? 0 : (epi_chunk & 1))) * 4096;
+                    uint8_t* gbuf = epi_stage + (q * 2 + 1) * 4096;
+                    if constexpr (kStaged || EPI == EPI_GELU) {
                         if (half == 0) {
-                            if (lane_id() == 0 && epi_chunk >= 2)  // this buffer's previous block has been read out
-                                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                            if (lane_id() == 0 && epi_chunk >= (EPI == EPI_GELU ? 1 : 2)) {
+                                if constexpr (EPI == EPI_GELU)  // both previous stores have read their blocks
+                                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                                else  // this buffer's previous block has been read out
+                                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                            }
                             __syncwarp();
                         }
                     }
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 4; ++j) {
                         const uint4 o = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
                                                    pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
-                        if constexpr (kStaged)
+                        if constexpr (kStaged || EPI == EPI_GELU)
                             *reinterpret_cast<uint4*>(sbuf + lane_id() * 128 + (((half * 4 + j) ^ (lane_id() & 7)) << 4)) = o;
                         else
                             d4[j] = o;
@@ -452,15 +458,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if constexpr (EPI == EPI_GELU) {
                         // activation from the bf16-rounded pre-activation, as the backward sees it
-                        uint4* g4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C2) + size_t(row) * p.ldc + col);
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             float g[8];
 #pragma unroll
                             for (int e = 0; e < 8; ++e)
                                 g[e] = gelu_f(__bfloat162float(__float2bfloat16_rn(v[8 * j + e])));
-                            g4[j] = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]),
-                                               pack_bf16(g[6], g[7]));
+                            *reinterpret_cast<uint4*>(gbuf + lane_id() * 128 + (((half * 4 + j) ^ (lane_id() & 7)) << 4)) =
+                                make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]),
+                                           pack_bf16(g[6], g[7]));
+                        }
+                        if (half == 1) {  // both 64-column blocks complete: two TMA stores
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            __syncwarp();
+                            if (lane_id() == 0) {
+                                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                                 reinterpret_cast<uint64_t>(&tma_c)),
+                                             "r"(smem_u32(sbuf)), "r"(col - 32), "r"(row - int(lane_id()))
+                                             : "memory");
+                                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                                 reinterpret_cast<uint64_t>(&tma_c2)),
+                                             "r"(smem_u32(gbuf)), "r"(col - 32), "r"(row - int(lane_id()))
+                                             : "memory");
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
+                            ++epi_chunk;
                         }
                     }
                 }
@@ -495,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (++acc == C_::kAccBufs) acc = 0, acc_phase ^= 1;
         }
-        if constexpr (EPI == EPI_F32 || EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU) {
+        if constexpr (EPI == EPI_F32 || EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU || EPI == EPI_GELU) {
             if (lane_id() == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // staging stays valid
         }
     }
@@ -586,7 +608,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int CG, int BM2 = 1>
 void launch(const GemmArgs& g, cudaStream_t s) {
     using C_ = Cfg<BN, CG, BM2>;
     auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, CG, BM2>;
-    constexpr bool staged = EPI == EPI_F32 || EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU;
+    constexpr bool staged = EPI == EPI_F32 || EPI == EPI_STORE || EPI == EPI_RESID || EPI == EPI_DGELU || EPI == EPI_GELU;
     constexpr int smem = staged ? C_::kSmemF32 : C_::kSmem;
     static bool attr = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -601,12 +623,14 @@ void launch(const GemmArgs& g, cudaStream_t s) {
         tc = make_map_t(g.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 32, 32);
     else if constexpr (staged)
         tc = make_map(g.C, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 64, 32);
+    CUtensorMap tc2{};
+    if constexpr (EPI == EPI_GELU) tc2 = make_map(g.C2, uint64_t(g.N), uint64_t(g.M), uint64_t(g.ldc), 64, 32);
     KParams kp{g.M, g.N, g.K, g.C, g.C2, g.aux, g.ldc, g.ldaux, g.accumulate, nullptr, 0, 0,
                g.rs, g.rs_inv_n, g.rs_eps, g.ss_out, g.ss_part, g.ss_cnt};
     const int tiles = ((g.M + BM * CG * BM2 - 1) / (BM * CG * BM2)) * ((g.N + BN - 1) / BN);
     const int slots = sm_count() / CG;
     const int grid = (tiles < slots ? tiles : slots) * CG;
-    launch_k(kern, dim3(grid), dim3(kThreads), smem, s, CG, ta, tb, tc, kp);
+    launch_k(kern, dim3(grid), dim3(kThreads), smem, s, CG, ta, tb, tc, tc2, kp);
 }
 
 template <int BN, int CG, int BM2 = 1>
@@ -701,7 +725,7 @@ void gemm_group_run(const GemmGroup& g, cudaStream_t s) {
     const int slots = sm_count() / 2;
     const int grid = (g.total_tiles < slots ? g.total_tiles : slots) * 2;
     CUtensorMap dummy{};
-    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmemF32, s, 2, dummy, dummy, dummy, kp);
+    launch_k(kern, dim3(grid), dim3(kThreads), C_::kSmemF32, s, 2, dummy, dummy, dummy, dummy, kp);
 }
 
 void gemm_group_destroy(GemmGroup& g) {
