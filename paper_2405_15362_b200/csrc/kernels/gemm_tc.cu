@@ -324,6 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) aux_next[j] = s4[j];
             }
+            float vnext[32];  // the next 32 accumulator columns, loaded from TMEM while this chunk is processed
+            tmem_ld32(tbase, vnext);
 #pragma unroll 1
             for (int c = 0; c < BN; c += 32) {
                 uint4 aux_cur[4];
@@ -337,8 +339,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 float v[32];
-                tmem_ld32(tbase + c, v);
                 tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = vnext[e];
+                if (c + 32 < BN) tmem_ld32(tbase + c + 32, vnext);
                 if (p.rs) {  // warp-uniform: folded RMSNorm of this row
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] *= rsc;
