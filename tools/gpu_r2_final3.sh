@@ -7,6 +7,7 @@ timeout 300 python -m tests.step_breakdown 2 32 > gpurun_out/r2z_breakdown.txt 2
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 12000 -c 3200 --csv --log-file gpurun_out/r2z_launches.csv python bench.py --steps 1 --warmup 3 --microbatches 8 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'gemm_kernel|attn_|row_sumsq' -c 12 -o gpurun_out/r2z_full -f python -m tests.prof_kernels > /dev/null 2>&1
 timeout 300 python -m tests.bench_attn > gpurun_out/r2z_attn.log 2>&1
+timeout 300 python -m tests.bench_gemm 4096 > gpurun_out/r2z_gemm.log 2>&1
 for t in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize.py > gpurun_out/r2z_sanitize_$t.log 2>&1
   echo "$t rc=$?" >> gpurun_out/r2z_sanitize_$t.log; tail -2 gpurun_out/r2z_sanitize_$t.log
