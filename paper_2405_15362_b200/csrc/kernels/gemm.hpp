@@ -34,7 +34,7 @@ struct GemmArgs {
     const float* rs = nullptr;
     float rs_inv_n = 0.f, rs_eps = 0.f;
     // RESID: ss_out[row] = sum of squares of the row's stored (bf16) outputs, deterministic: every
-    // tile writes one fp32 partial per 128 columns to ss_part ([N/128][M]); the last tile to finish a
+    // tile writes one fp32 partial per 128 columns to ss_part ([M][N/128]); the last tile to finish a
     // 32-row group (ss_cnt[row / 32], zero before the launch and reset by that tile) sums the partials
     // in column order.  row_sumsq() (ops.hpp) computes the bit-identical value from a stored matrix.
     float* ss_out = nullptr;

@@ -81,7 +81,7 @@ struct KParams {
     const float* rs;
     float rs_inv_n, rs_eps;
     // EPI_RESID: ss_out[row] = sum of bf16(out)^2 over the row (the next RMSNorm's statistic), from
-    // per-128-column partials (ss_part, [N/128][M]) summed in column order by the row group's last tile
+    // per-128-column partials (ss_part, [M][N/128]) summed in column order by the row group's last tile
     float* ss_out;
     float* ss_part;
     int* ss_cnt;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if constexpr (EPI == EPI_RESID) {
                         if (p.ss_out && ((c + 32) & 127) == 0) {  // end of a 128-column chunk: its partial
-                            p.ss_part[size_t(col >> 7) * p.M + row] = ssq;
+                            p.ss_part[size_t(row) * (p.N >> 7) + (col >> 7)] = ssq;
                             ssq = 0.f;
                         }
                     }
@@ -503,7 +503,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __threadfence();
                         if (row < p.M) {
                             float sum = 0.f;
-                            for (int q = 0; q < (p.N >> 7); ++q) sum += __ldcg(p.ss_part + size_t(q) * p.M + row);
+                            const int P = p.N >> 7;  // the row's partials are contiguous: vector loads, column order
+                            const float* pr = p.ss_part + size_t(row) * P;
+                            if ((P & 3) == 0) {
+                                for (int q = 0; q < P; q += 4) {
+                                    const float4 v4 = __ldcg(reinterpret_cast<const float4*>(pr + q));
+                                    sum += v4.x;
+                                    sum += v4.y;
+                                    sum += v4.z;
+                                    sum += v4.w;
+                                }
+                            } else {
+                                for (int q = 0; q < P; ++q) sum += __ldcg(pr + q);
+                            }
                             p.ss_out[row] = sum;
                         }
                         if (lane_id() == 0) p.ss_cnt[row >> 5] = 0;
