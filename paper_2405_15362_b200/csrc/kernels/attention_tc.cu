@@ -332,11 +332,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int e2 = 0; e2 < 32; ++e2) {
                     const int c = h2 * 64 + 2 * e2;
-                    const float p0 = fast_exp2(fmaf(s[c], sl2, -m_used));
-                    const float p1 = fast_exp2(fmaf(s[c + 1], sl2, -m_used));
-                    rs8[(2 * e2) & 7] += p0;
-                    rs8[(2 * e2 + 1) & 7] += p1;
-                    pk[e2] = pack_bf16(p0, p1);
+                    const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), make_float2(sl2, sl2),
+                                                make_float2(-m_used, -m_used));
+                    // every other pair on the FMA pipe (poly_exp2x2), see kFwdEmu
+                    const float2 pv = (e2 & 1) ? poly_exp2x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                    rs8[(2 * e2) & 7] += pv.x;
+                    rs8[(2 * e2 + 1) & 7] += pv.y;
+                    pk[e2] = pack_bf16(pv.x, pv.y);
                 }
                 tmem_st32u(tmem + lane_base + 384 + (j & 1) * 64 + h2 * 32, pk);
             }
@@ -812,6 +814,12 @@ struct Fwd3Smem {
     static constexpr int total = bars + 128 + 1024;
 };
 
+// Exponentials: kFwdEmu of every 16 pairs go to the FMA pipe (poly_exp2x2), the rest to the SFU,
+// whose 16 ex2 / clk / SM otherwise match the tensor pipe's S + PV time per tile exactly.
+// Measured (tests/bench_attn.py): 0 / 4 / 6 / 8 of 16 -> 68.3 / 73.4 / 66.8 / 66.2 us at 2x2048x16,
+// 160.5 / 163.7 / 153.8 / 154.1 us at 4096x32, 468 / 467 / 458 / 460 us at 6144x48.
+constexpr int kFwdEmu = 8;
+
 __global__ void __launch_bounds__(192, 2)
     attn_fwd_tc3_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
                         float* __restrict__ lse2, int seq, int H, int T, float scale) {
@@ -911,29 +919,55 @@ __global__ void __launch_bounds__(192, 2)
             mbar_wait(s_full, j & 1);
             tc_fence_after();
             const bool diag = j == nkv - 1;
-            // pass 1: row max (8 independent chains)
+            // S read from TMEM once (all 128 columns in flight, one wait); row max and P from registers
+            float s[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + c * 32, s[c]);
+            tmem_ld_wait();  // every S column is in registers before P overwrites [0,64)
+            if (__builtin_expect(diag, 0)) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (c * 32 + e > r) s[c][e] = -INFINITY;
+            }
             float mx8[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float s[32];
-                tmem_ld32(tmem + lane_base + c * 32, s);
-                tmem_ld_wait();
-                if (__builtin_expect(diag, 0)) {
+            for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (c * 32 + e > r) s[e] = -INFINITY;
-                }
-#pragma unroll
-                for (int e = 0; e < 32; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], s[e]);
-            }
+                for (int e = 0; e < 32; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], s[c][e]);
             const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
             const float m_new = fmaxf(m_used, mx);
             const bool rescale = (j > 0) && (m_new > m_used + 8.f);
-            if (__any_sync(0xffffffff, rescale)) {  // O stable: s_full(j) implies PV(j-1) retired
-                const float f = rescale ? exp2f(m_used - m_new) : 1.f;
+            // lazy O rescale: decided here, applied to O after P is written (O is stable until
+            // p_full(j): s_full(j) implies PV(j-1) retired), so S's registers are dead by then
+            const float f = rescale ? exp2f(m_used - m_new) : 1.f;
+            if (rescale || j == 0) {
+                l *= f;
+                m_used = m_new;
+            }
+            // P = exp2(S*c - m) -> bf16 pairs over the consumed S columns [0,64)
+            float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) {  // packed f32x2 FMA / ADD (FFMA2, FADD2)
+                    const float2 x = __ffma2_rn(make_float2(s[c][2 * e2], s[c][2 * e2 + 1]), make_float2(sl2, sl2),
+                                                make_float2(-m_used, -m_used));
+                    // Bresenham spread: kFwdEmu of the 16 pairs, evenly interleaved with the SFU pairs
+                    const bool emu = (e2 * kFwdEmu) / 16 != ((e2 + 1) * kFwdEmu) / 16;
+                    const float2 pv = emu ? poly_exp2x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                    rs4[e2 & 3] = __fadd2_rn(rs4[e2 & 3], pv);
+                    pk[e2] = pack_bf16(pv.x, pv.y);
+                }
+                tmem_st16u(tmem + lane_base + c * 16, pk);
+            }
+            l += ((rs4[0].x + rs4[1].x) + (rs4[2].x + rs4[3].x)) + ((rs4[0].y + rs4[1].y) + (rs4[2].y + rs4[3].y));
+            if (__any_sync(0xffffffff, rescale)) {
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     float o[32];
@@ -943,38 +977,7 @@ __global__ void __launch_bounds__(192, 2)
                     for (int e = 0; e < 32; ++e) o[e] *= f;
                     tmem_st32(tmem + lane_base + 128 + c * 32, o);
                 }
-                tmem_st_wait();
-                if (rescale) {
-                    l *= f;
-                    m_used = m_new;
-                }
             }
-            if (j == 0) m_used = m_new;
-            // pass 2: P = exp2(S*c - m) -> bf16 pairs over the consumed S columns [0,64)
-            float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            float s[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + c * 32, s[c]);
-            tmem_ld_wait();  // every S column is in registers before P overwrites [0,64)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                if (__builtin_expect(diag, 0)) {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (c * 32 + e > r) s[c][e] = -INFINITY;
-                }
-                uint32_t pk[16];
-#pragma unroll
-                for (int e2 = 0; e2 < 16; ++e2) {  // packed f32x2 FMA / ADD (FFMA2, FADD2)
-                    const float2 x = __ffma2_rn(make_float2(s[c][2 * e2], s[c][2 * e2 + 1]), make_float2(sl2, sl2),
-                                                make_float2(-m_used, -m_used));
-                    const float2 pv = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-                    rs4[e2 & 3] = __fadd2_rn(rs4[e2 & 3], pv);
-                    pk[e2] = pack_bf16(pv.x, pv.y);
-                }
-                tmem_st16u(tmem + lane_base + c * 16, pk);
-            }
-            l += ((rs4[0].x + rs4[1].x) + (rs4[2].x + rs4[3].x)) + ((rs4[0].y + rs4[1].y) + (rs4[2].y + rs4[3].y));
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();

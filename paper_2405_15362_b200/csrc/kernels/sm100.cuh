@@ -231,6 +231,25 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// 2^x for a pair on the FMA pipe (no SFU): x = n + f with n = rint(x) (the 1.5·2^23 rounding
+// trick), 2^f on [-0.5, 0.5] by a degree-3 minimax polynomial (max rel. error 7.5e-5, far below the
+// bf16 rounding of P), and n added to the exponent field with one integer shift-add.  The SFU does
+// 16 ex2 per clock per SM on B200, which at head_dim 128 is exactly the tensor pipe's time for
+// S = QKᵀ and O += PV, so the softmax routes part of its exponentials here.  x is clamped at -126
+// (masked -inf scores then give a denormal ~1e-38, never NaN).
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+    x.x = fmaxf(x.x, -126.f);
+    x.y = fmaxf(x.y, -126.f);
+    const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+    const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), x);
+    float2 p = __ffma2_rn(make_float2(0.05517098f, 0.05517098f), f, make_float2(0.24260972f, 0.24260972f));
+    p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+    p = __ffma2_rn(p, f, make_float2(0.99992818f, 0.99992818f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
