@@ -41,6 +41,11 @@ int pbt_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const fl
 int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int32_t T, int32_t h, void* stream);
 int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, const float* rstd, const void* dres, void* dx,
                     float* dgamma, int32_t T, int32_t h, void* stream);
+/* backward of y = rstd * x with gamma folded (the executor's norm backward): dyp = rstd * dy (the dX GEMM's
+ * row-scaled output), ss = the forward row sums of squares; dx = dyp - x * mean(dyp * x) / (ss / h + eps)
+ * (+ dres when not NULL); h % 256 == 0 */
+int pbt_rmsnorm_bwd_x(const void* dyp, const void* x, const float* ss, const void* dres, void* dx, int32_t T,
+                      int32_t h, float eps, void* stream);
 int pbt_embed_fwd(const int32_t* tok, const void* emb, void* x, int32_t T, int32_t h, void* stream);
 int pbt_embed_bwd(const int32_t* tok, const void* dx, float* demb, int32_t T, int32_t h, void* stream);
 int pbt_cross_entropy(void* logits, const int32_t* labels, float* loss, int32_t T, int32_t V, float scale,

@@ -76,6 +76,13 @@ extern "C" int pbt_rmsnorm_fwd(const void* x, const void* g, void* y, float* rst
         cuda_check("pbt_rmsnorm_fwd");
     });
 }
+extern "C" int pbt_rmsnorm_bwd_x(const void* dyp, const void* x, const float* ss, const void* dres, void* dx,
+                                 int32_t T, int32_t h, float eps, void* stream) {
+    return pbx::guard([&] {
+        pbk::rmsnorm_bwd_x(BF(dyp), BF(x), ss, BF(dres), BFM(dx), T, h, eps, ST(stream));
+        cuda_check("pbt_rmsnorm_bwd_x");
+    });
+}
 extern "C" int pbt_rmsnorm_bwd(const void* dy, const void* x, const void* g, const float* rstd, const void* dres,
                                void* dx, float* dgamma, int32_t T, int32_t h, void* stream) {
     return pbx::guard([&] {

@@ -164,6 +164,57 @@ __global__ void rmsnorm_bwd_x_kernel(const __nv_bfloat16* __restrict__ dyp, cons
     reinterpret_cast<uint4*>(dx + size_t(row) * h)[c] = pack8(o);
 }
 
+// The same, one warp per row with the whole row of dy' and x held in registers (NC 16-byte chunks
+// per lane, all loads in flight before the warp-shuffle dot; no block barriers): the one-CTA-per-row
+// kernel above reached 3.8 TB/s in-step (two __syncthreads per row, one chunk per thread in flight).
+template <int NC>
+__global__ void __launch_bounds__(128) rmsnorm_bwd_x_warp_kernel(const __nv_bfloat16* __restrict__ dyp,
+                                                                 const __nv_bfloat16* __restrict__ x,
+                                                                 const float* __restrict__ ss,
+                                                                 const __nv_bfloat16* __restrict__ dres,
+                                                                 __nv_bfloat16* __restrict__ dx, int T, float eps) {
+    pdl_wait();
+    pdl_launch();
+    constexpr int h = NC * 256;
+    const int row = int(blockIdx.x) * 4 + int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    if (row >= T) return;
+    const uint4* a4 = reinterpret_cast<const uint4*>(dyp + size_t(row) * h) + lane;
+    const uint4* b4 = reinterpret_cast<const uint4*>(x + size_t(row) * h) + lane;
+    uint4 a[NC], b[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) a[k] = a4[32 * k], b[k] = b4[32 * k];
+    const float ssr = ss[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float fa[8], fb[8];
+        unpack8(a[k], fa);
+        unpack8(b[k], fb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot = fmaf(fa[i], fb[i], dot);
+    }
+    dot = warp_sum(dot);
+    const float inv_h = 1.f / float(h);
+    const float kk = dot * inv_h / (ssr * inv_h + eps);
+    const uint4* r4 = dres ? reinterpret_cast<const uint4*>(dres + size_t(row) * h) + lane : nullptr;
+    uint4* o4 = reinterpret_cast<uint4*>(dx + size_t(row) * h) + lane;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float fa[8], fb[8], o[8];
+        unpack8(a[k], fa);
+        unpack8(b[k], fb);
+        if (r4) {
+            unpack8(r4[32 * k], o);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += fa[i] - fb[i] * kk;
+        o4[32 * k] = pack8(o);
+    }
+}
+
 
 // dgamma[j] += sum_t dy[t,j] * x[t,j] * rstd[t], deterministic two-stage column reduction:
 // stage 1: thread = 8 columns x `rows_per_block` rows -> partial[row_block][h] (no atomics)
@@ -494,7 +545,11 @@ void row_sumsq(const __nv_bfloat16* x, float* ss, int T, int h, cudaStream_t s) 
 void rmsnorm_bwd_x(const __nv_bfloat16* dyp, const __nv_bfloat16* x, const float* ss, const __nv_bfloat16* dres,
                    __nv_bfloat16* dx, int T, int h, float eps, cudaStream_t s) {
     if (h % 256 || h > 8192) throw std::invalid_argument("rmsnorm: h must be a multiple of 256 and <= 8192");
-    launch_k(rmsnorm_bwd_x_kernel, dim3(T), dim3(h / 8), 0, s, 1, dyp, x, ss, dres, dx, h, eps);
+    const dim3 g4((T + 3) / 4), b4(128);
+    if (h == 2048)  // wider rows spill the register-held row (ptxas: 255 regs + stack at h = 4096)
+        launch_k(rmsnorm_bwd_x_warp_kernel<8>, g4, b4, 0, s, 1, dyp, x, ss, dres, dx, T, eps);
+    else
+        launch_k(rmsnorm_bwd_x_kernel, dim3(T), dim3(h / 8), 0, s, 1, dyp, x, ss, dres, dx, h, eps);
 }
 
 void rmsnorm_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd, float* dgamma, float* scratch,

@@ -64,6 +64,13 @@ def rmsnorm_bwd(dy, x, g, rstd, dres=None, dgamma=None):
     return dx
 
 
+def rmsnorm_bwd_x(dyp, x, ss, dres=None, eps=1e-5):
+    T, h = x.shape
+    dx = torch.empty_like(x)
+    _lib.check(_lib.lib().pbt_rmsnorm_bwd_x(_p(dyp), _p(x), _f(ss), _p(dres), _p(dx), T, h, C.c_float(eps), _s()))
+    return dx
+
+
 def embed_fwd(tok, emb):
     T, h = tok.numel(), emb.shape[1]
     x = torch.empty(T, h, device="cuda", dtype=torch.bfloat16)

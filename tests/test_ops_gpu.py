@@ -150,6 +150,29 @@ def test_attention_forward_tcgen05_rescales():
     assert ((got_lse - lse).abs() / lse.abs().clamp_min(1)).max().item() < 1e-2
 
 
+@pytest.mark.parametrize("h", [1024, 2048, 4096])
+@pytest.mark.parametrize("with_dres", [False, True])
+def test_rmsnorm_bwd_folded(h, with_dres):
+    """The executor's norm backward (gamma folded, dy' = rstd * dy from the dX GEMM) vs torch fp32
+    autograd of y = x * rsqrt(mean(x^2) + eps); h = 2048 takes the warp-per-row kernel, T = 77 a ragged tail."""
+    g = torch.Generator(device="cuda").manual_seed(h + with_dres)
+    T, eps = 77, 1e-5
+    x = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    dres = torch.randn(T, h, device="cuda", generator=g).bfloat16() if with_dres else None
+    xf = x.float().requires_grad_(True)
+    ss = (xf.detach() ** 2).sum(-1)
+    rstd = torch.rsqrt(ss / h + eps)
+    y = xf * torch.rsqrt((xf ** 2).mean(-1, keepdim=True) + eps)
+    (ref,) = torch.autograd.grad(y, xf, dy.float())
+    if with_dres:
+        ref = ref + dres.float()
+    dyp = (dy.float() * rstd[:, None]).bfloat16()
+    got = K.rmsnorm_bwd_x(dyp, x, ss.contiguous(), dres, eps)
+    torch.cuda.synchronize()
+    assert rel(got, ref) < 1e-2
+
+
 @pytest.mark.parametrize("h", [1024, 2048])
 def test_rmsnorm_unit_gamma(h):
     """g = NULL (gamma folded into the next projection) equals g = 1."""
