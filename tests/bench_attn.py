@@ -49,6 +49,18 @@ def sdpa_times(batch, seq, heads, backend):
 
 
 def main():
+    # two passes over the shapes, the second one reported: the first shape of a fresh process reads
+    # 10-20 % slow for both arms
+    for rep in range(2):
+        rows = measure(quiet=rep == 0)
+    if len(sys.argv) > 1:
+        with open(sys.argv[1], "w") as f:
+            json.dump({"gpu": torch.cuda.get_device_name(0), "def": "causal FLOPs: fwd 2*s^2*h per sequence, bwd 2.5x; "
+                       "median of 20 CUDA-event timings per kernel, launched alone; second pass over the shapes",
+                       "rows": rows}, f, indent=1)
+
+
+def measure(quiet):
     rows = []
     for batch, seq, heads in SHAPES:
         qkv = torch.randn(batch * seq, 3 * heads * 128, device="cuda").bfloat16()
@@ -71,11 +83,9 @@ def main():
             row["fwd_vs_best_sdpa"] = row["fwd_tflops"] / max(b["fwd_tflops"] for b in best)
             row["bwd_vs_best_sdpa"] = row["bwd_tflops"] / max(b["bwd_tflops"] for b in best)
         rows.append(row)
-        print(json.dumps(row), flush=True)
-    if len(sys.argv) > 1:
-        with open(sys.argv[1], "w") as f:
-            json.dump({"gpu": torch.cuda.get_device_name(0), "def": "causal FLOPs: fwd 2*s^2*h per sequence, bwd 2.5x; "
-                       "median of 20 CUDA-event timings per kernel, launched alone", "rows": rows}, f, indent=1)
+        if not quiet:
+            print(json.dumps(row), flush=True)
+    return rows
 
 
 if __name__ == "__main__":
