@@ -95,7 +95,7 @@ def test_embedding():
     assert rel(demb, ref) < 1e-6
 
 
-@pytest.mark.parametrize("T,V", [(64, 1024), (256, 50304), (16, 65536)])  # 65536: the streaming (non-register) path
+@pytest.mark.parametrize("T,V", [(64, 1024), (256, 50304), (16, 65536)])  # 65536: a vocabulary above the GPT ones
 def test_cross_entropy(T, V):
     g = torch.Generator(device="cuda").manual_seed(T)
     z = (3 * torch.randn(T, V, device="cuda", generator=g)).bfloat16()
