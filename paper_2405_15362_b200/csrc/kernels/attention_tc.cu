@@ -804,8 +804,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // Per CTA and key tile j:  S(j) = Q K(j)^T -> softmax (thread = query row; P written back over S as
 // bf16 pairs) -> O += P(j) V(j) (A = P from TMEM).  The MMA pipe runs in issue order, so S(j+1)
 // overwrites P(j) only after PV(j) has read it, and when s_full(j) completes PV(j-1) has too (the
-// lazy O rescale needs no extra wait).  The softmax reads S twice (max pass, exp pass) instead of
-// holding 128 scores in registers, which keeps the kernel under 168 registers for 2 CTAs / SM.
+// lazy O rescale needs no extra wait).  The softmax reads S from TMEM once (128 scores per thread in
+// registers: 166 registers, under the 168 that two CTAs / SM allow) and applies the O rescale after
+// P is written, when the scores' registers are free.
 struct Fwd3Smem {
     static constexpr int q = 0;
     static constexpr int k = kTile;
