@@ -150,6 +150,21 @@ def test_attention_forward_tcgen05_rescales():
     assert ((got_lse - lse).abs() / lse.abs().clamp_min(1)).max().item() < 1e-2
 
 
+@pytest.mark.parametrize("batch,seq,heads", [(2, 2048, 16), (1, 1024, 2)])  # v3 (two CTAs / SM) and v1 grids
+def test_attention_forward_extreme_scores(batch, seq, heads):
+    """Scores of magnitude ~1e2-1e3 in log2 units: most exponentials underflow, including the ones the
+    FMA-pipe polynomial computes (its argument is clamped at -126), and the lazy rescale fires often."""
+    g = torch.Generator(device="cuda").manual_seed(31 + seq)
+    qkv = (12 * torch.randn(batch * seq, 3 * heads * 128, device="cuda", generator=g)).bfloat16()
+    out, lse2 = K.attn_fwd_tc(qkv, batch, seq, heads)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse2).all()
+    ref, lse = ref_attention(qkv, batch, seq, heads)
+    assert rel(out, ref) < 1e-2
+    got_lse = (lse2 * math.log(2)).view(heads, batch, seq).permute(1, 0, 2)
+    assert ((got_lse - lse).abs() / lse.abs().clamp_min(1)).max().item() < 1e-2
+
+
 @pytest.mark.parametrize("h", [1024, 2048, 4096])
 @pytest.mark.parametrize("with_dres", [False, True])
 def test_rmsnorm_bwd_folded(h, with_dres):
