@@ -817,9 +817,11 @@ struct Fwd3Smem {
 
 // Exponentials: kFwdEmu of every 16 pairs go to the FMA pipe (poly_exp2x2), the rest to the SFU,
 // whose 16 ex2 / clk / SM otherwise match the tensor pipe's S + PV time per tile exactly.
-// Measured (tests/bench_attn.py): 0 / 4 / 6 / 8 of 16 -> 68.3 / 73.4 / 66.8 / 66.2 us at 2x2048x16,
-// 160.5 / 163.7 / 153.8 / 154.1 us at 4096x32, 468 / 467 / 458 / 460 us at 6144x48.
-constexpr int kFwdEmu = 8;
+// Measured (tests/bench_attn.py), two-pass softmax: 0 / 4 / 6 / 8 of 16 -> 68.3 / 73.4 / 66.8 / 66.2 us at
+// 2x2048x16, 160.5 / 163.7 / 153.8 / 154.1 us at 4096x32, 468 / 467 / 458 / 460 us at 6144x48; with the
+// single-read softmax: 4 / 6 / 8 / 10 / 12 of 16 -> 62.7 / 62.4 / 62.5 / 66.8 / 68.9 us, 147.7 / 148.1 /
+// 149.8 / 158.0 / 173.1 us, 449 / 451 / 460 / 474 / 515 us.
+constexpr int kFwdEmu = 4;
 
 __global__ void __launch_bounds__(192, 2)
     attn_fwd_tc3_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
