@@ -59,6 +59,7 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dout, cons
     pdl_launch();
     const int t = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 4
     for (int head = warp; head < H; head += blockDim.x >> 5) {
         const size_t off = size_t(t) * H * D + head * D + lane * 4;
         uint2 a = *reinterpret_cast<const uint2*>(dout + off);
@@ -81,6 +82,7 @@ __global__ void attn_dq_store_kernel(const float* __restrict__ dq_acc, __nv_bflo
     pdl_launch();
     const int t = blockIdx.x;
     const float f = rs ? scale * rsqrtf(rs[t] * rs_inv_n + rs_eps) : scale;
+#pragma unroll 4  // the row's loads in flight together (one at a time: 4.8 TB/s under ncu)
     for (int c = threadIdx.x * 4; c < H * D; c += blockDim.x * 4) {
         float4 v = *reinterpret_cast<const float4*>(dq_acc + size_t(t) * H * D + c);
         uint2 o = make_uint2(pack_bf16(v.x * f, v.y * f), pack_bf16(v.z * f, v.w * f));
