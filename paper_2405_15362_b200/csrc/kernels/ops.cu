@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
     uint4* z4 = reinterpret_cast<uint4*>(z);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float m = -INFINITY;
+#pragma unroll 4  // four chunks' loads in flight per thread
     for (int c = threadIdx.x; c < nch; c += blockDim.x) {
         float f[8];
         unpack8(z4[c], f);
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
     m = red[0];
     __syncthreads();
     float s = 0.f;
+#pragma unroll 4  // four chunks' loads in flight per thread
     for (int c = threadIdx.x; c < nch; c += blockDim.x) {
         float f[8];
         unpack8(z4[c], f);
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(512) ce_kernel(__nv_bfloat16* __restrict__ log
     const float inv = 1.f / s;
     // folded final RMSNorm: dlogits' = rstd_f * dlogits (the head's dX and dW GEMMs then use x, not x-hat)
     const float gsc = rs ? scale * rsqrtf(rs[row] * rs_inv_n + rs_eps) : scale;
+#pragma unroll 4  // four chunks' loads in flight per thread
     for (int c = threadIdx.x; c < nch; c += blockDim.x) {
         float f[8];
         unpack8(z4[c], f);
